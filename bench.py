@@ -1,0 +1,341 @@
+"""Benchmark: spin-flip attempts/s of the PT Metropolis sampling loop.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c3|c1|c2|c4|c5]
+
+Workload (default, BASELINE.json configs[2], the config the metric's target is
+quoted on): 2D Ising 1024^2, 256 replicas, linear ladder 1+3i/R, J=1, B=0,
+exchange every 10 sweeps.  A step = one exchange interval = 10 checkerboard
+sweeps of every replica + one swap round (energies from the fused reduction,
+reference swap rule).  Attempts per step = R * L^2 * 10.
+
+* value: device-resident, CUDA events around each step, L2 flushed between
+  steps (256 MiB write), max over ranks.
+* e2e: the host-buffer plugin call (kernels.cb_interval -> C ABI
+  ptmh_host_cb_interval) on pinned int8 lattices, host<->device copies of the
+  lattices inside the timed region, pipelined against the sweeps.
+* roofline: the half-sweep kernel, algorithmic bytes = 0.25 B per attempt
+  (1-bit spin read + written) x R*L^2/2 attempts per launch,
+  over its CUDA-event duration inside the timed steps.
+* cpu_baseline / --impl reference: the reference's own algorithm (random-site
+  chain, kernels.py:62-113) restated in C (oracle/, "port") on all host cores
+  over a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (L, R, sweeps per exchange interval, description)
+    "c1": (32, 8, 1, "2D Ising 32x32, 8 replicas, geometric T-ladder, exchange every sweep"),
+    "c2": (256, 64, 1, "2D Ising 256x256, 64 replicas, exchange every sweep"),
+    "c3": (1024, 256, 10, "2D Ising 1024x1024, 256 replicas, exchange every 10 sweeps"),
+    "c4": (4096, 512, 10, "2D Ising 4096x4096, 512 replicas, exchange every 10 sweeps"),
+    "c5": (64, 4096, 1, "2D Ising 64x64, 4096 replicas, exchange every sweep"),
+}
+SEED = 42
+ALG_BYTES_PER_ATTEMPT = 0.25  # 1-bit multispin coding: read + write one bit
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback"
+
+
+def _traffic(cfg_name):
+    """dram bytes per half-sweep launch from the committed ncu --set full
+    capture summary (profiles/), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_sweep_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        ent = d.get(cfg_name)
+        return None if ent is None else float(ent["dram_bytes_per_launch"])
+    except Exception:  # noqa: BLE001
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------ CPU reference --
+def cpu_reference_rate(L, R, attempts_per_slot, threads, reps=1):
+    """Reference random-site chain (oracle C port of kernels.py:62-113,
+    executor.py:227-245 worker pool) on `threads` host cores; returns
+    (attempts/s, attempts, seconds)."""
+    import oracle
+
+    rs = np.random.default_rng(SEED)
+    spins = (rs.integers(0, 2, size=(R, L, L)) * 2 - 1).astype(np.int8)
+    betas = 1.0 / oracle.build_ladder(R)
+    energies = np.array([oracle.lattice_energy(spins[r], 1.0, 0.0) for r in range(R)])
+    sums = spins.reshape(R, -1).sum(axis=1).astype(np.int64)
+    s2r = np.arange(R, dtype=np.int64)
+    pos = np.full(R, L * L - 1, dtype=np.uint64)
+    iters = np.zeros(R, dtype=np.int64)
+    oracle.advance_block_mt(spins, s2r, betas, 1.0, 0.0, energies, sums, pos, iters, SEED, 1,
+                            max(1, attempts_per_slot // 100), threads)  # warm
+    best = None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        oracle.advance_block_mt(spins, s2r, betas, 1.0, 0.0, energies, sums, pos, iters, SEED,
+                                1, attempts_per_slot, threads)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    n = R * attempts_per_slot
+    return n / best, n, best
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:  # noqa: BLE001
+        return os.cpu_count() or 1
+
+
+# --------------------------------------------------------------------- main --
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    L, R, every, desc = CONFIGS[args.config]
+    attempts_per_step = R * L * L * every
+    config = {"workload": desc, "side": L, "replicas": R, "sweeps_per_step": every,
+              "attempts_per_step": attempts_per_step, "J": 1.0, "B": 0.0,
+              "ladder": "geometric 4^(i/(R-1))" if args.config == "c1" else "linear 1+3i/R",
+              "sweep": "checkerboard, 1-bit multispin", "l2": "flushed between steps (256 MiB write)",
+              "parallelism": f"rows sharded over {world} GPU(s), energies all-gathered"}
+    metric = "spin-flip attempts/sec"
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        threads = host_cores()
+        per_slot = max(1000, int(2.5e7 // R))  # ~1 s of 8-core work per step
+        for _ in range(args.warmup):
+            cpu_reference_rate(min(L, 256), R, per_slot // 10, threads)
+        times = []
+        spins_L = L
+        for _ in range(args.steps):
+            rate, n, dt = cpu_reference_rate(spins_L, R, per_slot, threads)
+            times.append(dt)
+        tot = sum(times)
+        val = args.steps * R * per_slot / tot
+        line = {"metric": metric, "value": val, "unit": "attempts/s", "n_gpus": 0, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+                "scaling": "none", "vs_baseline": None, "dtype": "int8/f64", "data": "synthetic",
+                "impl": "reference", "config": config,
+                "cpu_baseline": {"value": val, "unit": "attempts/s", "cores": threads, "kind": "port",
+                                 "sample": f"{R} slots x {per_slot} random-site attempts per step "
+                                           f"(reference chain kernels.py:62-113, C port, "
+                                           f"{threads} threads)"},
+                "e2e": {"value": val, "unit": "attempts/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_03825_b200 import geometric_ladder, build_ladder, kernels
+    from paper_2512_03825_b200.distributed import ShardedCheckerboard
+    from paper_2512_03825_b200.engine import CheckerboardEngine
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    temps = geometric_ladder(R) if args.config == "c1" else build_ladder(R)
+    if world > 1:
+        drv = ShardedCheckerboard(L, R, temps, SEED, device=local_rank)
+        eng = drv.eng
+        drv.init_state()
+    else:
+        drv = None
+        eng = CheckerboardEngine(L, R, temps, SEED, 1.0, 0.0, 0.5, local_rank)
+        eng.init_state()
+    torch.cuda.synchronize()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    state = {"sweep": 0, "round": 0}
+
+    def step(sweep_events=None):
+        t0 = state["sweep"]
+        if sweep_events is None:
+            eng.sweeps(t0, every)
+        else:
+            for k in range(every):
+                a, b = sweep_events[k]
+                a.record(stream)
+                eng.sweeps(t0 + k, 1)
+                b.record(stream)
+        if drv is not None:
+            drv.gather_stats()
+        eng.exchange(state["round"])
+        state["sweep"] += every
+        state["round"] += 1
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    step_ms, sweep_ms = [], []
+    with ClockSampler(local_rank) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in range(every)]
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            s0.record(stream)
+            step(ev)
+            s1.record(stream)
+            torch.cuda.synchronize()
+            step_ms.append(s0.elapsed_time(s1))
+            sweep_ms.extend(a.elapsed_time(b) for a, b in ev)
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = args.steps * attempts_per_step / (total_ms / 1e3)
+    launch_ms = statistics.mean(sweep_ms) / 2.0  # two colour launches per sweep
+    local_rows = eng.rows
+    bytes_per_launch = ALG_BYTES_PER_ATTEMPT * local_rows * L * L / 2
+    achieved = bytes_per_launch / (launch_ms / 1e3) / 1e9
+    peak, peak_kind = _peaks()
+    traffic = _traffic(args.config) if world == 1 else None
+
+    # ---- end to end through the host-buffer plugin (rank 0, single device)
+    e2e = None
+    if not args.no_e2e and world == 1:
+        spins_h = eng.final_spins()
+        pinned = torch.from_numpy(spins_h).pin_memory()
+        sp = pinned.numpy()
+        s2r = eng.slot_to_row.cpu().numpy().copy()
+        betas = 1.0 / temps
+        e = np.zeros(R)
+        ss = np.zeros(R, dtype=np.int64)
+        sweep0, rnd0 = state["sweep"], state["round"]
+        for k in range(2):  # warm the workspace
+            kernels.cb_interval(sp, s2r, betas, 1.0, 0.0, SEED, sweep0, every, rnd0, e, ss)
+            sweep0 += every
+            rnd0 += 1
+        n_e2e = max(3, min(args.steps, 10))
+        t0 = time.perf_counter()
+        for k in range(n_e2e):
+            kernels.cb_interval(sp, s2r, betas, 1.0, 0.0, SEED, sweep0, every, rnd0, e, ss)
+            sweep0 += every
+            rnd0 += 1
+        dt = time.perf_counter() - t0
+        e2e = {"value": n_e2e * attempts_per_step / dt, "unit": "attempts/s",
+               "h2d_bytes_per_step": int(R * L * L + R * 8 + R * 40 + R * 4 + R * 8),
+               "d2h_bytes_per_step": int(R * L * L + R * 8 * 3 + 16),
+               "path": "kernels.cb_interval -> ptmh_host_cb_interval (pinned int8 lattices)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = host_cores()
+        per_slot = max(1000, int(1.5e8 // R))
+        rate, n, dt = cpu_reference_rate(L, R, per_slot, threads)
+        cpu = {"value": rate, "unit": "attempts/s", "cores": threads, "kind": "port",
+               "sample": f"{R} slots x {per_slot} random-site attempts on {L}^2 lattices "
+                         f"({n:.3g} attempts, {dt:.1f} s; reference chain kernels.py:62-113 "
+                         f"in C, {threads} threads)"}
+
+    if rank == 0:
+        line = {"metric": metric, "value": value, "unit": "attempts/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "u32 (1-bit spins), integer RNG", "data": "synthetic (seeded exact-count init)",
+                "config": config,
+                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                             "frac": achieved / peak, "traffic": traffic,
+                             "kernel": "cb_half_sweep_fast", "launch_ms": launch_ms,
+                             "alg_bytes_per_launch": bytes_per_launch, "peak_kind": peak_kind,
+                             "note": "issue-bound (Philox + bit-sliced logic), see DESIGN.md 5"},
+                "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": args.steps * (2 * every + 2),
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,168 @@
+/*
+ * ptmh.h -- C ABI of the B200 Parallel-Tempering Metropolis engine.
+ *
+ * Plain C types only.  Two groups of entry points:
+ *
+ *  (A) Host-buffer entry points, ptmh_host_*: exactly the reference's kernel
+ *      boundary.  The reference executor calls the numba kernels in
+ *      isingpt/kernels.py as module attributes (executor.py:23,204-206,
+ *      218-220,241-245,258-260) on caller-owned, C-contiguous host arrays
+ *      that the kernels mutate in place.  Each ptmh_host_* function takes
+ *      the same arrays (host pointers + shapes), copies them to the device,
+ *      runs the CUDA kernel and copies the results back, so a ctypes binding
+ *      can be installed as isingpt.kernels.<name>.
+ *
+ *  (B) Device-resident entry points: the same operations on device pointers
+ *      (torch-allocated), asynchronous on the given cudaStream_t, plus the
+ *      checkerboard (Mode F) sweep, pack/unpack and observable kernels.  The
+ *      engine (paper_2512_03825_b200/engine.py) keeps every replica's state
+ *      in HBM for the whole run and only calls these.
+ *
+ * Conventions: every function returns 0 (PTMH_OK) or a negative code;
+ * ptmh_last_error() returns the message of the calling thread's last error.
+ * No device function allocates or synchronises except the ptmh_host_* ones.
+ */
+#ifndef PTMH_H_
+#define PTMH_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PTMH_OK 0
+#define PTMH_ERR_ARG (-1)
+#define PTMH_ERR_CUDA (-2)
+
+#define PTMH_ABI_VERSION 1
+
+int ptmh_abi_version(void);
+const char *ptmh_last_error(void);
+
+/* ------------------------------------------------ (A) host-buffer ABI -- */
+
+/* isingpt/kernels.py:26-27 fill_lattice(out, up_count, seed, stream, position)
+ * -> new position.  out: int8 host array of n sites (any 2D shape). */
+int ptmh_host_fill_lattice(int8_t *out, int64_t n, int64_t up_count,
+                           uint64_t seed, uint64_t stream, uint64_t position,
+                           uint64_t *new_position);
+
+/* isingpt/kernels.py:48-49 lattice_energy(spins, J, B) -> float.
+ * spins: int8 host (L, L). */
+int ptmh_host_lattice_energy(const int8_t *spins, int64_t L, double J, double B,
+                             double *energy);
+
+/* isingpt/kernels.py:62-65 advance_block(spins, slot_to_row, lo, hi, betas, J,
+ * B, energies, spin_sums, positions, iters_done, seed, start_iter, nsteps,
+ * obs_e, obs_m, record, states).
+ *   spins (rows, L, L) int8; slot_to_row/betas/energies/spin_sums/positions/
+ *   iters_done: R entries; obs_e/obs_m (R, ncols) f64 (ignored if record==0);
+ *   states (R, ncols, L, L) int8 (only if record==2). */
+int ptmh_host_advance_block(int8_t *spins, int64_t rows, int64_t L,
+                            const int64_t *slot_to_row, int64_t R, int64_t lo,
+                            int64_t hi, const double *betas, double J, double B,
+                            double *energies, int64_t *spin_sums,
+                            uint64_t *positions, int64_t *iters_done,
+                            uint64_t seed, int64_t start_iter, int64_t nsteps,
+                            double *obs_e, double *obs_m, int64_t ncols,
+                            int record, int8_t *states);
+
+/* isingpt/kernels.py:116-118 swap_chunk(slot_to_row, energies, spin_sums,
+ * betas, seed, stream_base, round_index, first, pair_lo, pair_hi) -> int. */
+int ptmh_host_swap_chunk(int64_t *slot_to_row, double *energies,
+                         int64_t *spin_sums, const double *betas, int64_t R,
+                         uint64_t seed, int64_t stream_base,
+                         int64_t round_index, int64_t first, int64_t pair_lo,
+                         int64_t pair_hi, int64_t *accepted);
+
+/* Checkerboard interval on host lattices (Mode F): the
+ * plugin call bench.py times end to end.  Copies the int8 lattices
+ * (rows, L, L) in, runs n_sweeps checkerboard sweeps starting at global
+ * sweep first_sweep and -- if round_index >= 0 -- one swap round with the
+ * reference rule, and copies the lattices, slot_to_row (R), by-slot
+ * energies / spin sums (R) back.  Copies are pipelined over replica chunks
+ * against the sweeps.  rows == R (single device). */
+int ptmh_host_cb_interval(int8_t *spins, int64_t R, int64_t L,
+                          int64_t *slot_to_row, const double *betas, double J,
+                          double B, uint64_t seed, int64_t first_sweep,
+                          int64_t n_sweeps, int64_t round_index,
+                          double *energies, int64_t *spin_sums,
+                          int64_t *accepted);
+
+/* ---------------------------------------- (B) device-resident ABI ------ */
+
+/* fill_lattice for rows [0, rows): row r uses stream stream0 + r from
+ * position pos0 (executor.py:203-205).  spins: device (rows, L, L) int8. */
+int ptmh_fill_lattices(int8_t *spins, int64_t rows, int64_t L,
+                       int64_t up_count, uint64_t seed, uint64_t stream0,
+                       uint64_t pos0, void *stream);
+
+/* stats[2r] = sum(s), stats[2r+1] = sum(s*(down+right)) of each int8 lattice
+ * (the integer accumulators of kernels.py:48-59). */
+int ptmh_row_stats(const int8_t *spins, int64_t rows, int64_t L,
+                   int64_t *stats, void *stream);
+
+/* advance_block on device arrays.  The acceptance exponentials are built on
+ * the host with the reference's own expression and libm exp:
+ *   dcls[c]      = 2.0*s*(J*nb - B),  c = 5*(s>0) + (nb+4)/2   (10 classes)
+ *   tbl[k*10+c]  = exp(-betas[k]*dcls[c])                      (R x 10)
+ * int_energy != 0 allows order-free energy accumulation (integer J, B). */
+int ptmh_advance_block(int8_t *spins, int64_t L, const int64_t *slot_to_row,
+                       int64_t lo, int64_t hi, const double *tbl,
+                       const double *dcls, int int_energy, double *energies,
+                       int64_t *spin_sums, uint64_t *positions,
+                       int64_t *iters_done, uint64_t seed, int64_t start_iter,
+                       int64_t nsteps, double *obs_e, double *obs_m,
+                       int64_t ncols, int record, int8_t *states, void *stream);
+
+/* swap_chunk on device arrays; accepted[0] += accepted pairs, near_ties[0] +=
+ * decisions with |u - p| <= 4 ulp(p) (device exp vs host libm guard band).
+ * If row_to_slot is non-NULL it is rebuilt from slot_to_row afterwards. */
+int ptmh_swap_chunk(int64_t *slot_to_row, double *energies, int64_t *spin_sums,
+                    const double *betas, int64_t R, uint64_t seed,
+                    int64_t stream_base, int64_t round_index, int64_t first,
+                    int64_t pair_lo, int64_t pair_hi, int64_t *accepted,
+                    int64_t *near_ties, int32_t *row_to_slot, void *stream);
+
+/* Checkerboard (Mode F) storage: per lattice, colour c in {0,1}, half-lattice
+ * site h = i*(L/2) + (j>>1) of colour (i+j)&1 is bit (h & 31) of word
+ * packed[(row*2 + c)*W + (h >> 5)], W = ceil(L*L/64); bit set <=> spin +1. */
+int64_t ptmh_cb_words_per_color(int64_t L);
+int ptmh_cb_pack(const int8_t *spins, int64_t rows, int64_t L, uint32_t *packed,
+                 void *stream);
+int ptmh_cb_unpack(const uint32_t *packed, int64_t rows, int64_t L,
+                   int8_t *spins, void *stream);
+
+/* n_sweeps checkerboard sweeps (colour 0 then 1) of rows [0, rows) starting
+ * at global sweep first_sweep.  Row r is at slot row_to_slot[r] (global slot
+ * index; row_offset is the global index of local row 0, unused by the
+ * kernel but kept for sharded callers).  thresh: (R, 10) uint32, always_mask:
+ * the classes with dE <= 0.  stats (rows, 2) int64 is updated incrementally
+ * (fused reduction). */
+int ptmh_cb_sweeps(uint32_t *packed, int64_t rows, int64_t L,
+                   const int32_t *row_to_slot, const uint32_t *thresh,
+                   uint32_t always_mask, uint64_t seed, int64_t first_sweep,
+                   int64_t n_sweeps, int64_t *stats, void *stream);
+
+/* Per-lattice (S, Bond) recomputed from the packed state (audit of the
+ * incremental stats; L % 64 == 0 or any even L). */
+int ptmh_cb_row_stats(const uint32_t *packed, int64_t rows, int64_t L,
+                      int64_t *stats, void *stream);
+
+/* energies[k] = B*S - J*Bond and spin_sums[k] = S of lattice slot_to_row[k]
+ * (lattice.py:61-65), for k in [0, R).  stats_all holds every lattice. */
+int ptmh_cb_slot_energies(const int64_t *stats_all, const int64_t *slot_to_row,
+                          int64_t R, double J, double B, double *energies,
+                          int64_t *spin_sums, void *stream);
+
+/* obs_e[k*ncols + col] = energy of slot k, obs_m[...] = S / L^2. */
+int ptmh_cb_observe(const int64_t *stats_all, const int64_t *slot_to_row,
+                    int64_t R, int64_t L, double J, double B, double *obs_e,
+                    double *obs_m, int64_t ncols, int64_t col, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PTMH_H_ */

@@ -1,0 +1,73 @@
+"""ctypes binding of libptmh.so (include/ptmh.h).
+
+The CUDA library is the product: there is no CPU fallback.  Importing this
+module raises if the library is missing, and every call raises
+``PtmhError`` on a non-zero return code.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libptmh.so")
+
+
+class PtmhError(RuntimeError):
+    """A libptmh call returned an error code."""
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+            f"g.build()'` (nvcc, sm_100a). There is no CPU fallback.")
+    lib = ctypes.CDLL(LIB_PATH)
+    P = ctypes.c_void_p
+    i64, u64, f64, i32, u32 = (ctypes.c_int64, ctypes.c_uint64, ctypes.c_double,
+                               ctypes.c_int, ctypes.c_uint32)
+    sigs = {
+        "ptmh_abi_version": ([], i32),
+        "ptmh_last_error": ([], ctypes.c_char_p),
+        # host-buffer ABI (isingpt/kernels.py boundary)
+        "ptmh_host_fill_lattice": ([P, i64, i64, u64, u64, u64, P], i32),
+        "ptmh_host_lattice_energy": ([P, i64, f64, f64, P], i32),
+        "ptmh_host_advance_block": ([P, i64, i64, P, i64, i64, i64, P, f64, f64, P, P, P, P,
+                                     u64, i64, i64, P, P, i64, i32, P], i32),
+        "ptmh_host_swap_chunk": ([P, P, P, P, i64, u64, i64, i64, i64, i64, i64, P], i32),
+        "ptmh_host_cb_interval": ([P, i64, i64, P, P, f64, f64, u64, i64, i64, i64, P, P, P],
+                                  i32),
+        # device-resident ABI
+        "ptmh_fill_lattices": ([P, i64, i64, i64, u64, u64, u64, P], i32),
+        "ptmh_row_stats": ([P, i64, i64, P, P], i32),
+        "ptmh_advance_block": ([P, i64, P, i64, i64, P, P, i32, P, P, P, P, u64, i64, i64,
+                                P, P, i64, i32, P, P], i32),
+        "ptmh_swap_chunk": ([P, P, P, P, i64, u64, i64, i64, i64, i64, i64, P, P, P, P], i32),
+        "ptmh_cb_words_per_color": ([i64], i64),
+        "ptmh_cb_pack": ([P, i64, i64, P, P], i32),
+        "ptmh_cb_unpack": ([P, i64, i64, P, P], i32),
+        "ptmh_cb_sweeps": ([P, i64, i64, P, P, u32, u64, i64, i64, P, P], i32),
+        "ptmh_cb_row_stats": ([P, i64, i64, P, P], i32),
+        "ptmh_cb_slot_energies": ([P, P, i64, f64, f64, P, P, P], i32),
+        "ptmh_cb_observe": ([P, P, i64, i64, f64, f64, P, P, i64, i64, P], i32),
+    }
+    for name, (args, res) in sigs.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    return lib, sorted(sigs)
+
+
+LIB, EXPORTED = _load()
+ABI_VERSION = LIB.ptmh_abi_version()
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = LIB.ptmh_last_error().decode(errors="replace")
+        raise PtmhError(f"{what} failed (rc={rc}): {msg}")
+
+
+def call(name: str, *args) -> None:
+    check(getattr(LIB, name)(*args), name)

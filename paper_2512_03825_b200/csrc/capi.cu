@@ -1,0 +1,409 @@
+// capi.cu -- extern "C" entry points declared in include/ptmh.h.
+//
+// (B) device-resident wrappers forward to the launchers in exact.cu /
+// checkerboard.cu.  (A) host-buffer entry points reproduce the reference's
+// kernel boundary (isingpt/kernels.py) on caller-owned host arrays: they
+// stage the arrays in a grow-only device workspace, launch, and copy back.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "launchers.cuh"
+
+namespace ptmh {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+// ------------------------------------------------- host-side table builders --
+// dE per class written as the reference writes it (kernels.py:94), and the
+// acceptance exponentials with the host libm exp (kernels.py:98).
+static double class_delta(int cls, double J, double B) {
+    const double s = cls >= 5 ? 1.0 : -1.0;
+    const double nb = (double)(2 * (cls % 5) - 4);
+    return 2.0 * s * (J * nb - B);
+}
+
+static void exact_tables(const double* betas, int64_t R, double J, double B, std::vector<double>& tbl,
+                         std::vector<double>& dcls) {
+    dcls.resize(10);
+    tbl.assign((size_t)R * 10, 1.0);
+    for (int c = 0; c < 10; ++c) dcls[c] = class_delta(c, J, B);
+    for (int64_t k = 0; k < R; ++k)
+        for (int c = 0; c < 10; ++c)
+            if (dcls[c] > 0.0) tbl[(size_t)k * 10 + c] = std::exp(-betas[k] * dcls[c]);
+}
+
+static uint32_t cb_tables(const double* betas, int64_t R, double J, double B, std::vector<uint32_t>& thr) {
+    uint32_t always = 0;
+    thr.assign((size_t)R * 10, 0xffffffffu);
+    for (int c = 0; c < 10; ++c) {
+        const double d = class_delta(c, J, B);
+        if (d <= 0.0) {
+            always |= 1u << c;
+            continue;
+        }
+        for (int64_t k = 0; k < R; ++k) {
+            const double p = std::exp(-betas[k] * d);
+            const double x = p * 4294967296.0;
+            thr[(size_t)k * 10 + c] = x >= 4294967295.0 ? 0xffffffffu : (uint32_t)x;
+        }
+    }
+    if (B == 0.0) always |= 1u << 16;  // thresholds depend on k only
+    return always;
+}
+
+static bool integral(double x) { return std::isfinite(x) && std::fabs(x) < 1e15 && x == std::floor(x); }
+
+// --------------------------------------------------------------- workspace --
+struct Buf {
+    void* p = nullptr;
+    size_t n = 0;
+};
+
+struct Workspace {
+    std::mutex mu;
+    int device = -1;
+    std::vector<Buf> bufs;
+    cudaStream_t s[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t ev_in[64], ev_out[64];
+    bool events = false;
+};
+
+static Workspace g_ws;
+
+static int ws_prepare(Workspace& w) {
+    int dev = 0;
+    PTMH_CUDA(cudaGetDevice(&dev));
+    if (w.device != dev) {
+        w.bufs.clear();  // a device switch leaks the old buffers on purpose
+        for (auto& st : w.s) st = nullptr;
+        w.events = false;
+        w.device = dev;
+    }
+    for (auto& st : w.s)
+        if (!st) PTMH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    if (!w.events) {
+        for (int k = 0; k < 64; ++k) {
+            PTMH_CUDA(cudaEventCreateWithFlags(&w.ev_in[k], cudaEventDisableTiming));
+            PTMH_CUDA(cudaEventCreateWithFlags(&w.ev_out[k], cudaEventDisableTiming));
+        }
+        w.events = true;
+    }
+    return PTMH_OK;
+}
+
+template <typename T>
+static int ws_get(Workspace& w, size_t idx, size_t count, T** out) {
+    if (w.bufs.size() <= idx) w.bufs.resize(idx + 1);
+    Buf& b = w.bufs[idx];
+    const size_t bytes = std::max<size_t>(count * sizeof(T), 256);
+    if (b.n < bytes) {
+        if (b.p) PTMH_CUDA(cudaFree(b.p));
+        b.p = nullptr;
+        b.n = 0;
+        PTMH_CUDA(cudaMalloc(&b.p, bytes));
+        b.n = bytes;
+    }
+    *out = static_cast<T*>(b.p);
+    return PTMH_OK;
+}
+
+#define PTMH_TRY(expr)          \
+    do {                        \
+        int rc_ = (expr);       \
+        if (rc_ != PTMH_OK) return rc_; \
+    } while (0)
+
+}  // namespace ptmh
+
+using namespace ptmh;
+
+extern "C" {
+
+int ptmh_abi_version(void) { return PTMH_ABI_VERSION; }
+const char* ptmh_last_error(void) { return g_last_error.c_str(); }
+
+// ------------------------------------------------------------- device ABI --
+int ptmh_fill_lattices(int8_t* spins, int64_t rows, int64_t L, int64_t up_count, uint64_t seed,
+                       uint64_t stream0, uint64_t pos0, void* stream) {
+    PTMH_CHECK_ARG(rows >= 0 && L >= 1 && up_count >= 0 && up_count <= L * L, "fill_lattices shape");
+    return launch_fill(spins, rows, L * L, up_count, seed, stream0, pos0, as_stream(stream));
+}
+
+int ptmh_row_stats(const int8_t* spins, int64_t rows, int64_t L, int64_t* stats, void* stream) {
+    PTMH_CHECK_ARG(rows >= 0 && L >= 1, "row_stats shape");
+    return launch_row_stats(spins, rows, L, stats, as_stream(stream));
+}
+
+int ptmh_advance_block(int8_t* spins, int64_t L, const int64_t* slot_to_row, int64_t lo, int64_t hi,
+                       const double* tbl, const double* dcls, int int_energy, double* energies,
+                       int64_t* spin_sums, uint64_t* positions, int64_t* iters_done, uint64_t seed,
+                       int64_t start_iter, int64_t nsteps, double* obs_e, double* obs_m, int64_t ncols,
+                       int record, int8_t* states, void* stream) {
+    PTMH_CHECK_ARG(L >= 2 && L * L < (1LL << 31), "advance_block: need 2 <= L, L*L < 2^31");
+    PTMH_CHECK_ARG(lo >= 0 && hi >= lo && nsteps >= 0 && start_iter >= 0, "advance_block range");
+    PTMH_CHECK_ARG(record >= 0 && record <= 2, "advance_block record flag");
+    PTMH_CHECK_ARG(record == 0 || start_iter + nsteps <= ncols, "advance_block: obs columns");
+    AdvanceArgs a{spins, L, slot_to_row, lo, hi, tbl, dcls, int_energy, energies, spin_sums,
+                  positions, iters_done, seed, start_iter, nsteps, obs_e, obs_m, ncols, record, states};
+    return launch_advance(a, as_stream(stream));
+}
+
+int ptmh_swap_chunk(int64_t* slot_to_row, double* energies, int64_t* spin_sums, const double* betas,
+                    int64_t R, uint64_t seed, int64_t stream_base, int64_t round_index, int64_t first,
+                    int64_t pair_lo, int64_t pair_hi, int64_t* accepted, int64_t* near_ties,
+                    int32_t* row_to_slot, void* stream) {
+    PTMH_CHECK_ARG(pair_lo >= 0 && pair_hi >= pair_lo && first + 2 * pair_hi <= R, "swap_chunk pairs");
+    return launch_swap(slot_to_row, energies, spin_sums, betas, R, seed, stream_base, round_index, first,
+                       pair_lo, pair_hi, accepted, near_ties, row_to_slot, as_stream(stream));
+}
+
+int64_t ptmh_cb_words_per_color(int64_t L) { return cb_words(L); }
+
+int ptmh_cb_pack(const int8_t* spins, int64_t rows, int64_t L, uint32_t* packed, void* stream) {
+    PTMH_CHECK_ARG(L >= 2 && L % 2 == 0, "checkerboard needs even L");
+    return launch_cb_pack(spins, rows, L, packed, as_stream(stream));
+}
+
+int ptmh_cb_unpack(const uint32_t* packed, int64_t rows, int64_t L, int8_t* spins, void* stream) {
+    PTMH_CHECK_ARG(L >= 2 && L % 2 == 0, "checkerboard needs even L");
+    return launch_cb_unpack(packed, rows, L, spins, as_stream(stream));
+}
+
+int ptmh_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* row_to_slot,
+                   const uint32_t* thresh, uint32_t always_mask, uint64_t seed, int64_t first_sweep,
+                   int64_t n_sweeps, int64_t* stats, void* stream) {
+    PTMH_CHECK_ARG(L >= 2 && L % 2 == 0 && L <= 65536, "checkerboard needs even 2 <= L <= 65536");
+    PTMH_CHECK_ARG(first_sweep >= 0 && n_sweeps >= 0 && first_sweep + n_sweeps < (1LL << 31),
+                   "checkerboard sweep index must stay below 2^31");
+    return launch_cb_sweeps(packed, rows, L, row_to_slot, thresh, always_mask, seed, first_sweep, n_sweeps,
+                            stats, as_stream(stream));
+}
+
+int ptmh_cb_row_stats(const uint32_t* packed, int64_t rows, int64_t L, int64_t* stats, void* stream) {
+    PTMH_CHECK_ARG(L >= 2 && L % 2 == 0, "checkerboard needs even L");
+    return launch_cb_row_stats(packed, rows, L, stats, as_stream(stream));
+}
+
+int ptmh_cb_slot_energies(const int64_t* stats_all, const int64_t* slot_to_row, int64_t R, double J, double B,
+                          double* energies, int64_t* spin_sums, void* stream) {
+    return launch_cb_slot_energies(stats_all, slot_to_row, R, J, B, energies, spin_sums, as_stream(stream));
+}
+
+int ptmh_cb_observe(const int64_t* stats_all, const int64_t* slot_to_row, int64_t R, int64_t L, double J,
+                    double B, double* obs_e, double* obs_m, int64_t ncols, int64_t col, void* stream) {
+    PTMH_CHECK_ARG(col >= 0 && col < ncols, "observe column");
+    return launch_cb_observe(stats_all, slot_to_row, R, L, J, B, obs_e, obs_m, ncols, col, as_stream(stream));
+}
+
+// --------------------------------------------------------------- host ABI --
+int ptmh_host_fill_lattice(int8_t* out, int64_t n, int64_t up_count, uint64_t seed, uint64_t stream,
+                           uint64_t position, uint64_t* new_position) {
+    PTMH_CHECK_ARG(n >= 1 && up_count >= 0, "fill_lattice shape");
+    std::lock_guard<std::mutex> lk(g_ws.mu);
+    PTMH_TRY(ws_prepare(g_ws));
+    cudaStream_t s = g_ws.s[1];
+    int8_t* d = nullptr;
+    PTMH_TRY(ws_get(g_ws, 0, (size_t)n, &d));
+    PTMH_TRY(launch_fill(d, 1, n, up_count, seed, stream, position, s));
+    PTMH_CUDA(cudaMemcpyAsync(out, d, (size_t)n, cudaMemcpyDeviceToHost, s));
+    PTMH_CUDA(cudaStreamSynchronize(s));
+    if (new_position) *new_position = position + (uint64_t)(n - 1);  // kernels.py:45
+    return PTMH_OK;
+}
+
+int ptmh_host_lattice_energy(const int8_t* spins, int64_t L, double J, double B, double* energy) {
+    PTMH_CHECK_ARG(L >= 1 && energy, "lattice_energy shape");
+    std::lock_guard<std::mutex> lk(g_ws.mu);
+    PTMH_TRY(ws_prepare(g_ws));
+    cudaStream_t s = g_ws.s[1];
+    int8_t* d = nullptr;
+    int64_t* st = nullptr;
+    PTMH_TRY(ws_get(g_ws, 0, (size_t)(L * L), &d));
+    PTMH_TRY(ws_get(g_ws, 1, 2, &st));
+    int64_t h[2];
+    PTMH_CUDA(cudaMemcpyAsync(d, spins, (size_t)(L * L), cudaMemcpyHostToDevice, s));
+    PTMH_TRY(launch_row_stats(d, 1, L, st, s));
+    PTMH_CUDA(cudaMemcpyAsync(h, st, sizeof(h), cudaMemcpyDeviceToHost, s));
+    PTMH_CUDA(cudaStreamSynchronize(s));
+    *energy = B * (double)h[0] - J * (double)h[1];  // kernels.py:59
+    return PTMH_OK;
+}
+
+int ptmh_host_advance_block(int8_t* spins, int64_t rows, int64_t L, const int64_t* slot_to_row, int64_t R,
+                            int64_t lo, int64_t hi, const double* betas, double J, double B,
+                            double* energies, int64_t* spin_sums, uint64_t* positions,
+                            int64_t* iters_done, uint64_t seed, int64_t start_iter, int64_t nsteps,
+                            double* obs_e, double* obs_m, int64_t ncols, int record, int8_t* states) {
+    PTMH_CHECK_ARG(rows >= 1 && R >= 1 && lo >= 0 && hi <= R && lo <= hi, "advance_block shape");
+    PTMH_CHECK_ARG(record == 0 || (obs_e && obs_m && start_iter + nsteps <= ncols), "advance_block obs");
+    PTMH_CHECK_ARG(record != 2 || states, "advance_block states");
+    if (hi == lo || nsteps == 0) {
+        for (int64_t k = lo; k < hi; ++k) iters_done[k] = start_iter + nsteps;
+        return PTMH_OK;
+    }
+    std::vector<double> tbl, dcls;
+    exact_tables(betas, R, J, B, tbl, dcls);
+    int int_energy = integral(J) && integral(B) && std::fabs(J) <= 1e6 && std::fabs(B) <= 1e6;
+    for (int64_t k = lo; k < hi && int_energy; ++k) int_energy = integral(energies[k]);
+    std::lock_guard<std::mutex> lk(g_ws.mu);
+    PTMH_TRY(ws_prepare(g_ws));
+    cudaStream_t s = g_ws.s[1];
+    const size_t nsite = (size_t)(L * L);
+    int8_t* d_spins; int64_t* d_s2r; double *d_tbl, *d_dcls, *d_e, *d_oe = nullptr, *d_om = nullptr;
+    int64_t *d_sums, *d_iters; uint64_t* d_pos; int8_t* d_states = nullptr;
+    PTMH_TRY(ws_get(g_ws, 0, (size_t)rows * nsite, &d_spins));
+    PTMH_TRY(ws_get(g_ws, 1, (size_t)R, &d_s2r));
+    PTMH_TRY(ws_get(g_ws, 2, (size_t)R * 10, &d_tbl));
+    PTMH_TRY(ws_get(g_ws, 3, 10, &d_dcls));
+    PTMH_TRY(ws_get(g_ws, 4, (size_t)R, &d_e));
+    PTMH_TRY(ws_get(g_ws, 5, (size_t)R, &d_sums));
+    PTMH_TRY(ws_get(g_ws, 6, (size_t)R, &d_pos));
+    PTMH_TRY(ws_get(g_ws, 7, (size_t)R, &d_iters));
+    PTMH_CUDA(cudaMemcpyAsync(d_spins, spins, (size_t)rows * nsite, cudaMemcpyHostToDevice, s));
+    PTMH_CUDA(cudaMemcpyAsync(d_s2r, slot_to_row, R * 8, cudaMemcpyHostToDevice, s));
+    PTMH_CUDA(cudaMemcpyAsync(d_tbl, tbl.data(), R * 80, cudaMemcpyHostToDevice, s));
+    PTMH_CUDA(cudaMemcpyAsync(d_dcls, dcls.data(), 80, cudaMemcpyHostToDevice, s));
+    PTMH_CUDA(cudaMemcpyAsync(d_e, energies, R * 8, cudaMemcpyHostToDevice, s));
+    PTMH_CUDA(cudaMemcpyAsync(d_sums, spin_sums, R * 8, cudaMemcpyHostToDevice, s));
+    PTMH_CUDA(cudaMemcpyAsync(d_pos, positions, R * 8, cudaMemcpyHostToDevice, s));
+    PTMH_CUDA(cudaMemcpyAsync(d_iters, iters_done, R * 8, cudaMemcpyHostToDevice, s));
+    if (record >= 1) {
+        PTMH_TRY(ws_get(g_ws, 8, (size_t)R * ncols, &d_oe));
+        PTMH_TRY(ws_get(g_ws, 9, (size_t)R * ncols, &d_om));
+    }
+    if (record == 2) PTMH_TRY(ws_get(g_ws, 10, (size_t)R * ncols * nsite, &d_states));
+    AdvanceArgs a{d_spins, L, d_s2r, lo, hi, d_tbl, d_dcls, int_energy, d_e, d_sums, d_pos, d_iters, seed,
+                  start_iter, nsteps, d_oe, d_om, ncols, record, d_states};
+    PTMH_TRY(launch_advance(a, s));
+    PTMH_CUDA(cudaMemcpyAsync(spins, d_spins, (size_t)rows * nsite, cudaMemcpyDeviceToHost, s));
+    PTMH_CUDA(cudaMemcpyAsync(energies + lo, d_e + lo, (hi - lo) * 8, cudaMemcpyDeviceToHost, s));
+    PTMH_CUDA(cudaMemcpyAsync(spin_sums + lo, d_sums + lo, (hi - lo) * 8, cudaMemcpyDeviceToHost, s));
+    PTMH_CUDA(cudaMemcpyAsync(positions + lo, d_pos + lo, (hi - lo) * 8, cudaMemcpyDeviceToHost, s));
+    PTMH_CUDA(cudaMemcpyAsync(iters_done + lo, d_iters + lo, (hi - lo) * 8, cudaMemcpyDeviceToHost, s));
+    if (record >= 1) {
+        // only the columns this call wrote, as the numba kernel does
+        const size_t pitch = (size_t)ncols * 8;
+        PTMH_CUDA(cudaMemcpy2DAsync(obs_e + lo * ncols + start_iter, pitch, d_oe + lo * ncols + start_iter,
+                                    pitch, nsteps * 8, hi - lo, cudaMemcpyDeviceToHost, s));
+        PTMH_CUDA(cudaMemcpy2DAsync(obs_m + lo * ncols + start_iter, pitch, d_om + lo * ncols + start_iter,
+                                    pitch, nsteps * 8, hi - lo, cudaMemcpyDeviceToHost, s));
+    }
+    if (record == 2) {
+        const size_t pitch = (size_t)ncols * nsite;
+        PTMH_CUDA(cudaMemcpy2DAsync(states + (lo * ncols + start_iter) * nsite, pitch,
+                                    d_states + (lo * ncols + start_iter) * nsite, pitch, nsteps * nsite,
+                                    hi - lo, cudaMemcpyDeviceToHost, s));
+    }
+    PTMH_CUDA(cudaStreamSynchronize(s));
+    return PTMH_OK;
+}
+
+int ptmh_host_swap_chunk(int64_t* slot_to_row, double* energies, int64_t* spin_sums, const double* betas,
+                         int64_t R, uint64_t seed, int64_t stream_base, int64_t round_index, int64_t first,
+                         int64_t pair_lo, int64_t pair_hi, int64_t* accepted) {
+    PTMH_CHECK_ARG(R >= 0 && pair_lo >= 0 && pair_hi >= pair_lo && first + 2 * pair_hi <= R,
+                   "swap_chunk pairs");
+    if (accepted) *accepted = 0;
+    if (pair_hi == pair_lo) return PTMH_OK;
+    std::lock_guard<std::mutex> lk(g_ws.mu);
+    PTMH_TRY(ws_prepare(g_ws));
+    cudaStream_t s = g_ws.s[1];
+    int64_t *d_s2r, *d_sums, *d_cnt; double *d_e, *d_b;
+    PTMH_TRY(ws_get(g_ws, 1, (size_t)R, &d_s2r));
+    PTMH_TRY(ws_get(g_ws, 4, (size_t)R, &d_e));
+    PTMH_TRY(ws_get(g_ws, 5, (size_t)R, &d_sums));
+    PTMH_TRY(ws_get(g_ws, 11, (size_t)R, &d_b));
+    PTMH_TRY(ws_get(g_ws, 12, 2, &d_cnt));
+    PTMH_CUDA(cudaMemcpyAsync(d_s2r, slot_to_row, R * 8, cudaMemcpyHostToDevice, s));
+    PTMH_CUDA(cudaMemcpyAsync(d_e, energies, R * 8, cudaMemcpyHostToDevice, s));
+    PTMH_CUDA(cudaMemcpyAsync(d_sums, spin_sums, R * 8, cudaMemcpyHostToDevice, s));
+    PTMH_CUDA(cudaMemcpyAsync(d_b, betas, R * 8, cudaMemcpyHostToDevice, s));
+    PTMH_CUDA(cudaMemsetAsync(d_cnt, 0, 16, s));
+    PTMH_TRY(launch_swap(d_s2r, d_e, d_sums, d_b, R, seed, stream_base, round_index, first, pair_lo, pair_hi,
+                         d_cnt, d_cnt + 1, nullptr, s));
+    int64_t cnt[2];
+    PTMH_CUDA(cudaMemcpyAsync(slot_to_row, d_s2r, R * 8, cudaMemcpyDeviceToHost, s));
+    PTMH_CUDA(cudaMemcpyAsync(energies, d_e, R * 8, cudaMemcpyDeviceToHost, s));
+    PTMH_CUDA(cudaMemcpyAsync(spin_sums, d_sums, R * 8, cudaMemcpyDeviceToHost, s));
+    PTMH_CUDA(cudaMemcpyAsync(cnt, d_cnt, 16, cudaMemcpyDeviceToHost, s));
+    PTMH_CUDA(cudaStreamSynchronize(s));
+    if (accepted) *accepted = cnt[0];
+    return PTMH_OK;
+}
+
+int ptmh_host_cb_interval(int8_t* spins, int64_t R, int64_t L, int64_t* slot_to_row, const double* betas,
+                          double J, double B, uint64_t seed, int64_t first_sweep, int64_t n_sweeps,
+                          int64_t round_index, double* energies, int64_t* spin_sums, int64_t* accepted) {
+    PTMH_CHECK_ARG(R >= 1 && L >= 2 && L % 2 == 0 && L <= 65536, "cb_interval shape");
+    PTMH_CHECK_ARG(first_sweep >= 0 && n_sweeps >= 0, "cb_interval sweeps");
+    std::vector<uint32_t> thr;
+    const uint32_t always = cb_tables(betas, R, J, B, thr);
+    std::vector<int32_t> r2s((size_t)R);
+    for (int64_t k = 0; k < R; ++k) {
+        PTMH_CHECK_ARG(slot_to_row[k] >= 0 && slot_to_row[k] < R, "slot_to_row out of range");
+        r2s[(size_t)slot_to_row[k]] = (int32_t)k;
+    }
+    std::lock_guard<std::mutex> lk(g_ws.mu);
+    PTMH_TRY(ws_prepare(g_ws));
+    cudaStream_t sin = g_ws.s[0], sc = g_ws.s[1], sout = g_ws.s[2];
+    const int64_t nsite = L * L, W = cb_words(L);
+    int8_t* d_spins; uint32_t *d_packed, *d_thr; int64_t *d_stats, *d_s2r, *d_sums, *d_cnt;
+    int32_t* d_r2s; double *d_b, *d_e;
+    PTMH_TRY(ws_get(g_ws, 0, (size_t)(R * nsite), &d_spins));
+    PTMH_TRY(ws_get(g_ws, 13, (size_t)(R * 2 * W), &d_packed));
+    PTMH_TRY(ws_get(g_ws, 14, (size_t)(R * 2), &d_stats));
+    PTMH_TRY(ws_get(g_ws, 15, (size_t)(R * 10), &d_thr));
+    PTMH_TRY(ws_get(g_ws, 1, (size_t)R, &d_s2r));
+    PTMH_TRY(ws_get(g_ws, 16, (size_t)R, &d_r2s));
+    PTMH_TRY(ws_get(g_ws, 11, (size_t)R, &d_b));
+    PTMH_TRY(ws_get(g_ws, 4, (size_t)R, &d_e));
+    PTMH_TRY(ws_get(g_ws, 5, (size_t)R, &d_sums));
+    PTMH_TRY(ws_get(g_ws, 12, 2, &d_cnt));
+    PTMH_CUDA(cudaMemcpyAsync(d_thr, thr.data(), R * 40, cudaMemcpyHostToDevice, sc));
+    PTMH_CUDA(cudaMemcpyAsync(d_s2r, slot_to_row, R * 8, cudaMemcpyHostToDevice, sc));
+    PTMH_CUDA(cudaMemcpyAsync(d_r2s, r2s.data(), R * 4, cudaMemcpyHostToDevice, sc));
+    PTMH_CUDA(cudaMemcpyAsync(d_b, betas, R * 8, cudaMemcpyHostToDevice, sc));
+    PTMH_CUDA(cudaMemsetAsync(d_cnt, 0, 16, sc));
+    // pipeline: H2D chunk c | pack + stats + sweeps + unpack chunk c | D2H chunk c
+    const int64_t nch = std::min<int64_t>(R, 8);
+    for (int64_t c = 0; c < nch; ++c) {
+        const int64_t lo = R * c / nch, hi = R * (c + 1) / nch, n = hi - lo;
+        PTMH_CUDA(cudaMemcpyAsync(d_spins + lo * nsite, spins + lo * nsite, (size_t)(n * nsite),
+                                  cudaMemcpyHostToDevice, sin));
+        PTMH_CUDA(cudaEventRecord(g_ws.ev_in[c], sin));
+        PTMH_CUDA(cudaStreamWaitEvent(sc, g_ws.ev_in[c], 0));
+        PTMH_TRY(launch_cb_pack(d_spins + lo * nsite, n, L, d_packed + lo * 2 * W, sc));
+        PTMH_TRY(launch_row_stats(d_spins + lo * nsite, n, L, d_stats + 2 * lo, sc));
+        PTMH_TRY(launch_cb_sweeps(d_packed + lo * 2 * W, n, L, d_r2s + lo, d_thr, always, seed, first_sweep,
+                                  n_sweeps, d_stats + 2 * lo, sc));
+        PTMH_TRY(launch_cb_unpack(d_packed + lo * 2 * W, n, L, d_spins + lo * nsite, sc));
+        PTMH_CUDA(cudaEventRecord(g_ws.ev_out[c], sc));
+        PTMH_CUDA(cudaStreamWaitEvent(sout, g_ws.ev_out[c], 0));
+        PTMH_CUDA(cudaMemcpyAsync(spins + lo * nsite, d_spins + lo * nsite, (size_t)(n * nsite),
+                                  cudaMemcpyDeviceToHost, sout));
+    }
+    PTMH_TRY(launch_cb_slot_energies(d_stats, d_s2r, R, J, B, d_e, d_sums, sc));
+    if (round_index >= 0) {
+        const int64_t first = round_index % 2, n_pairs = std::max<int64_t>(0, (R - first) / 2);
+        if (n_pairs > 0)
+            PTMH_TRY(launch_swap(d_s2r, d_e, d_sums, d_b, R, seed, R, round_index, first, 0, n_pairs, d_cnt,
+                                 d_cnt + 1, nullptr, sc));
+    }
+    int64_t cnt[2];
+    PTMH_CUDA(cudaMemcpyAsync(slot_to_row, d_s2r, R * 8, cudaMemcpyDeviceToHost, sc));
+    PTMH_CUDA(cudaMemcpyAsync(energies, d_e, R * 8, cudaMemcpyDeviceToHost, sc));
+    PTMH_CUDA(cudaMemcpyAsync(spin_sums, d_sums, R * 8, cudaMemcpyDeviceToHost, sc));
+    PTMH_CUDA(cudaMemcpyAsync(cnt, d_cnt, 16, cudaMemcpyDeviceToHost, sc));
+    PTMH_CUDA(cudaStreamSynchronize(sc));
+    PTMH_CUDA(cudaStreamSynchronize(sout));
+    if (accepted) *accepted = cnt[0];
+    return PTMH_OK;
+}
+}  // extern "C"

@@ -1,0 +1,53 @@
+// launchers.cuh -- host-side launchers shared between the translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace ptmh {
+
+struct AdvanceArgs {
+    int8_t* spins;
+    int64_t L;
+    const int64_t* slot_to_row;
+    int64_t lo, hi;
+    const double* tbl;   // (R, 10) exp(-beta_k * dE_c), host-built
+    const double* dcls;  // (10) dE_c
+    int int_energy;
+    double* energies;
+    int64_t* spin_sums;
+    uint64_t* positions;
+    int64_t* iters_done;
+    uint64_t seed;
+    int64_t start_iter, nsteps;
+    double* obs_e;
+    double* obs_m;
+    int64_t ncols;
+    int record;
+    int8_t* states;
+};
+
+// exact.cu (n = sites per lattice row)
+int launch_fill(int8_t* spins, int64_t rows, int64_t n, int64_t up_count, uint64_t seed,
+                uint64_t stream0, uint64_t pos0, cudaStream_t s);
+int launch_row_stats(const int8_t* spins, int64_t rows, int64_t L, int64_t* stats, cudaStream_t s);
+int launch_advance(const AdvanceArgs& a, cudaStream_t s);
+int launch_swap(int64_t* slot_to_row, double* energies, int64_t* spin_sums, const double* betas,
+                int64_t R, uint64_t seed, int64_t stream_base, int64_t round_index, int64_t first,
+                int64_t pair_lo, int64_t pair_hi, int64_t* accepted, int64_t* near_ties,
+                int32_t* row_to_slot, cudaStream_t s);
+
+// checkerboard.cu
+int64_t cb_words(int64_t L);
+int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* row_to_slot,
+                     const uint32_t* thresh, uint32_t always_mask, uint64_t seed, int64_t first_sweep,
+                     int64_t n_sweeps, int64_t* stats, cudaStream_t s);
+int launch_cb_pack(const int8_t* spins, int64_t rows, int64_t L, uint32_t* packed, cudaStream_t s);
+int launch_cb_unpack(const uint32_t* packed, int64_t rows, int64_t L, int8_t* spins, cudaStream_t s);
+int launch_cb_row_stats(const uint32_t* packed, int64_t rows, int64_t L, int64_t* stats, cudaStream_t s);
+int launch_cb_slot_energies(const int64_t* stats, const int64_t* s2r, int64_t R, double J, double B,
+                            double* energies, int64_t* sums, cudaStream_t s);
+int launch_cb_observe(const int64_t* stats, const int64_t* s2r, int64_t R, int64_t L, double J, double B,
+                      double* obs_e, double* obs_m, int64_t ncols, int64_t col, cudaStream_t s);
+
+}  // namespace ptmh

@@ -1,0 +1,214 @@
+"""Device-resident replica state and the calls that advance it.
+
+Every tensor here lives in HBM for the whole run (allocated through torch's
+caching allocator); each method is a handful of asynchronous launches of the
+CUDA kernels in csrc/ through the C ABI (include/ptmh.h) on the current
+torch stream.  Nothing is copied to the host until the run asks for results.
+
+Two chains:
+
+* ``ExactEngine`` -- the reference's random-site chain, bit-exact with
+  ``isingpt.executor.run`` (csrc/exact.cu).
+* ``CheckerboardEngine`` -- Mode F, the multispin-coded checkerboard sweep
+  (csrc/checkerboard.cu), DESIGN.md section 3.
+
+Lattice ("row") r of a run holds a configuration; slot k holds a temperature.
+Exchanges permute slot_to_row / row_to_slot only -- lattices never move
+(kernels.py:138-146 does the same with its row indirection).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .tables import cb_tables, exact_tables, integer_energy_ok
+
+_P = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+
+
+def _stream(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def require_cuda(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2512_03825_b200 needs a CUDA device (B200, sm_100a); "
+                           "there is no CPU fallback")
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    if isinstance(device, torch.device):
+        return torch.device("cuda", device.index if device.index is not None
+                            else torch.cuda.current_device())
+    return torch.device("cuda", int(device))
+
+
+class _Base:
+    def __init__(self, side: int, replicas: int, temperatures: np.ndarray, seed: int,
+                 J: float, B: float, up_fraction: float, device=None,
+                 row_range: tuple[int, int] | None = None):
+        self.dev = require_cuda(device)
+        self.L, self.R = int(side), int(replicas)
+        self.seed = int(seed) & ((1 << 64) - 1)
+        self.J, self.B = float(J), float(B)
+        self.temps = np.asarray(temperatures, dtype=np.float64)
+        self.betas_np = 1.0 / self.temps  # executor.py:195
+        self.up_count = round(up_fraction * self.L * self.L)  # executor.py:202
+        lo, hi = row_range if row_range is not None else (0, self.R)
+        self.row_lo, self.row_hi = int(lo), int(hi)
+        self.rows = self.row_hi - self.row_lo
+        d = self.dev
+        self.betas = torch.from_numpy(self.betas_np.copy()).to(d)
+        self.slot_to_row = torch.arange(self.R, dtype=torch.int64, device=d)
+        self.counters = torch.zeros(2, dtype=torch.int64, device=d)  # accepted, near ties
+
+    def _s(self) -> int:
+        return _stream(self.dev)
+
+    def swap_counts(self) -> tuple[int, int]:
+        c = self.counters.cpu().tolist()
+        return int(c[0]), int(c[1])
+
+
+class ExactEngine(_Base):
+    """The reference chain on device arrays (executor.py:196-220 state)."""
+
+    def __init__(self, *a, **kw):
+        super().__init__(*a, **kw)
+        if self.rows != self.R:
+            raise ValueError("the exact chain runs unsharded (one device)")
+        d, R, L = self.dev, self.R, self.L
+        self.spins = torch.empty((R, L, L), dtype=torch.int8, device=d)
+        self.positions = torch.zeros(R, dtype=torch.int64, device=d)
+        self.energies = torch.zeros(R, dtype=torch.float64, device=d)
+        self.spin_sums = torch.zeros(R, dtype=torch.int64, device=d)
+        self.iters_done = torch.zeros(R, dtype=torch.int64, device=d)
+        tbl, dcls = exact_tables(self.betas_np, self.J, self.B)
+        self.tbl = torch.from_numpy(tbl).to(d)
+        self.dcls = torch.from_numpy(dcls).to(d)
+        self.int_energy = 0
+
+    def init_state(self) -> None:
+        """executor.py:203-207: row r from stream r, position 0."""
+        s = self._s()
+        R, L = self.R, self.L
+        _lib.call("ptmh_fill_lattices", _P(self.spins), R, L, self.up_count, self.seed, 0, 0, s)
+        stats = torch.empty((R, 2), dtype=torch.int64, device=self.dev)
+        _lib.call("ptmh_row_stats", _P(self.spins), R, L, _P(stats), s)
+        st = stats.cpu().numpy()
+        # kernels.py:59 B*total - J*bond, evaluated with the same FP64 ops
+        e = self.B * st[:, 0].astype(np.float64) - self.J * st[:, 1].astype(np.float64)
+        self.energies.copy_(torch.from_numpy(e))
+        self.spin_sums.copy_(torch.from_numpy(st[:, 0].copy()))
+        self.positions.fill_(L * L - 1)  # fill_lattice consumes L^2-1 draws
+        self.int_energy = int(integer_energy_ok(self.J, self.B, e))
+
+    def advance(self, start_iter: int, nsteps: int, obs_e=None, obs_m=None, record: int = 0,
+                states=None, lo: int = 0, hi: int | None = None) -> None:
+        """kernels.py:62-113 over slots [lo, hi)."""
+        hi = self.R if hi is None else hi
+        ncols = obs_e.shape[1] if obs_e is not None else 0
+        _lib.call("ptmh_advance_block", _P(self.spins), self.L, _P(self.slot_to_row), lo, hi,
+                  _P(self.tbl), _P(self.dcls), self.int_energy, _P(self.energies),
+                  _P(self.spin_sums), _P(self.positions), _P(self.iters_done), self.seed,
+                  start_iter, nsteps, _P(obs_e), _P(obs_m), ncols, record, _P(states), self._s())
+
+    def exchange(self, round_index: int) -> int:
+        """One swap round (executor.py:250-262, kernels.py:116-148); returns
+        the number of pairs attempted."""
+        first = round_index % 2
+        n_pairs = max(0, (self.R - first) // 2)
+        if n_pairs:
+            _lib.call("ptmh_swap_chunk", _P(self.slot_to_row), _P(self.energies),
+                      _P(self.spin_sums), _P(self.betas), self.R, self.seed, self.R,
+                      round_index, first, 0, n_pairs, _P(self.counters),
+                      self.counters.data_ptr() + 8, None, self._s())
+        return n_pairs
+
+    def final_spins(self) -> np.ndarray:
+        return self.spins.cpu().numpy()
+
+
+class CheckerboardEngine(_Base):
+    """Mode F state: bit-packed lattices (rows, 2, W) uint32 + per-lattice
+    (sum s, sum bonds) int64 kept current by the fused reduction."""
+
+    def __init__(self, *a, **kw):
+        super().__init__(*a, **kw)
+        if self.L % 2:
+            raise ValueError("the checkerboard sweep needs an even lattice side")
+        d, R = self.dev, self.R
+        self.W = int(_lib.LIB.ptmh_cb_words_per_color(self.L))
+        self.packed = torch.zeros((self.rows, 2, self.W), dtype=torch.int32, device=d)
+        self.stats = torch.zeros((R, 2), dtype=torch.int64, device=d)  # all lattices
+        self.row_to_slot = torch.arange(R, dtype=torch.int32, device=d)
+        thr, always = cb_tables(self.betas_np, self.J, self.B)
+        self.thr = torch.from_numpy(thr.view(np.int32)).to(d)
+        self.always = int(always)
+        self.energies = torch.zeros(R, dtype=torch.float64, device=d)
+        self.spin_sums = torch.zeros(R, dtype=torch.int64, device=d)
+
+    @property
+    def local_stats(self) -> torch.Tensor:
+        return self.stats[self.row_lo:self.row_hi]
+
+    def init_state(self) -> None:
+        """Exact-count init identical to the reference (executor.py:203-207)
+        for the local rows, then per-lattice stats and packing."""
+        s = self._s()
+        if self.rows == 0:
+            return
+        spins = torch.empty((self.rows, self.L, self.L), dtype=torch.int8, device=self.dev)
+        _lib.call("ptmh_fill_lattices", _P(spins), self.rows, self.L, self.up_count, self.seed,
+                  self.row_lo, 0, s)
+        _lib.call("ptmh_row_stats", _P(spins), self.rows, self.L, _P(self.local_stats), s)
+        _lib.call("ptmh_cb_pack", _P(spins), self.rows, self.L, _P(self.packed), s)
+        del spins
+
+    def load_spins(self, spins: torch.Tensor) -> None:
+        """Replace the local lattices with given int8 configurations."""
+        s = self._s()
+        spins = spins.to(self.dev, torch.int8).contiguous()
+        _lib.call("ptmh_row_stats", _P(spins), self.rows, self.L, _P(self.local_stats), s)
+        _lib.call("ptmh_cb_pack", _P(spins), self.rows, self.L, _P(self.packed), s)
+
+    def sweeps(self, first_sweep: int, n: int) -> None:
+        if self.rows == 0 or n <= 0:
+            return
+        rts = self.row_to_slot[self.row_lo:self.row_hi]
+        _lib.call("ptmh_cb_sweeps", _P(self.packed), self.rows, self.L, _P(rts), _P(self.thr),
+                  self.always, self.seed, first_sweep, n, _P(self.local_stats), self._s())
+
+    def exchange(self, round_index: int) -> int:
+        """Swap round on the energies of every lattice (self.stats must hold
+        all lattices: the distributed driver all-gathers them first)."""
+        s = self._s()
+        first = round_index % 2
+        n_pairs = max(0, (self.R - first) // 2)
+        _lib.call("ptmh_cb_slot_energies", _P(self.stats), _P(self.slot_to_row), self.R, self.J,
+                  self.B, _P(self.energies), _P(self.spin_sums), s)
+        if n_pairs:
+            _lib.call("ptmh_swap_chunk", _P(self.slot_to_row), _P(self.energies),
+                      _P(self.spin_sums), _P(self.betas), self.R, self.seed, self.R,
+                      round_index, first, 0, n_pairs, _P(self.counters),
+                      self.counters.data_ptr() + 8, _P(self.row_to_slot), s)
+        return n_pairs
+
+    def observe(self, obs_e: torch.Tensor, obs_m: torch.Tensor, col: int) -> None:
+        _lib.call("ptmh_cb_observe", _P(self.stats), _P(self.slot_to_row), self.R, self.L,
+                  self.J, self.B, _P(obs_e), _P(obs_m), obs_e.shape[1], col, self._s())
+
+    def audit_stats(self) -> torch.Tensor:
+        """(S, Bond) recomputed from the packed lattices (local rows)."""
+        out = torch.empty((self.rows, 2), dtype=torch.int64, device=self.dev)
+        _lib.call("ptmh_cb_row_stats", _P(self.packed), self.rows, self.L, _P(out), self._s())
+        return out
+
+    def spins_int8(self) -> torch.Tensor:
+        out = torch.empty((self.rows, self.L, self.L), dtype=torch.int8, device=self.dev)
+        _lib.call("ptmh_cb_unpack", _P(self.packed), self.rows, self.L, _P(out), self._s())
+        return out
+
+    def final_spins(self) -> np.ndarray:
+        return self.spins_int8().cpu().numpy()

@@ -1,0 +1,302 @@
+"""run(SimulationConfig) -> RunRecord: the drop-in for isingpt.executor.run.
+
+Same dataclasses, validation, interval plan, swap schedule and record fields
+as the reference (executor.py:28-300).  The state lives on the GPU for the
+whole run (engine.py); the host only walks the interval plan and launches.
+
+Extensions (all defaulted so reference configs run unchanged):
+
+* ``sweep_mode``: "exact" (default) runs the reference's random-site chain,
+  bit-exact with isingpt; "checkerboard" runs Mode F,
+  where ``iterations`` and ``swap_interval`` must be whole sweeps (multiples
+  of side**2) and observables are recorded per sweep (every
+  ``record_every`` sweeps), shape (R, sweeps // record_every).
+* ``temperatures``: explicit ladder (e.g. tempering.geometric_ladder);
+  default is the reference's build_ladder.
+* ``device``: CUDA device index.  ``workers`` is validated and recorded
+  but the GPU replaces the thread pool.
+* ``return_final_state``: also return the final lattices (by row) and
+  slot_to_row, for parity checks.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .lattice import IsingParams
+from .tempering import build_ladder
+
+RECORD_MODES = ("none", "observables", "full_states")
+SWEEP_MODES = ("exact", "checkerboard")
+MASK64 = (1 << 64) - 1
+
+
+class ConfigurationError(ValueError):
+    """Invalid simulation configuration; raised before any work starts."""
+
+
+@dataclass(frozen=True)
+class SimulationConfig:
+    """All parameters of a single run (executor.py:35-67, plus extensions)."""
+
+    side: int = 32
+    replicas: int = 16
+    iterations: int = 50_000
+    swap_interval: int = 100  # 0 disables swaps
+    workers: int = 4
+    seed: int = 42
+    params: IsingParams = field(default_factory=IsingParams)
+    init_up_fraction: float = 0.5
+    record_mode: str = "observables"
+    # --- extensions
+    sweep_mode: str = "exact"
+    temperatures: tuple | None = None
+    record_every: int = 1
+    device: int | None = None
+    return_final_state: bool = False
+
+    def validate(self) -> None:
+        if self.side < 2:
+            raise ConfigurationError(f"side must be >= 2, got {self.side}")
+        if self.replicas < 1:
+            raise ConfigurationError(f"replicas must be >= 1, got {self.replicas}")
+        if self.iterations < 1:
+            raise ConfigurationError(f"iterations must be >= 1, got {self.iterations}")
+        if self.swap_interval < 0:
+            raise ConfigurationError(f"swap_interval must be >= 0, got {self.swap_interval}")
+        if self.workers < 1:
+            raise ConfigurationError(f"workers must be >= 1, got {self.workers}")
+        if not 0.0 <= self.init_up_fraction <= 1.0:
+            raise ConfigurationError(
+                f"init_up_fraction must be in [0, 1], got {self.init_up_fraction}")
+        if self.record_mode not in RECORD_MODES:
+            raise ConfigurationError(
+                f"record_mode must be one of {RECORD_MODES}, got {self.record_mode!r}")
+        if self.sweep_mode not in SWEEP_MODES:
+            raise ConfigurationError(
+                f"sweep_mode must be one of {SWEEP_MODES}, got {self.sweep_mode!r}")
+        if self.temperatures is not None:
+            t = np.asarray(self.temperatures, dtype=np.float64)
+            if t.shape != (self.replicas,) or not np.all(t > 0) or not np.all(np.isfinite(t)):
+                raise ConfigurationError(
+                    "temperatures must be `replicas` positive finite values")
+        if self.record_every < 1:
+            raise ConfigurationError(f"record_every must be >= 1, got {self.record_every}")
+        if self.sweep_mode == "checkerboard":
+            n = self.side * self.side
+            if self.side % 2:
+                raise ConfigurationError(
+                    f"side must be even for the checkerboard sweep, got {self.side}")
+            if self.iterations % n or self.swap_interval % n:
+                raise ConfigurationError(
+                    "iterations and swap_interval must be whole sweeps (multiples of side**2) "
+                    "in checkerboard mode")
+            if self.record_mode == "full_states":
+                raise ConfigurationError(
+                    "record_mode 'full_states' is only available with sweep_mode='exact'")
+            if (self.iterations // n) // self.record_every < 1 and self.record_mode != "none":
+                raise ConfigurationError("record_every exceeds the number of sweeps")
+
+    def ladder(self) -> np.ndarray:
+        if self.temperatures is not None:
+            return np.asarray(self.temperatures, dtype=np.float64)
+        return build_ladder(self.replicas)
+
+
+@dataclass
+class RunRecord:
+    """Everything one run produced (executor.py:70-88, plus extensions)."""
+
+    config: SimulationConfig
+    temperatures: np.ndarray
+    energies: np.ndarray | None
+    magnetizations: np.ndarray | None
+    states: np.ndarray | None
+    swap_rounds: int
+    swaps_attempted: int
+    swaps_accepted: int
+    rng_positions: np.ndarray
+    round_entry_iterations: np.ndarray | None
+    init_seconds: float
+    exec_seconds: float
+    total_seconds: float
+    valid: bool = True
+    error: str | None = None
+    # --- extensions
+    sweep_mode: str = "exact"
+    swap_near_ties: int = 0
+    final_spins: np.ndarray | None = None
+    slot_to_row: np.ndarray | None = None
+
+
+def assign_replicas(replica_count: int, workers: int) -> list[tuple[int, int]]:
+    """Contiguous ranges, sizes differing by at most one (executor.py:91-102);
+    also the row sharding across GPUs (distributed.py)."""
+    if workers < 1:
+        raise ConfigurationError(f"workers must be >= 1, got {workers}")
+    base, extra = divmod(replica_count, workers)
+    bounds, lo = [], 0
+    for w in range(workers):
+        hi = lo + base + (1 if w < extra else 0)
+        bounds.append((lo, hi))
+        lo = hi
+    return bounds
+
+
+def _interval_plan(iterations: int, interval: int) -> list[tuple[int, int | None]]:
+    """(target count, swap round or None) per interval (executor.py:111-125)."""
+    plan: list[tuple[int, int | None]] = []
+    if interval > 0:
+        k = 1
+        while k * interval < iterations:
+            plan.append((k * interval, k - 1))
+            k += 1
+    plan.append((iterations, None))
+    return plan
+
+
+def _sync(dev):
+    torch.cuda.synchronize(dev)
+
+
+def run(config: SimulationConfig) -> RunRecord:
+    """Execute one simulation on the GPU: init phase, then synchronized
+    intervals.  Mid-run failures return a record flagged invalid
+    (executor.py:283-299); invalid configurations raise first."""
+    config.validate()
+    if config.sweep_mode == "checkerboard":
+        return _run_checkerboard(config)
+    return _run_exact(config)
+
+
+def _run_exact(config: SimulationConfig) -> RunRecord:
+    from .engine import ExactEngine, require_cuda
+
+    t_start = time.perf_counter()
+    R, L, N, I = config.replicas, config.side, config.iterations, config.swap_interval
+    rec_flag = RECORD_MODES.index(config.record_mode)
+    dev = require_cuda(config.device)
+    temps = config.ladder()
+    eng = None
+    errors: list[BaseException] = []
+    obs_e = obs_m = states = None
+    rounds = attempted = 0
+    snaps = None
+    init_seconds = exec_seconds = 0.0
+    with torch.cuda.device(dev):
+        t0 = time.perf_counter()
+        eng = ExactEngine(L, R, temps, config.seed, config.params.J, config.params.B,
+                          config.init_up_fraction, dev)
+        eng.init_state()
+        if rec_flag >= 1:
+            obs_e = torch.empty((R, N), dtype=torch.float64, device=dev)
+            obs_m = torch.empty((R, N), dtype=torch.float64, device=dev)
+        if rec_flag == 2:
+            states = torch.empty((R, N, L, L), dtype=torch.int8, device=dev)
+        eng.advance(0, 1, obs_e, obs_m, rec_flag, states)  # iteration 0 (executor.py:218-220)
+        _sync(dev)
+        init_seconds = time.perf_counter() - t0
+
+        t1 = time.perf_counter()
+        plan = _interval_plan(N, I)
+        n_rounds = sum(1 for _, ri in plan if ri is not None)
+        snaps = np.zeros((n_rounds, R), dtype=np.int64) if rec_flag >= 1 and n_rounds else None
+        completed = 1
+        try:
+            for target, ri in plan:
+                if target > completed:
+                    eng.advance(completed, target - completed, obs_e, obs_m, rec_flag, states)
+                completed = target
+                if ri is None:
+                    continue
+                if snaps is not None:
+                    snaps[ri, :] = completed  # == iters_done of every slot
+                rounds += 1
+                attempted += eng.exchange(ri)
+            _sync(dev)
+        except BaseException as exc:  # noqa: BLE001 - any failure invalidates the run
+            errors.append(exc)
+        exec_seconds = time.perf_counter() - t1
+
+    valid = not errors
+    accepted, near = eng.swap_counts() if valid else (0, 0)
+    return RunRecord(
+        config=config, temperatures=temps,
+        energies=obs_e.cpu().numpy() if (valid and obs_e is not None) else None,
+        magnetizations=obs_m.cpu().numpy() if (valid and obs_m is not None) else None,
+        states=states.cpu().numpy() if (valid and states is not None) else None,
+        swap_rounds=rounds, swaps_attempted=attempted, swaps_accepted=accepted,
+        rng_positions=eng.positions.cpu().numpy() if valid else np.zeros(R, np.int64),
+        round_entry_iterations=snaps, init_seconds=init_seconds, exec_seconds=exec_seconds,
+        total_seconds=time.perf_counter() - t_start, valid=valid,
+        error=None if valid else repr(errors[0]), sweep_mode="exact", swap_near_ties=near,
+        final_spins=eng.final_spins() if (valid and config.return_final_state) else None,
+        slot_to_row=eng.slot_to_row.cpu().numpy() if (valid and config.return_final_state) else None)
+
+
+def _run_checkerboard(config: SimulationConfig) -> RunRecord:
+    from .engine import CheckerboardEngine, require_cuda
+
+    t_start = time.perf_counter()
+    R, L = config.replicas, config.side
+    n_sites = L * L
+    sweeps, every_sw = config.iterations // n_sites, config.swap_interval // n_sites
+    record = config.record_mode != "none"
+    dev = require_cuda(config.device)
+    temps = config.ladder()
+    errors: list[BaseException] = []
+    with torch.cuda.device(dev):
+        t0 = time.perf_counter()
+        eng = CheckerboardEngine(L, R, temps, config.seed, config.params.J, config.params.B,
+                                 config.init_up_fraction, dev)
+        eng.init_state()
+        n_samples = sweeps // config.record_every if record else 0
+        obs_e = torch.empty((R, n_samples), dtype=torch.float64, device=dev) if record else None
+        obs_m = torch.empty((R, n_samples), dtype=torch.float64, device=dev) if record else None
+        _sync(dev)
+        init_seconds = time.perf_counter() - t0
+
+        t1 = time.perf_counter()
+        plan = _interval_plan(sweeps, every_sw)
+        n_rounds = sum(1 for _, ri in plan if ri is not None)
+        snaps = np.zeros((n_rounds, R), dtype=np.int64) if record and n_rounds else None
+        done = rounds = attempted = 0
+        try:
+            for target, ri in plan:
+                while done < target:
+                    if record:
+                        nxt = min(target, (done // config.record_every + 1) * config.record_every)
+                    else:
+                        nxt = target
+                    eng.sweeps(done, nxt - done)
+                    done = nxt
+                    if record and done % config.record_every == 0:
+                        eng.observe(obs_e, obs_m, done // config.record_every - 1)
+                if ri is None:
+                    continue
+                if snaps is not None:
+                    snaps[ri, :] = done * n_sites
+                rounds += 1
+                attempted += eng.exchange(ri)
+            _sync(dev)
+        except BaseException as exc:  # noqa: BLE001
+            errors.append(exc)
+        exec_seconds = time.perf_counter() - t1
+
+    valid = not errors
+    accepted, near = eng.swap_counts() if valid else (0, 0)
+    return RunRecord(
+        config=config, temperatures=temps,
+        energies=obs_e.cpu().numpy() if (valid and record) else None,
+        magnetizations=obs_m.cpu().numpy() if (valid and record) else None,
+        states=None, swap_rounds=rounds, swaps_attempted=attempted, swaps_accepted=accepted,
+        rng_positions=np.full(R, n_sites - 1, dtype=np.int64),
+        round_entry_iterations=snaps, init_seconds=init_seconds, exec_seconds=exec_seconds,
+        total_seconds=time.perf_counter() - t_start, valid=valid,
+        error=None if valid else repr(errors[0]), sweep_mode="checkerboard", swap_near_ties=near,
+        final_spins=eng.final_spins() if (valid and config.return_final_state) else None,
+        slot_to_row=eng.slot_to_row.cpu().numpy() if (valid and config.return_final_state) else None)

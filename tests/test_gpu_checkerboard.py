@@ -1,0 +1,168 @@
+"""Mode F (checkerboard, multispin-coded) on the GPU vs the CPU oracle:
+bit-exact final lattices, per-lattice stats, observables, swap decisions."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mods():
+    import paper_2512_03825_b200 as p
+    from paper_2512_03825_b200 import engine, kernels, tables
+    return p, engine, kernels, tables
+
+
+def _rand_spins(R, L, seed):
+    rs = np.random.default_rng(seed)
+    return (rs.integers(0, 2, size=(R, L, L)) * 2 - 1).astype(np.int8)
+
+
+@pytest.mark.parametrize("L", [2, 4, 6, 10, 32, 64, 128, 192])
+def test_pack_unpack_roundtrip_and_stats(mods, L):
+    p, engine, _, _ = mods
+    R = 3
+    sp = _rand_spins(R, L, L)
+    eng = engine.CheckerboardEngine(L, R, p.build_ladder(R), 1, 1.0, 0.0, 0.5, 0)
+    eng.load_spins(torch.from_numpy(sp))
+    assert np.array_equal(eng.final_spins(), sp)
+    st = eng.local_stats.cpu().numpy()
+    assert np.array_equal(st, oracle.row_stats(sp))
+    assert np.array_equal(eng.audit_stats().cpu().numpy(), st)
+
+
+@pytest.mark.parametrize("L,R,J,B,seed,nsweeps", [
+    (64, 4, 1.0, 0.0, 42, 5),      # fast path
+    (128, 3, 1.0, 0.0, 7, 4),
+    (192, 2, 0.8, 0.0, 9, 3),
+    (64, 3, 1.0, 0.5, 5, 4),       # field: 10-class path
+    (128, 2, -1.0, 0.25, 6, 3),    # antiferromagnet with field
+    (32, 5, 1.0, 0.0, 11, 6),      # generic path (L % 64 != 0)
+    (10, 4, 1.0, 0.3, 12, 8),
+    (2, 3, 1.0, 0.0, 13, 10),
+    (6, 2, 0.5, -0.5, 14, 10),
+])
+def test_sweeps_match_oracle(mods, L, R, J, B, seed, nsweeps):
+    p, engine, _, tables = mods
+    temps = p.build_ladder(R)
+    sp = _rand_spins(R, L, seed)
+    eng = engine.CheckerboardEngine(L, R, temps, seed, J, B, 0.5, 0)
+    perm = np.random.default_rng(seed).permutation(R)
+    eng.slot_to_row.copy_(torch.from_numpy(perm.astype(np.int64)))
+    r2s = np.empty(R, dtype=np.int64); r2s[perm] = np.arange(R)
+    eng.row_to_slot.copy_(torch.from_numpy(r2s.astype(np.int32)))
+    eng.load_spins(torch.from_numpy(sp))
+    eng.sweeps(3, nsweeps)
+    ref = sp.copy()
+    stats = oracle.row_stats(ref)
+    thr, always = oracle.cb_tables(1.0 / temps, J, B)
+    t_thr, t_always = tables.cb_tables(1.0 / temps, J, B)
+    assert np.array_equal(thr, t_thr) and always == (t_always & 0x3FF)
+    for t in range(3, 3 + nsweeps):
+        oracle.cb_sweep(ref, r2s, thr, always, seed, t, stats)
+    got = eng.final_spins()
+    assert np.array_equal(got, ref)
+    assert np.array_equal(eng.local_stats.cpu().numpy(), stats)
+    assert np.array_equal(eng.audit_stats().cpu().numpy(), stats)
+
+
+@pytest.mark.parametrize("L,R,sweeps,every,seed,J,B,rec_every", [
+    (64, 6, 20, 2, 42, 1.0, 0.0, 1),
+    (32, 8, 30, 1, 3, 1.0, 0.0, 3),
+    (128, 5, 12, 5, 4, 1.0, 0.1, 2),
+    (4, 7, 50, 3, 5, 1.0, 0.0, 1),
+])
+def test_run_matches_oracle(mods, L, R, sweeps, every, seed, J, B, rec_every):
+    p = mods[0]
+    cfg = p.SimulationConfig(side=L, replicas=R, iterations=sweeps * L * L,
+                             swap_interval=every * L * L, seed=seed,
+                             params=p.IsingParams(J=J, B=B), sweep_mode="checkerboard",
+                             record_every=rec_every, return_final_state=True)
+    rec = p.run(cfg)
+    assert rec.valid, rec.error
+    ref = oracle.run_checkerboard(L, R, sweeps, every, seed, J=J, B=B, record_every=rec_every)
+    assert np.array_equal(rec.final_spins, ref.final_spins)
+    assert np.array_equal(rec.slot_to_row, ref.slot_to_row)
+    assert np.array_equal(rec.energies, ref.energies)
+    assert np.array_equal(rec.magnetizations, ref.magnetizations)
+    assert (rec.swap_rounds, rec.swaps_attempted, rec.swaps_accepted) == \
+        (ref.swap_rounds, ref.swaps_attempted, ref.swaps_accepted)
+    assert rec.swap_near_ties == 0
+
+
+def test_host_interval_plugin_matches_oracle(mods):
+    p, _, kernels, _ = mods
+    L, R, seed = 64, 8, 21
+    temps = p.build_ladder(R)
+    betas = 1.0 / temps
+    sp = np.empty((R, L, L), dtype=np.int8)
+    for r in range(R):
+        oracle.fill_lattice(sp[r], L * L // 2, seed, r, 0)
+    ref = sp.copy()
+    s2r = np.arange(R, dtype=np.int64)
+    ref_s2r = s2r.copy()
+    stats = oracle.row_stats(ref)
+    thr, always = oracle.cb_tables(betas, 1.0, 0.0)
+    done = 0
+    for rnd in range(4):
+        e = np.zeros(R); ss = np.zeros(R, dtype=np.int64)
+        acc = kernels.cb_interval(sp, s2r, betas, 1.0, 0.0, seed, done, 3, rnd, e, ss)
+        r2s = np.empty(R, dtype=np.int64); r2s[ref_s2r] = np.arange(R)
+        for t in range(done, done + 3):
+            oracle.cb_sweep(ref, r2s, thr, always, seed, t, stats)
+        done += 3
+        s = stats[ref_s2r]
+        re = 0.0 * s[:, 0] - 1.0 * s[:, 1].astype(np.float64)
+        rs_ = s[:, 0].copy()
+        racc = oracle.swap_chunk(ref_s2r, re, rs_, betas, seed, R, rnd, rnd % 2, 0,
+                                 (R - rnd % 2) // 2)
+        assert acc == racc
+        assert np.array_equal(sp, ref)
+        assert np.array_equal(s2r, ref_s2r)
+        assert np.array_equal(e, re) and np.array_equal(ss, rs_)
+
+
+def test_c3_scale_properties(mods):
+    """BASELINE C3 shape (1024^2, 256 replicas): incremental stats equal the
+    recomputed ones after an exchange interval, the run is deterministic, and
+    the spin sums stay consistent with the packed state."""
+    p, engine, _, _ = mods
+    L, R = 1024, 256
+    temps = p.build_ladder(R)
+    outs = []
+    for _ in range(2):
+        eng = engine.CheckerboardEngine(L, R, temps, 42, 1.0, 0.0, 0.5, 0)
+        eng.init_state()
+        eng.sweeps(0, 10)
+        eng.exchange(0)
+        eng.sweeps(10, 2)
+        st = eng.local_stats.clone()
+        assert torch.equal(eng.audit_stats(), st)
+        outs.append((st.cpu().numpy(), eng.slot_to_row.cpu().numpy(),
+                     eng.packed.view(torch.int64).sum().item()))
+        del eng
+        torch.cuda.empty_cache()
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1])
+    assert outs[0][2] == outs[1][2]
+
+
+def test_one_lattice_matches_oracle_at_1024(mods):
+    p, engine, _, _ = mods
+    L, R = 1024, 2
+    temps = np.array([1.5, 2.269])
+    eng = engine.CheckerboardEngine(L, R, temps, 5, 1.0, 0.0, 0.5, 0)
+    eng.init_state()
+    sp0 = eng.final_spins()
+    eng.sweeps(0, 2)
+    ref = sp0.copy()
+    stats = oracle.row_stats(ref)
+    thr, always = oracle.cb_tables(1.0 / temps, 1.0, 0.0)
+    for t in range(2):
+        oracle.cb_sweep(ref, np.arange(R, dtype=np.int64), thr, always, 5, t, stats)
+    assert np.array_equal(eng.final_spins(), ref)
+    assert np.array_equal(eng.local_stats.cpu().numpy(), stats)
