@@ -44,8 +44,12 @@ static uint32_t cb_tables(const double* betas, int64_t R, double J, double B, st
     thr.assign((size_t)R * 10, 0xffffffffu);
     for (int c = 0; c < 10; ++c) {
         const double d = class_delta(c, J, B);
-        if (d <= 0.0) {
+        if (d < 0.0) {
             always |= 1u << c;
+            continue;
+        }
+        if (d == 0.0) {  // neutral: probability 1/2
+            for (int64_t k = 0; k < R; ++k) thr[(size_t)k * 10 + c] = 0x80000000u;
             continue;
         }
         for (int64_t k = 0; k < R; ++k) {

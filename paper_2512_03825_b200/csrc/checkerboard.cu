@@ -44,7 +44,7 @@ struct ClassPlan {
 __device__ __forceinline__ void decide_word(uint32_t S, uint32_t n1, uint32_t n2, uint32_t n3,
                                             uint32_t n4, uint32_t valid, uint32_t w,
                                             uint32_t h_base, int slot, uint32_t ctr1,
-                                            uint32_t key0, uint32_t key1, const ClassPlan& plan,
+                                            const RoundKeys32& rk, const ClassPlan& plan,
                                             const uint32_t* __restrict__ thr_slot,
                                             uint32_t& acc_out, int& dS, int& dB) {
     // aligned-neighbour indicators and their bit-sliced sum k = k0 + 2 k1 + 4 k2
@@ -77,8 +77,8 @@ __device__ __forceinline__ void decide_word(uint32_t S, uint32_t n1, uint32_t n2
     }
     uint32_t acc = valid & ~uphill;  // dE <= 0: always accepted
     if (uphill) {
-        const uint4 r0 = philox4x32_10(make_uint4(2u * w, ctr1, (uint32_t)slot, 0u), key0, key1);
-        const uint4 r1 = philox4x32_10(make_uint4(2u * w + 1u, ctr1, (uint32_t)slot, 0u), key0, key1);
+        const uint4 r0 = philox4x32_10(make_uint4(2u * w, ctr1, (uint32_t)slot, 0u), rk);
+        const uint4 r1 = philox4x32_10(make_uint4(2u * w + 1u, ctr1, (uint32_t)slot, 0u), rk);
         const uint32_t U[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
         uint32_t lt = 0, eq = uphill;
 #pragma unroll
@@ -99,8 +99,7 @@ __device__ __forceinline__ void decide_word(uint32_t S, uint32_t n1, uint32_t n2
 #pragma unroll
             for (int q = 0; q < 10; ++q)
                 if (q < plan.n_up && ((M[q] >> bit) & 1u)) t24 = thr[q] & 0x00ffffffu;
-            const uint4 r2 = philox4x32_10(make_uint4(h_base + (uint32_t)bit, ctr1, (uint32_t)slot, 1u),
-                                           key0, key1);
+            const uint4 r2 = philox4x32_10(make_uint4(h_base + (uint32_t)bit, ctr1, (uint32_t)slot, 1u), rk);
             if ((r2.x >> 8) < t24) acc |= 1u << bit;
         }
     }
@@ -135,7 +134,7 @@ template <int kRows>
 __global__ void __launch_bounds__(256) cb_half_sweep_fast(
     uint32_t* __restrict__ packed, int64_t rows, int L, int WR, int64_t W,
     const int32_t* __restrict__ row_to_slot, const uint32_t* __restrict__ thresh, ClassPlan plan,
-    uint32_t key0, uint32_t key1, uint32_t ctr1, int color, int64_t* __restrict__ stats) {
+    const RoundKeys32 rk, uint32_t ctr1, int color, int64_t* __restrict__ stats) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int strips = L / kRows;
     const int64_t per_lat = (int64_t)strips * WR;
@@ -176,11 +175,175 @@ __global__ void __launch_bounds__(256) cb_half_sweep_fast(
             }
             uint32_t acc;
             decide_word(S, O[rr], O[rr + 2], mid, hz, 0xffffffffu, (uint32_t)wi, (uint32_t)(wi * 32),
-                        slot, ctr1, key0, key1, plan, thr_slot, acc, dS, dB);
+                        slot, ctr1, rk, plan, thr_slot, acc, dS, dB);
             if (acc) own[wi] = S ^ acc;
         }
     }
     flush_stats(stats, lat, active, dS, dB);
+}
+
+// ------------------------------------ fast path, J > 0 and B = 0 (ferro) --
+// The benchmark and paper setting.  k = 0, 1 aligned neighbours (dE < 0) are
+// always accepted, k = 2 (dE = 0) with probability 1/2 (u < 2^31: random
+// plane 0 clear), k = 3 (dE = 4J) and k = 4 (dE = 8J) against thresholds
+// t3 = thr[slot][8], t4 = thr[slot][9] for both spin signs, so the per-site
+// threshold plane is a select on K4.
+//
+// Rows are walked with a rolling window of the other colour's words (one new
+// load per row).  Ties on the top random byte are queued per warp in shared
+// memory and resolved 32 per secondary-Philox pass after the row loop; an
+// accepted tie flips its spin with atomicXor (the owner already stored the
+// word).  Statistics: the colour-0 pass zeroes the lattice's (S, Bond); the
+// colour-1 pass recomputes them from the new configuration -- S from both
+// colours' words, Bond = sum over colour-1 sites of s*nb (every bond has
+// exactly one colour-1 end) -- plus the deltas of its own tie flips.
+constexpr int kQCap = 128;
+
+template <int kRows, bool kStats>
+__global__ void __launch_bounds__(256) cb_half_sweep_ferro(
+    uint32_t* __restrict__ packed, int64_t rows, int L, int WR, int64_t W,
+    const int32_t* __restrict__ row_to_slot, const uint32_t* __restrict__ thresh, const RoundKeys32 rk,
+    uint32_t ctr1, int color, int64_t* __restrict__ stats) {
+    constexpr int kWarps = 8;
+    __shared__ uint32_t q_gw[kWarps][kQCap], q_h[kWarps][kQCap], q_sl[kWarps][kQCap], q_info[kWarps][kQCap];
+    __shared__ uint32_t q_res[kWarps], q_ok[kWarps];
+    __shared__ int extra_s[kWarps][32], extra_b[kWarps][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (kStats) {
+        extra_s[warp][lane] = 0;
+        extra_b[warp][lane] = 0;
+    }
+    if (lane == 0) { q_res[warp] = 0; q_ok[warp] = 0; }
+    __syncwarp();
+
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int strips = L / kRows;
+    const int64_t per_lat = (int64_t)strips * WR;
+    const bool active = tid < rows * per_lat;
+    const int64_t lat = active ? tid / per_lat : 0;
+    const int rem = (int)(tid - lat * per_lat);
+    const int strip = rem / WR;
+    const int k = rem - strip * WR;
+    int sumS = 0, sumB = 0;
+    if (active) {
+        if (!kStats && rem == 0) {  // colour-0 pass: reset, colour-1 pass recomputes
+            stats[2 * lat] = 0;
+            stats[2 * lat + 1] = 0;
+        }
+        const uint32_t own_base = (uint32_t)((lat * 2 + color) * W);
+        const uint32_t* __restrict__ other = packed + (lat * 2 + (1 - color)) * W;
+        uint32_t* __restrict__ own = packed + own_base;
+        const int slot = row_to_slot[lat];
+        const uint32_t t3 = __ldg(thresh + slot * 10 + 8);
+        const uint32_t t4 = __ldg(thresh + slot * 10 + 9);
+        uint32_t TA[8], TB[8];
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+            TA[p] = 0u - ((t3 >> (31 - p)) & 1u);
+            TB[p] = 0u - ((t4 >> (31 - p)) & 1u);
+        }
+        const int kl = (k == 0) ? WR - 1 : k - 1;
+        const int kr = (k == WR - 1) ? 0 : k + 1;
+        const int i0 = strip * kRows;
+        uint32_t up = __ldg(other + (i0 == 0 ? L - 1 : i0 - 1) * WR + k);
+        uint32_t mid = __ldg(other + i0 * WR + k);
+#pragma unroll 2
+        for (int rr = 0; rr < kRows; ++rr) {
+            const int i = i0 + rr;
+            const int row = i * WR;
+            const uint32_t dn = __ldg(other + (i + 1 == L ? 0 : row + WR) + k);
+            const uint32_t S = own[row + k];
+            uint32_t hz;
+            if (((i + color) & 1) == 0) {
+                hz = __funnelshift_l(__ldg(other + row + kl), mid, 1);  // site m sees m-1
+            } else {
+                hz = __funnelshift_r(mid, __ldg(other + row + kr), 1);  // site m sees m+1
+            }
+            const uint32_t a = ~(S ^ up), b = ~(S ^ dn), c = ~(S ^ mid), d = ~(S ^ hz);
+            const uint32_t s1 = a ^ b, c1 = a & b, s2 = c ^ d, c2 = c & d;
+            const uint32_t k0 = s1 ^ s2, c3 = s1 & s2;
+            const uint32_t k1 = c1 ^ c2 ^ c3, K4 = c1 & c2;
+            const uint32_t upm = (k1 & k0) | K4;   // k = 3, 4
+            const uint32_t K2 = k1 & ~k0;          // k = 2: dE = 0
+            uint32_t acc = ~(k1 | K4);             // k = 0, 1: dE < 0
+            {
+                const uint32_t w32 = (uint32_t)(row + k);
+                const uint4 r0 = philox4x32_10(make_uint4(2u * w32, ctr1, (uint32_t)slot, 0u), rk);
+                const uint4 r1 = philox4x32_10(make_uint4(2u * w32 + 1u, ctr1, (uint32_t)slot, 0u), rk);
+                const uint32_t U[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+                acc |= K2 & ~U[0];  // neutral: u < 2^31 <=> top bit clear
+                uint32_t lt = 0, eq = upm;
+#pragma unroll
+                for (int p = 0; p < 8; ++p) {
+                    const uint32_t Tm = (K4 & TB[p]) | (~K4 & TA[p]);
+                    lt |= eq & ~U[p] & Tm;
+                    eq &= ~(U[p] ^ Tm);
+                }
+                acc |= lt;
+                if (eq) {  // ties on the top byte: queue them
+                    const uint32_t n = __popc(eq);
+                    const uint32_t off = atomicAdd(&q_res[warp], n);
+                    if (off + n <= kQCap) {
+                        atomicAdd(&q_ok[warp], n);
+                        uint32_t o = off;
+                        while (eq) {
+                            const int bit = __ffs(eq) - 1;
+                            eq &= eq - 1;
+                            const uint32_t k4 = (K4 >> bit) & 1u, sb = (S >> bit) & 1u;
+                            q_gw[warp][o] = own_base + w32;
+                            q_h[warp][o] = w32 * 32u + (uint32_t)bit;
+                            q_sl[warp][o] = (uint32_t)slot;
+                            q_info[warp][o] = ((k4 ? t4 : t3) & 0x00ffffffu) | (k4 << 24) | (sb << 25) |
+                                              ((uint32_t)lane << 26);
+                            ++o;
+                        }
+                    } else {  // queue full: resolve in place
+                        while (eq) {
+                            const int bit = __ffs(eq) - 1;
+                            eq &= eq - 1;
+                            const uint32_t t24 = (((K4 >> bit) & 1u) ? t4 : t3) & 0x00ffffffu;
+                            const uint4 r2 =
+                                philox4x32_10(make_uint4(w32 * 32u + (uint32_t)bit, ctr1, (uint32_t)slot, 1u), rk);
+                            if ((r2.x >> 8) < t24) acc |= 1u << bit;
+                        }
+                    }
+                }
+            }
+            const uint32_t Sn = S ^ acc;
+            if (acc) own[row + k] = Sn;
+            if (kStats) {
+                // new aligned masks: a flip toggles alignment with all four neighbours
+                const int kk = __popc(a ^ acc) + __popc(b ^ acc) + __popc(c ^ acc) + __popc(d ^ acc);
+                sumB += 2 * kk - 128;                                  // sum of s*nb = 2k - 4 per site
+                sumS += 2 * (__popc(Sn) + __popc(mid)) - 64;           // both colours' words
+            }
+            up = mid;
+            mid = dn;
+        }
+    }
+    __syncwarp();
+    const uint32_t nq = q_ok[warp];
+    for (uint32_t base = 0; base < nq; base += 32) {
+        const uint32_t e = base + (uint32_t)lane;
+        if (e < nq) {
+            const uint32_t h = q_h[warp][e], info = q_info[warp][e];
+            const uint4 r2 = philox4x32_10(make_uint4(h, ctr1, q_sl[warp][e], 1u), rk);
+            if ((r2.x >> 8) < (info & 0x00ffffffu)) {
+                atomicXor(packed + q_gw[warp][e], 1u << (h & 31u));
+                if (kStats) {
+                    const uint32_t owner = info >> 26;
+                    atomicAdd(&extra_s[warp][owner], ((info >> 25) & 1u) ? -2 : 2);
+                    atomicAdd(&extra_b[warp][owner], ((info >> 24) & 1u) ? -8 : -4);
+                }
+            }
+        }
+    }
+    if (kStats) {
+        __syncwarp();
+        sumS += extra_s[warp][lane];
+        sumB += extra_b[warp][lane];
+        flush_stats(stats, lat, active, sumS, sumB);
+    }
 }
 
 // ------------------------------------------------------- generic even L --
@@ -191,7 +354,7 @@ __device__ __forceinline__ uint32_t get_bit(const uint32_t* p, int64_t h) {
 __global__ void __launch_bounds__(256) cb_half_sweep_generic(
     uint32_t* __restrict__ packed, int64_t rows, int L, int64_t W,
     const int32_t* __restrict__ row_to_slot, const uint32_t* __restrict__ thresh, ClassPlan plan,
-    uint32_t key0, uint32_t key1, uint32_t ctr1, int color, int64_t* __restrict__ stats) {
+    const RoundKeys32 rk, uint32_t ctr1, int color, int64_t* __restrict__ stats) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool active = tid < rows * W;
     const int64_t lat = active ? tid / W : 0;
@@ -222,7 +385,7 @@ __global__ void __launch_bounds__(256) cb_half_sweep_generic(
         }
         const uint32_t S = own[w];
         uint32_t acc;
-        decide_word(S, n1, n2, n3, n4, valid, (uint32_t)w, (uint32_t)(w * 32), slot, ctr1, key0, key1,
+        decide_word(S, n1, n2, n3, n4, valid, (uint32_t)w, (uint32_t)(w * 32), slot, ctr1, rk,
                     plan, thresh + (int64_t)slot * 10, acc, dS, dB);
         if (acc) own[w] = S ^ acc;
     }
@@ -367,22 +530,34 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
                      int64_t n_sweeps, int64_t* stats, cudaStream_t s) {
     if (rows == 0 || n_sweeps == 0) return PTMH_OK;
     const ClassPlan plan = make_plan(always_mask);
-    const uint32_t key0 = (uint32_t)seed, key1 = (uint32_t)(seed >> 32);
+    const RoundKeys32 rk = make_round_keys32(seed);
     const int64_t W = cb_words(L);
     const bool fast = (L % 64) == 0 && (L % kFastRows) == 0;
+    // symmetric thresholds, k <= 1 always, k = 2 neutral (1/2), k = 3, 4 uphill
+    const bool ferro = (always_mask & kSymmetricFlag) && (always_mask & 0x3ffu) == 0x078u &&
+                       rows * 2 * W < (1LL << 32);  // 32-bit word offsets in the tie queue
     for (int64_t t = first_sweep; t < first_sweep + n_sweeps; ++t) {
         for (int color = 0; color < 2; ++color) {
             const uint32_t ctr1 = (uint32_t)(2 * t + color);
-            if (fast) {
+            if (fast && ferro) {
+                const int WR = (int)(L / 64);
+                const int64_t threads = rows * (L / kFastRows) * WR;
+                if (color == 0)
+                    cb_half_sweep_ferro<kFastRows, false><<<ceil_div(threads, 256), 256, 0, s>>>(
+                        packed, rows, (int)L, WR, W, row_to_slot, thresh, rk, ctr1, color, stats);
+                else
+                    cb_half_sweep_ferro<kFastRows, true><<<ceil_div(threads, 256), 256, 0, s>>>(
+                        packed, rows, (int)L, WR, W, row_to_slot, thresh, rk, ctr1, color, stats);
+            } else if (fast) {
                 const int WR = (int)(L / 64);
                 const int64_t threads = rows * (L / kFastRows) * WR;
                 cb_half_sweep_fast<kFastRows><<<ceil_div(threads, 256), 256, 0, s>>>(
-                    packed, rows, (int)L, WR, W, row_to_slot, thresh, plan, key0, key1, ctr1, color,
+                    packed, rows, (int)L, WR, W, row_to_slot, thresh, plan, rk, ctr1, color,
                     stats);
             } else {
                 const int64_t threads = rows * W;
                 cb_half_sweep_generic<<<ceil_div(threads, 256), 256, 0, s>>>(
-                    packed, rows, (int)L, W, row_to_slot, thresh, plan, key0, key1, ctr1, color, stats);
+                    packed, rows, (int)L, W, row_to_slot, thresh, plan, rk, ctr1, color, stats);
             }
             PTMH_LAUNCH_CHECK();
         }

@@ -62,4 +62,32 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
     return c;
 }
 
+// Round keys of one Philox4x32-10 key, precomputed on the host and passed as a
+// kernel parameter: the XORs then read them straight from the constant bank.
+struct RoundKeys32 {
+    uint32_t k0[10], k1[10];
+};
+
+inline RoundKeys32 make_round_keys32(uint64_t seed) {
+    RoundKeys32 rk;
+    uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+    for (int r = 0; r < 10; ++r) {
+        rk.k0[r] = k0;
+        rk.k1[r] = k1;
+        k0 += kPh32W0;
+        k1 += kPh32W1;
+    }
+    return rk;
+}
+
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, const RoundKeys32& rk) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t hi0 = __umulhi(kPh32M0, c.x), lo0 = kPh32M0 * c.x;
+        const uint32_t hi1 = __umulhi(kPh32M1, c.z), lo1 = kPh32M1 * c.z;
+        c = make_uint4(hi1 ^ c.y ^ rk.k0[r], lo1, hi0 ^ c.w ^ rk.k1[r], lo0);
+    }
+    return c;
+}
+
 }  // namespace ptmh

@@ -6,7 +6,8 @@ libm (kernels.py:98).  Both GPU chains look the value up instead:
 * exact chain:  tbl[k, c] = math.exp(-beta_k * d_c), compared against the
   FP64 uniform exactly as the reference compares it;
 * checkerboard: thr[k, c] = floor(math.exp(-beta_k * d_c) * 2^32), compared
-  against a 32-bit uniform.
+  against a 32-bit uniform; dE < 0 always accepted, dE == 0 accepted with
+  probability 1/2 (threshold 2^31) -- DESIGN.md section 3.2.
 
 Python's math.exp is the host libm exp numba's math.exp lowers to, so the
 tables reproduce the reference's acceptance decisions bit for bit.
@@ -44,8 +45,11 @@ def cb_tables(betas: np.ndarray, J: float, B: float) -> tuple[np.ndarray, int]:
     always = 0
     for c in range(N_CLASSES):
         d = class_delta(c, J, B)
-        if d <= 0.0:
+        if d < 0.0:
             always |= 1 << c
+            continue
+        if d == 0.0:  # neutral: probability 1/2 keeps the checkerboard chain irreducible
+            thr[:, c] = 0x80000000
             continue
         for k, beta in enumerate(np.asarray(betas, dtype=np.float64)):
             p = math.exp(-float(beta) * d)

@@ -1,0 +1,32 @@
+"""Time the checkerboard sweep kernels alone (CUDA events), per config.
+
+    python tools/time_sweep.py c3 c5 ...
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from bench import CONFIGS  # noqa: E402
+from paper_2512_03825_b200 import build_ladder  # noqa: E402
+from paper_2512_03825_b200.engine import CheckerboardEngine  # noqa: E402
+
+for name in (sys.argv[1:] or ["c3"]):
+    L, R, every, _ = CONFIGS[name]
+    eng = CheckerboardEngine(L, R, build_ladder(R), 42, 1.0, 0.0, 0.5, 0)
+    eng.init_state()
+    n = max(2, min(200, int(4e9 // (R * L * L))))
+    eng.sweeps(0, 2)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    eng.sweeps(2, n)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    print(f"{name}: L={L} R={R} {n} sweeps {ms:.3f} ms -> {n * R * L * L / ms / 1e9:.4g} G attempts/s "
+          f"({ms / n * 1e3:.1f} us/sweep)", flush=True)
+    del eng
+    torch.cuda.empty_cache()
