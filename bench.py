@@ -95,7 +95,7 @@ class ClockSampler:
                     self.samples.append([x.strip() for x in out.split(",")])
             except Exception:  # noqa: BLE001
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.05)
 
     def __enter__(self):
         self._t.start()
@@ -157,8 +157,8 @@ def host_cores():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--no-e2e", action="store_true")
@@ -181,6 +181,9 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
+        config = dict(config, sweep="reference random-site chain (kernels.py:62-113), int8 spins",
+                      parallelism=f"{host_cores()} host threads over replica blocks "
+                                  "(executor.py:227-245)", l2="n/a (CPU)")
         threads = host_cores()
         per_slot = max(1000, int(2.5e7 // R))  # ~1 s of 8-core work per step
         for _ in range(args.warmup):
@@ -247,12 +250,11 @@ def main():
         state["sweep"] += every
         state["round"] += 1
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-
     step_ms, sweep_ms = [], []
     with ClockSampler(local_rank) as clk:
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
         for _ in range(args.steps):
             flush.zero_()
             ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -325,7 +327,7 @@ def main():
                 "config": config,
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak, "traffic": traffic,
-                             "kernel": "cb_half_sweep_fast", "launch_ms": launch_ms,
+                             "kernel": "cb_half_sweep_ferro<8,0|1>", "launch_ms": launch_ms,
                              "alg_bytes_per_launch": bytes_per_launch, "peak_kind": peak_kind,
                              "note": "issue-bound (Philox + bit-sliced logic), see DESIGN.md 5"},
                 "cpu_baseline": cpu, "e2e": e2e,
