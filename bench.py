@@ -46,6 +46,9 @@ CONFIGS = {
     "c4": (4096, 512, 10, "2D Ising 4096x4096, 512 replicas, exchange every 10 sweeps"),
     "c5": (64, 4096, 1, "2D Ising 64x64, 4096 replicas, exchange every sweep"),
 }
+# exchange intervals per timed step: one for the big lattices, 100 (one
+# persistent launch of 100 sweeps + 100 rounds) where an interval is 1 sweep
+INTERVALS_PER_STEP = {"c1": 100, "c2": 100, "c3": 1, "c4": 1, "c5": 100}
 SEED = 42
 ALG_BYTES_PER_ATTEMPT = 0.25  # 1-bit multispin coding: read + write one bit
 
@@ -170,8 +173,10 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     L, R, every, desc = CONFIGS[args.config]
-    attempts_per_step = R * L * L * every
-    config = {"workload": desc, "side": L, "replicas": R, "sweeps_per_step": every,
+    ips = INTERVALS_PER_STEP[args.config]
+    attempts_per_step = R * L * L * every * ips
+    config = {"workload": desc, "side": L, "replicas": R, "sweeps_per_step": every * ips,
+              "exchange_rounds_per_step": ips,
               "attempts_per_step": attempts_per_step, "J": 1.0, "B": 0.0,
               "ladder": "geometric 4^(i/(R-1))" if args.config == "c1" else "linear 1+3i/R",
               "sweep": "checkerboard, 1-bit multispin", "l2": "flushed between steps (256 MiB write)",
@@ -233,9 +238,23 @@ def main():
     stream = torch.cuda.current_stream()
 
     state = {"sweep": 0, "round": 0}
+    from paper_2512_03825_b200.executor import _resident_wins
+    resident = world == 1 and _resident_wins(L, every)
+    big = 1 << 30  # run length for the resident kernel: every interval ends in a round
 
     def step(sweep_events=None):
         t0 = state["sweep"]
+        if resident:  # one persistent launch = `ips` intervals, sweeps + exchange rounds
+            if sweep_events is not None:
+                sweep_events[0][0].record(stream)
+            eng.run_resident(t0, every * ips, big, every)
+            if sweep_events is not None:
+                sweep_events[0][1].record(stream)
+            state["sweep"] += every * ips
+            state["round"] += ips
+            return
+        if ips != 1:
+            raise ValueError("multi-interval steps are only defined for the resident path")
         if sweep_events is None:
             eng.sweeps(t0, every)
         else:
@@ -258,7 +277,7 @@ def main():
         for _ in range(args.steps):
             flush.zero_()
             ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                  for _ in range(every)]
+                  for _ in range(1 if resident else every)]
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             if world > 1:
                 dist.barrier()
@@ -275,9 +294,16 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     value = args.steps * attempts_per_step / (total_ms / 1e3)
-    launch_ms = statistics.mean(sweep_ms) / 2.0  # two colour launches per sweep
     local_rows = eng.rows
-    bytes_per_launch = ALG_BYTES_PER_ATTEMPT * local_rows * L * L / 2
+    if resident:  # one launch per step: `every` sweeps of every lattice + the round
+        sweep_ms = [m for m in sweep_ms if m > 0]
+        launch_ms = statistics.mean(sweep_ms)
+        bytes_per_launch = ALG_BYTES_PER_ATTEMPT * local_rows * L * L * every * ips
+        kernel_name = "cb_resident_kernel<fast,ferro>"
+    else:
+        launch_ms = statistics.mean(sweep_ms) / 2.0  # two colour launches per sweep
+        bytes_per_launch = ALG_BYTES_PER_ATTEMPT * local_rows * L * L / 2
+        kernel_name = "cb_half_sweep_ferro<8,0|1>"
     achieved = bytes_per_launch / (launch_ms / 1e3) / 1e9
     peak, peak_kind = _peaks()
     traffic = _traffic(args.config) if world == 1 else None
@@ -304,7 +330,7 @@ def main():
             sweep0 += every
             rnd0 += 1
         dt = time.perf_counter() - t0
-        e2e = {"value": n_e2e * attempts_per_step / dt, "unit": "attempts/s",
+        e2e = {"value": n_e2e * R * L * L * every / dt, "unit": "attempts/s",
                "h2d_bytes_per_step": int(R * L * L + R * 8 + R * 40 + R * 4 + R * 8),
                "d2h_bytes_per_step": int(R * L * L + R * 8 * 3 + 16),
                "path": "kernels.cb_interval -> ptmh_host_cb_interval (pinned int8 lattices)"}
@@ -327,11 +353,11 @@ def main():
                 "config": config,
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak, "traffic": traffic,
-                             "kernel": "cb_half_sweep_ferro<8,0|1>", "launch_ms": launch_ms,
+                             "kernel": kernel_name, "launch_ms": launch_ms,
                              "alg_bytes_per_launch": bytes_per_launch, "peak_kind": peak_kind,
                              "note": "issue-bound (Philox + bit-sliced logic), see DESIGN.md 5"},
                 "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": args.steps * (2 * every + 2),
+                "gpu_launches": args.steps * (1 if resident else 2 * every + 2),
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:

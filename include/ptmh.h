@@ -145,6 +145,25 @@ int ptmh_cb_sweeps(uint32_t *packed, int64_t rows, int64_t L,
                    uint32_t always_mask, uint64_t seed, int64_t first_sweep,
                    int64_t n_sweeps, int64_t *stats, void *stream);
 
+/* Persistent single-device run segment (csrc/resident.cu): sweeps
+ * first_sweep .. first_sweep+n_sweeps-1 of a run of total_sweeps sweeps,
+ * with the swap rounds (every swap_every sweeps, strictly before the end,
+ * executor.py:111-125) and observations (every record_every sweeps, by slot,
+ * before the round; record_every 0 = none) inside ONE cooperative launch.
+ * slot_to_row2 (2, R) int64 / row_to_slot2 (2, R) int32 are double buffers;
+ * `buf` names the one holding the current permutation, *buf_out receives the
+ * one holding it afterwards.  stats (R, 2) hold every lattice's (S, Bond)
+ * after the segment.  Same chain and random numbers as ptmh_cb_sweeps. */
+int ptmh_cb_run_resident(uint32_t *packed, int64_t R, int64_t L,
+                         int64_t *slot_to_row2, int32_t *row_to_slot2, int buf,
+                         const uint32_t *thresh, uint32_t always_mask,
+                         uint64_t seed, double J, double B, const double *betas,
+                         int64_t *stats, int64_t *counters, double *obs_e,
+                         double *obs_m, int64_t ncols, int64_t first_sweep,
+                         int64_t n_sweeps, int64_t total_sweeps,
+                         int64_t swap_every, int64_t record_every, int *buf_out,
+                         void *stream);
+
 /* Per-lattice (S, Bond) recomputed from the packed state (audit of the
  * incremental stats; L % 64 == 0 or any even L). */
 int ptmh_cb_row_stats(const uint32_t *packed, int64_t rows, int64_t L,

@@ -11,7 +11,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libptmh.so")
+# PTMH_LIB overrides the path (A/B builds of the same sources; tools/ only)
+LIB_PATH = os.environ.get("PTMH_LIB") or os.path.join(_HERE, "libptmh.so")
 
 
 class PtmhError(RuntimeError):
@@ -49,6 +50,8 @@ def _load():
         "ptmh_cb_unpack": ([P, i64, i64, P, P], i32),
         "ptmh_cb_sweeps": ([P, i64, i64, P, P, u32, u64, i64, i64, P, P], i32),
         "ptmh_cb_row_stats": ([P, i64, i64, P, P], i32),
+        "ptmh_cb_run_resident": ([P, i64, i64, P, P, i32, P, u32, u64, f64, f64, P, P, P, P, P,
+                                  i64, i64, i64, i64, i64, i64, P, P], i32),
         "ptmh_cb_slot_energies": ([P, P, i64, f64, f64, P, P, P], i32),
         "ptmh_cb_observe": ([P, P, i64, i64, f64, f64, P, P, i64, i64, P], i32),
     }

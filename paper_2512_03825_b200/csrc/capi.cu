@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -75,7 +77,7 @@ struct Workspace {
     int device = -1;
     std::vector<Buf> bufs;
     cudaStream_t s[3] = {nullptr, nullptr, nullptr};
-    cudaEvent_t ev_in[64], ev_out[64];
+    cudaEvent_t ev_in[64], ev_out[64];  // >= chunks per pipelined call
     bool events = false;
 };
 
@@ -188,6 +190,53 @@ int ptmh_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* row
                    "checkerboard sweep index must stay below 2^31");
     return launch_cb_sweeps(packed, rows, L, row_to_slot, thresh, always_mask, seed, first_sweep, n_sweeps,
                             stats, as_stream(stream));
+}
+
+int ptmh_cb_run_resident(uint32_t* packed, int64_t R, int64_t L, int64_t* slot_to_row2, int32_t* row_to_slot2,
+                         int buf, const uint32_t* thresh, uint32_t always_mask, uint64_t seed, double J, double B,
+                         const double* betas, int64_t* stats, int64_t* counters, double* obs_e, double* obs_m,
+                         int64_t ncols, int64_t first_sweep, int64_t n_sweeps, int64_t total_sweeps,
+                         int64_t swap_every, int64_t record_every, int* buf_out, void* stream) {
+    PTMH_CHECK_ARG(L >= 2 && L % 2 == 0 && L <= 65536 && R >= 1 && R < (1LL << 26), "resident shape");
+    PTMH_CHECK_ARG(buf == 0 || buf == 1, "resident buffer index");
+    PTMH_CHECK_ARG(first_sweep >= 0 && n_sweeps >= 0 && first_sweep + n_sweeps <= total_sweeps &&
+                       total_sweeps < (1LL << 31), "resident sweep range");
+    PTMH_CHECK_ARG(record_every == 0 || (obs_e && obs_m && total_sweeps / record_every <= ncols),
+                   "resident observables");
+    ResidentArgs a{};
+    a.packed = packed;
+    a.R = (int)R;
+    a.L = (int)L;
+    a.W = (int)cb_words(L);
+    a.WR = (L % 64 == 0) ? (int)(L / 64) : 0;
+    a.thresh = thresh;
+    a.rk = make_round_keys32(seed);
+    a.seed = seed;
+    a.J = J;
+    a.B = B;
+    a.betas = betas;
+    a.s2r[0] = slot_to_row2;
+    a.s2r[1] = slot_to_row2 + R;
+    a.r2s[0] = row_to_slot2;
+    a.r2s[1] = row_to_slot2 + R;
+    a.stats = stats;
+    a.counters = counters;
+    a.obs_e = obs_e;
+    a.obs_m = obs_m;
+    a.ncols = ncols;
+    a.first_sweep = first_sweep;
+    a.n_sweeps = n_sweeps;
+    a.total_sweeps = total_sweeps;
+    a.swap_every = swap_every;
+    a.record_every = record_every;
+    a.buf = buf;
+    fill_class_plan(always_mask, &a.n_up, a.up_k, a.up_sf, a.up_cls, &a.ferro);
+    int rounds = 0;
+    for (int64_t d = first_sweep + 1; d <= first_sweep + n_sweeps; ++d)
+        if (swap_every > 0 && d % swap_every == 0 && d < total_sweeps) ++rounds;
+    if (buf_out) *buf_out = buf ^ (rounds & 1);
+    if (n_sweeps == 0) return PTMH_OK;
+    return launch_cb_resident(a, a.WR > 0, as_stream(stream), nullptr);
 }
 
 int ptmh_cb_row_stats(const uint32_t* packed, int64_t rows, int64_t L, int64_t* stats, void* stream) {
@@ -357,6 +406,11 @@ int ptmh_host_cb_interval(int8_t* spins, int64_t R, int64_t L, int64_t* slot_to_
     std::lock_guard<std::mutex> lk(g_ws.mu);
     PTMH_TRY(ws_prepare(g_ws));
     cudaStream_t sin = g_ws.s[0], sc = g_ws.s[1], sout = g_ws.s[2];
+    if (getenv("PTMH_DEBUG")) {
+        cudaPointerAttributes pa;
+        cudaError_t e = cudaPointerGetAttributes(&pa, spins);
+        fprintf(stderr, "ptmh: spins %p attr rc=%d type=%d\n", (void*)spins, (int)e, (int)pa.type);
+    }
     const int64_t nsite = L * L, W = cb_words(L);
     int8_t* d_spins; uint32_t *d_packed, *d_thr; int64_t *d_stats, *d_s2r, *d_sums, *d_cnt;
     int32_t* d_r2s; double *d_b, *d_e;
@@ -375,20 +429,35 @@ int ptmh_host_cb_interval(int8_t* spins, int64_t R, int64_t L, int64_t* slot_to_
     PTMH_CUDA(cudaMemcpyAsync(d_r2s, r2s.data(), R * 4, cudaMemcpyHostToDevice, sc));
     PTMH_CUDA(cudaMemcpyAsync(d_b, betas, R * 8, cudaMemcpyHostToDevice, sc));
     PTMH_CUDA(cudaMemsetAsync(d_cnt, 0, 16, sc));
-    // pipeline: H2D chunk c | pack + stats + sweeps + unpack chunk c | D2H chunk c
+    // pipeline over replica chunks: all H2D copies are issued first, then the
+    // compute chain (each chunk waits for its copy), then the D2H copies (each
+    // waits for its chunk), so no queue ever blocks behind a later dependency
     const int64_t nch = std::min<int64_t>(R, 8);
+    auto chunk = [&](int64_t c, int64_t& lo, int64_t& n) {
+        lo = R * c / nch;
+        n = R * (c + 1) / nch - lo;
+    };
     for (int64_t c = 0; c < nch; ++c) {
-        const int64_t lo = R * c / nch, hi = R * (c + 1) / nch, n = hi - lo;
+        int64_t lo, n;
+        chunk(c, lo, n);
         PTMH_CUDA(cudaMemcpyAsync(d_spins + lo * nsite, spins + lo * nsite, (size_t)(n * nsite),
                                   cudaMemcpyHostToDevice, sin));
         PTMH_CUDA(cudaEventRecord(g_ws.ev_in[c], sin));
+    }
+    for (int64_t c = 0; c < nch; ++c) {
+        int64_t lo, n;
+        chunk(c, lo, n);
         PTMH_CUDA(cudaStreamWaitEvent(sc, g_ws.ev_in[c], 0));
         PTMH_TRY(launch_cb_pack(d_spins + lo * nsite, n, L, d_packed + lo * 2 * W, sc));
-        PTMH_TRY(launch_row_stats(d_spins + lo * nsite, n, L, d_stats + 2 * lo, sc));
+        PTMH_TRY(launch_cb_row_stats(d_packed + lo * 2 * W, n, L, d_stats + 2 * lo, sc));
         PTMH_TRY(launch_cb_sweeps(d_packed + lo * 2 * W, n, L, d_r2s + lo, d_thr, always, seed, first_sweep,
                                   n_sweeps, d_stats + 2 * lo, sc));
         PTMH_TRY(launch_cb_unpack(d_packed + lo * 2 * W, n, L, d_spins + lo * nsite, sc));
         PTMH_CUDA(cudaEventRecord(g_ws.ev_out[c], sc));
+    }
+    for (int64_t c = 0; c < nch; ++c) {
+        int64_t lo, n;
+        chunk(c, lo, n);
         PTMH_CUDA(cudaStreamWaitEvent(sout, g_ws.ev_out[c], 0));
         PTMH_CUDA(cudaMemcpyAsync(spins + lo * nsite, d_spins + lo * nsite, (size_t)(n * nsite),
                                   cudaMemcpyDeviceToHost, sout));

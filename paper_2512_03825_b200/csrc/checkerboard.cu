@@ -198,23 +198,20 @@ __global__ void __launch_bounds__(256) cb_half_sweep_fast(
 // colours' words, Bond = sum over colour-1 sites of s*nb (every bond has
 // exactly one colour-1 end) -- plus the deltas of its own tie flips.
 constexpr int kQCap = 128;
+#ifndef PTMH_FERRO_MINB
+#define PTMH_FERRO_MINB 1
+#endif
 
 template <int kRows, bool kStats>
-__global__ void __launch_bounds__(256) cb_half_sweep_ferro(
+__global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_half_sweep_ferro(
     uint32_t* __restrict__ packed, int64_t rows, int L, int WR, int64_t W,
     const int32_t* __restrict__ row_to_slot, const uint32_t* __restrict__ thresh, const RoundKeys32 rk,
     uint32_t ctr1, int color, int64_t* __restrict__ stats) {
     constexpr int kWarps = 8;
     __shared__ uint32_t q_gw[kWarps][kQCap], q_h[kWarps][kQCap], q_sl[kWarps][kQCap], q_info[kWarps][kQCap];
-    __shared__ uint32_t q_res[kWarps], q_ok[kWarps];
+    __shared__ uint32_t tie_m[kWarps][kRows][32], tie_k4[kWarps][kRows][32], tie_s[kWarps][kRows][32];
     __shared__ int extra_s[kWarps][32], extra_b[kWarps][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (kStats) {
-        extra_s[warp][lane] = 0;
-        extra_b[warp][lane] = 0;
-    }
-    if (lane == 0) { q_res[warp] = 0; q_ok[warp] = 0; }
-    __syncwarp();
 
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int strips = L / kRows;
@@ -224,18 +221,22 @@ __global__ void __launch_bounds__(256) cb_half_sweep_ferro(
     const int rem = (int)(tid - lat * per_lat);
     const int strip = rem / WR;
     const int k = rem - strip * WR;
+    const int i0 = strip * kRows;
+    const uint32_t own_base = (uint32_t)((lat * 2 + color) * W);
+    int slot = 0;
+    uint32_t t3 = 0, t4 = 0;
     int sumS = 0, sumB = 0;
+    uint32_t any_tie = 0;
     if (active) {
         if (!kStats && rem == 0) {  // colour-0 pass: reset, colour-1 pass recomputes
             stats[2 * lat] = 0;
             stats[2 * lat + 1] = 0;
         }
-        const uint32_t own_base = (uint32_t)((lat * 2 + color) * W);
         const uint32_t* __restrict__ other = packed + (lat * 2 + (1 - color)) * W;
         uint32_t* __restrict__ own = packed + own_base;
-        const int slot = row_to_slot[lat];
-        const uint32_t t3 = __ldg(thresh + slot * 10 + 8);
-        const uint32_t t4 = __ldg(thresh + slot * 10 + 9);
+        slot = row_to_slot[lat];
+        t3 = __ldg(thresh + slot * 10 + 8);
+        t4 = __ldg(thresh + slot * 10 + 9);
         uint32_t TA[8], TB[8];
 #pragma unroll
         for (int p = 0; p < 8; ++p) {
@@ -244,21 +245,26 @@ __global__ void __launch_bounds__(256) cb_half_sweep_ferro(
         }
         const int kl = (k == 0) ? WR - 1 : k - 1;
         const int kr = (k == WR - 1) ? 0 : k + 1;
-        const int i0 = strip * kRows;
+        // horizontal neighbour word column: kl when (i + colour) is even, else kr
+        const int kadj0 = ((i0 + color) & 1) == 0 ? kl : kr;
+        const int kadj1 = ((i0 + color) & 1) == 0 ? kr : kl;
         uint32_t up = __ldg(other + (i0 == 0 ? L - 1 : i0 - 1) * WR + k);
         uint32_t mid = __ldg(other + i0 * WR + k);
+        uint32_t dn = __ldg(other + (i0 + 1 == L ? 0 : i0 + 1) * WR + k);
+        uint32_t S = own[i0 * WR + k];
+        uint32_t adj = __ldg(other + i0 * WR + kadj0);
 #pragma unroll 2
         for (int rr = 0; rr < kRows; ++rr) {
             const int i = i0 + rr;
             const int row = i * WR;
-            const uint32_t dn = __ldg(other + (i + 1 == L ? 0 : row + WR) + k);
-            const uint32_t S = own[row + k];
-            uint32_t hz;
-            if (((i + color) & 1) == 0) {
-                hz = __funnelshift_l(__ldg(other + row + kl), mid, 1);  // site m sees m-1
-            } else {
-                hz = __funnelshift_r(mid, __ldg(other + row + kr), 1);  // site m sees m+1
-            }
+            // prefetch row i+1 (own, adjacent) and row i+2 (other colour, below)
+            const int i1 = (i + 1 == L) ? 0 : i + 1;
+            const int i2 = (i1 + 1 == L) ? 0 : i1 + 1;
+            const uint32_t dn_n = __ldg(other + i2 * WR + k);
+            const uint32_t S_n = own[i1 * WR + k];
+            const uint32_t adj_n = __ldg(other + i1 * WR + ((rr & 1) ? kadj0 : kadj1));
+            const uint32_t hz = (((i + color) & 1) == 0) ? __funnelshift_l(adj, mid, 1)   // m sees m-1
+                                                         : __funnelshift_r(mid, adj, 1);  // m sees m+1
             const uint32_t a = ~(S ^ up), b = ~(S ^ dn), c = ~(S ^ mid), d = ~(S ^ hz);
             const uint32_t s1 = a ^ b, c1 = a & b, s2 = c ^ d, c2 = c & d;
             const uint32_t k0 = s1 ^ s2, c3 = s1 & s2;
@@ -266,74 +272,104 @@ __global__ void __launch_bounds__(256) cb_half_sweep_ferro(
             const uint32_t upm = (k1 & k0) | K4;   // k = 3, 4
             const uint32_t K2 = k1 & ~k0;          // k = 2: dE = 0
             uint32_t acc = ~(k1 | K4);             // k = 0, 1: dE < 0
-            {
-                const uint32_t w32 = (uint32_t)(row + k);
-                const uint4 r0 = philox4x32_10(make_uint4(2u * w32, ctr1, (uint32_t)slot, 0u), rk);
-                const uint4 r1 = philox4x32_10(make_uint4(2u * w32 + 1u, ctr1, (uint32_t)slot, 0u), rk);
-                const uint32_t U[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
-                acc |= K2 & ~U[0];  // neutral: u < 2^31 <=> top bit clear
-                uint32_t lt = 0, eq = upm;
+            const uint32_t w32 = (uint32_t)(row + k);
+            const uint4 r0 = philox4x32_10(make_uint4(2u * w32, ctr1, (uint32_t)slot, 0u), rk);
+            const uint4 r1 = philox4x32_10(make_uint4(2u * w32 + 1u, ctr1, (uint32_t)slot, 0u), rk);
+            const uint32_t U[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+            acc |= K2 & ~U[0];  // neutral: u < 2^31 <=> top bit clear
+            uint32_t lt = 0, eq = upm;
 #pragma unroll
-                for (int p = 0; p < 8; ++p) {
-                    const uint32_t Tm = (K4 & TB[p]) | (~K4 & TA[p]);
-                    lt |= eq & ~U[p] & Tm;
-                    eq &= ~(U[p] ^ Tm);
-                }
-                acc |= lt;
-                if (eq) {  // ties on the top byte: queue them
-                    const uint32_t n = __popc(eq);
-                    const uint32_t off = atomicAdd(&q_res[warp], n);
-                    if (off + n <= kQCap) {
-                        atomicAdd(&q_ok[warp], n);
-                        uint32_t o = off;
-                        while (eq) {
-                            const int bit = __ffs(eq) - 1;
-                            eq &= eq - 1;
-                            const uint32_t k4 = (K4 >> bit) & 1u, sb = (S >> bit) & 1u;
-                            q_gw[warp][o] = own_base + w32;
-                            q_h[warp][o] = w32 * 32u + (uint32_t)bit;
-                            q_sl[warp][o] = (uint32_t)slot;
-                            q_info[warp][o] = ((k4 ? t4 : t3) & 0x00ffffffu) | (k4 << 24) | (sb << 25) |
-                                              ((uint32_t)lane << 26);
-                            ++o;
-                        }
-                    } else {  // queue full: resolve in place
-                        while (eq) {
-                            const int bit = __ffs(eq) - 1;
-                            eq &= eq - 1;
-                            const uint32_t t24 = (((K4 >> bit) & 1u) ? t4 : t3) & 0x00ffffffu;
-                            const uint4 r2 =
-                                philox4x32_10(make_uint4(w32 * 32u + (uint32_t)bit, ctr1, (uint32_t)slot, 1u), rk);
-                            if ((r2.x >> 8) < t24) acc |= 1u << bit;
-                        }
-                    }
-                }
+            for (int p = 0; p < 8; ++p) {
+                const uint32_t Tm = (K4 & TB[p]) | (~K4 & TA[p]);
+                lt |= eq & ~U[p] & Tm;
+                eq &= ~(U[p] ^ Tm);
             }
+            acc |= lt;
+            // ties (top byte equal): bookkeeping only, resolved after the loop
+            tie_m[warp][rr][lane] = eq;
+            tie_k4[warp][rr][lane] = eq & K4;
+            tie_s[warp][rr][lane] = eq & S;
+            any_tie |= eq;
             const uint32_t Sn = S ^ acc;
             if (acc) own[row + k] = Sn;
             if (kStats) {
                 // new aligned masks: a flip toggles alignment with all four neighbours
                 const int kk = __popc(a ^ acc) + __popc(b ^ acc) + __popc(c ^ acc) + __popc(d ^ acc);
-                sumB += 2 * kk - 128;                                  // sum of s*nb = 2k - 4 per site
-                sumS += 2 * (__popc(Sn) + __popc(mid)) - 64;           // both colours' words
+                sumB += 2 * kk - 128;                         // sum of s*nb = 2k - 4 per site
+                sumS += 2 * (__popc(Sn) + __popc(mid)) - 64;  // both colours' words
             }
             up = mid;
             mid = dn;
+            dn = dn_n;
+            S = S_n;
+            adj = adj_n;
         }
     }
-    __syncwarp();
-    const uint32_t nq = q_ok[warp];
-    for (uint32_t base = 0; base < nq; base += 32) {
-        const uint32_t e = base + (uint32_t)lane;
-        if (e < nq) {
-            const uint32_t h = q_h[warp][e], info = q_info[warp][e];
-            const uint4 r2 = philox4x32_10(make_uint4(h, ctr1, q_sl[warp][e], 1u), rk);
-            if ((r2.x >> 8) < (info & 0x00ffffffu)) {
-                atomicXor(packed + q_gw[warp][e], 1u << (h & 31u));
-                if (kStats) {
-                    const uint32_t owner = info >> 26;
-                    atomicAdd(&extra_s[warp][owner], ((info >> 25) & 1u) ? -2 : 2);
-                    atomicAdd(&extra_b[warp][owner], ((info >> 24) & 1u) ? -8 : -4);
+    // ---- tie resolution: build one warp queue, 32 secondary draws per pass
+    if (kStats) {
+        extra_s[warp][lane] = 0;
+        extra_b[warp][lane] = 0;
+    }
+    if (__any_sync(kFullMask, any_tie != 0)) {
+        int cnt = 0;
+        if (any_tie) {
+#pragma unroll
+            for (int rr = 0; rr < kRows; ++rr) cnt += __popc(tie_m[warp][rr][lane]);
+        }
+        int off = cnt;  // inclusive scan -> exclusive offset
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(kFullMask, off, o);
+            if (lane >= o) off += v;
+        }
+        const int total = __shfl_sync(kFullMask, off, 31);
+        off -= cnt;
+        const bool queued = total <= kQCap;
+        if (cnt) {
+            for (int rr = 0; rr < kRows; ++rr) {
+                uint32_t m = tie_m[warp][rr][lane];
+                const uint32_t mk4 = tie_k4[warp][rr][lane], ms = tie_s[warp][rr][lane];
+                const uint32_t w32 = (uint32_t)((i0 + rr) * WR + k);
+                while (m) {
+                    const int bit = __ffs(m) - 1;
+                    m &= m - 1;
+                    const uint32_t k4 = (mk4 >> bit) & 1u, sb = (ms >> bit) & 1u;
+                    const uint32_t t24 = (k4 ? t4 : t3) & 0x00ffffffu;
+                    const uint32_t info = t24 | (k4 << 24) | (sb << 25) | ((uint32_t)lane << 26);
+                    if (queued) {
+                        q_gw[warp][off] = own_base + w32;
+                        q_h[warp][off] = w32 * 32u + (uint32_t)bit;
+                        q_sl[warp][off] = (uint32_t)slot;
+                        q_info[warp][off] = info;
+                        ++off;
+                    } else {  // more ties than the queue holds: resolve in place
+                        const uint4 r2 =
+                            philox4x32_10(make_uint4(w32 * 32u + (uint32_t)bit, ctr1, (uint32_t)slot, 1u), rk);
+                        if ((r2.x >> 8) < t24) {
+                            atomicXor(packed + own_base + w32, 1u << bit);
+                            if (kStats) {
+                                sumS += sb ? -2 : 2;
+                                sumB += k4 ? -8 : -4;
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        const int nq = queued ? total : 0;
+        for (int base = 0; base < nq; base += 32) {
+            const int e = base + lane;
+            if (e < nq) {
+                const uint32_t h = q_h[warp][e], info = q_info[warp][e];
+                const uint4 r2 = philox4x32_10(make_uint4(h, ctr1, q_sl[warp][e], 1u), rk);
+                if ((r2.x >> 8) < (info & 0x00ffffffu)) {
+                    atomicXor(packed + q_gw[warp][e], 1u << (h & 31u));
+                    if (kStats) {
+                        const uint32_t owner = info >> 26;
+                        atomicAdd(&extra_s[warp][owner], ((info >> 25) & 1u) ? -2 : 2);
+                        atomicAdd(&extra_b[warp][owner], ((info >> 24) & 1u) ? -8 : -4);
+                    }
                 }
             }
         }
@@ -521,6 +557,17 @@ static ClassPlan make_plan(uint32_t always_mask) {
         if (!am) { p.k[p.n_up] = k; p.sf[p.n_up] = 2; p.cls[p.n_up] = cm; ++p.n_up; }
     }
     return p;
+}
+
+void fill_class_plan(uint32_t always_mask, int* n_up, int* k, int* sf, int* cls, int* ferro) {
+    const ClassPlan p = make_plan(always_mask);
+    *n_up = p.n_up;
+    for (int q = 0; q < 10; ++q) {
+        k[q] = p.k[q];
+        sf[q] = p.sf[q];
+        cls[q] = p.cls[q];
+    }
+    *ferro = (always_mask & kSymmetricFlag) && (always_mask & 0x3ffu) == 0x078u;
 }
 
 constexpr int kFastRows = 8;

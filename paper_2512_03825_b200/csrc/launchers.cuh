@@ -4,6 +4,8 @@
 
 #include <cstdint>
 
+#include "philox.cuh"
+
 namespace ptmh {
 
 struct AdvanceArgs {
@@ -49,5 +51,31 @@ int launch_cb_slot_energies(const int64_t* stats, const int64_t* s2r, int64_t R,
                             double* energies, int64_t* sums, cudaStream_t s);
 int launch_cb_observe(const int64_t* stats, const int64_t* s2r, int64_t R, int64_t L, double J, double B,
                       double* obs_e, double* obs_m, int64_t ncols, int64_t col, cudaStream_t s);
+
+// resident.cu: one cooperative launch = many sweeps + exchange rounds
+struct ResidentArgs {
+    uint32_t* packed;  // (R, 2, W)
+    int R, L, W, WR;   // WR = L/64 when L % 64 == 0, else 0 (generic gather)
+    const uint32_t* thresh;
+    RoundKeys32 rk;
+    uint64_t seed;
+    double J, B;
+    const double* betas;
+    int64_t* s2r[2];   // double-buffered slot_to_row
+    int32_t* r2s[2];   // double-buffered row_to_slot
+    int64_t* stats;    // (R, 2)
+    int64_t* counters; // accepted, near ties
+    double* obs_e;
+    double* obs_m;
+    int64_t ncols;
+    int64_t first_sweep, n_sweeps, total_sweeps;
+    int64_t swap_every;    // sweeps, 0 = never
+    int64_t record_every;  // 0 = no recording
+    int buf;               // permutation buffer holding the current mapping
+    int n_up, up_k[10], up_sf[10], up_cls[10];
+    int ferro;
+};
+int launch_cb_resident(const ResidentArgs& a, bool fast, cudaStream_t s, int* grid_out);
+void fill_class_plan(uint32_t always_mask, int* n_up, int* k, int* sf, int* cls, int* ferro);
 
 }  // namespace ptmh

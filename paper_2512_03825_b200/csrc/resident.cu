@@ -1,0 +1,296 @@
+// resident.cu -- persistent checkerboard PT run for small and many lattices.
+//
+// One cooperative launch runs many sweeps *and* the exchange rounds between
+// them.  Each CTA owns whole lattices (lattice r -> CTA r % gridDim.x), so the
+// two colour half-sweeps of a lattice only need __syncthreads, and its (S, Bond)
+// come from a block reduction (no atomics).  The only grid-wide barrier is the
+// one before an exchange round, when every lattice's energy must be final.
+//
+// Exchange without a second barrier: the owner of lattice r (slot k) decides
+// the pair containing k itself -- both owners of a pair evaluate the same
+// reference rule (kernels.py:116-148) on the same inputs (energies from stats,
+// the swap draw at stream R+p, position = round), so they agree -- and writes
+// r's new slot into the *other* buffer of the double-buffered permutation.
+// Partner lookups read the current buffer, which nobody writes this round.
+//
+// The per-word update is the same arithmetic as checkerboard.cu (same chain,
+// same random numbers, bit-exact with oracle/ptmh_oracle.c); ties are resolved
+// in place by the owning lane.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "launchers.cuh"
+#include "philox.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace ptmh {
+
+// ResidentArgs is declared in launchers.cuh
+
+__device__ __forceinline__ uint32_t resident_bit(const uint32_t* p, int h) {
+    return (p[h >> 5] >> (h & 31)) & 1u;
+}
+
+// one colour-c word of a lattice: gather neighbour words, decide, store;
+// returns nothing, adds the colour-1 (S, Bond) contributions when `stats`
+template <bool kFast, bool kFerro>
+__device__ __forceinline__ void resident_word(const ResidentArgs& A, uint32_t* own, const uint32_t* oth,
+                                              int w, int color, int slot, uint32_t ctr1, int& sumS,
+                                              int& sumB, bool stats) {
+    const int L = A.L;
+    uint32_t S = own[w], n1, n2, n3, n4, valid;
+    if (kFast) {
+        const int WR = A.WR;
+        const int i = w / WR, k = w - i * WR;
+        const int iu = (i == 0) ? L - 1 : i - 1, id = (i == L - 1) ? 0 : i + 1;
+        const uint32_t mid = oth[w];
+        n1 = oth[iu * WR + k];
+        n2 = oth[id * WR + k];
+        n3 = mid;
+        if (((i + color) & 1) == 0) {
+            n4 = __funnelshift_l(oth[i * WR + (k == 0 ? WR - 1 : k - 1)], mid, 1);
+        } else {
+            n4 = __funnelshift_r(mid, oth[i * WR + (k == WR - 1 ? 0 : k + 1)], 1);
+        }
+        valid = 0xffffffffu;
+    } else {
+        const int Lh = L / 2, H = L * Lh;
+        n1 = n2 = n3 = n4 = valid = 0;
+        for (int b = 0; b < 32; ++b) {
+            const int h = w * 32 + b;
+            if (h >= H) break;
+            valid |= 1u << b;
+            const int i = h / Lh, m = h - i * Lh;
+            const int j = 2 * m + ((i + color) & 1);
+            const int iu = (i == 0) ? L - 1 : i - 1, id = (i == L - 1) ? 0 : i + 1;
+            const int jl = (j == 0) ? L - 1 : j - 1, jr = (j == L - 1) ? 0 : j + 1;
+            n1 |= resident_bit(oth, iu * Lh + (j >> 1)) << b;
+            n2 |= resident_bit(oth, id * Lh + (j >> 1)) << b;
+            n3 |= resident_bit(oth, i * Lh + (jl >> 1)) << b;
+            n4 |= resident_bit(oth, i * Lh + (jr >> 1)) << b;
+        }
+    }
+    const uint32_t a = ~(S ^ n1), b = ~(S ^ n2), c = ~(S ^ n3), d = ~(S ^ n4);
+    const uint32_t s1 = a ^ b, c1 = a & b, s2 = c ^ d, c2 = c & d;
+    const uint32_t k0 = s1 ^ s2, c3 = s1 & s2;
+    const uint32_t k1 = c1 ^ c2 ^ c3, k2 = c1 & c2;
+    const uint32_t* thr = A.thresh + slot * 10;
+    uint32_t acc;
+    if (kFerro) {
+        // J > 0, B = 0: k <= 1 always, k = 2 with probability 1/2, k = 3, 4 thresholds
+        const uint32_t K4 = k2, upm = ((k1 & k0) | k2) & valid, K2 = k1 & ~k0 & valid;
+        const uint32_t t3 = __ldg(thr + 8), t4 = __ldg(thr + 9);
+        acc = ~(k1 | k2) & valid;
+        const uint4 r0 = philox4x32_10(make_uint4(2u * (uint32_t)w, ctr1, (uint32_t)slot, 0u), A.rk);
+        const uint4 r1 = philox4x32_10(make_uint4(2u * (uint32_t)w + 1u, ctr1, (uint32_t)slot, 0u), A.rk);
+        const uint32_t U[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+        acc |= K2 & ~U[0];
+        uint32_t lt = 0, eq = upm;
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+            const uint32_t TA = 0u - ((t3 >> (31 - p)) & 1u), TB = 0u - ((t4 >> (31 - p)) & 1u);
+            const uint32_t Tm = (K4 & TB) | (~K4 & TA);
+            lt |= eq & ~U[p] & Tm;
+            eq &= ~(U[p] ^ Tm);
+        }
+        acc |= lt;
+        while (eq) {
+            const int bit = __ffs(eq) - 1;
+            eq &= eq - 1;
+            const uint32_t t24 = (((K4 >> bit) & 1u) ? t4 : t3) & 0x00ffffffu;
+            const uint4 r2 =
+                philox4x32_10(make_uint4((uint32_t)w * 32u + (uint32_t)bit, ctr1, (uint32_t)slot, 1u), A.rk);
+            if ((r2.x >> 8) < t24) acc |= 1u << bit;
+        }
+    } else {
+        uint32_t K[5];
+        K[4] = k2;
+        K[3] = k1 & k0;
+        K[2] = k1 & ~k0;
+        K[1] = k0 & ~k1;
+        K[0] = ~(k0 | k1 | k2);
+        uint32_t M[10], T[10], up = 0;
+        const int nq = A.n_up;
+#pragma unroll
+        for (int q = 0; q < 10; ++q) {
+            if (q < nq) {
+                const uint32_t sf = A.up_sf[q] == 0 ? 0xffffffffu : (A.up_sf[q] == 1 ? S : ~S);
+                M[q] = K[A.up_k[q]] & sf & valid;
+                T[q] = __ldg(thr + A.up_cls[q]);
+                up |= M[q];
+            } else {
+                M[q] = 0;
+                T[q] = 0;
+            }
+        }
+        acc = valid & ~up;
+        if (up) {
+            const uint4 r0 = philox4x32_10(make_uint4(2u * (uint32_t)w, ctr1, (uint32_t)slot, 0u), A.rk);
+            const uint4 r1 = philox4x32_10(make_uint4(2u * (uint32_t)w + 1u, ctr1, (uint32_t)slot, 0u), A.rk);
+            const uint32_t U[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+            uint32_t lt = 0, eq = up;
+#pragma unroll
+            for (int p = 0; p < 8; ++p) {
+                uint32_t Tm = 0;
+#pragma unroll
+                for (int q = 0; q < 10; ++q)
+                    if (q < nq) Tm |= M[q] & (0u - ((T[q] >> (31 - p)) & 1u));
+                lt |= eq & ~U[p] & Tm;
+                eq &= ~(U[p] ^ Tm);
+            }
+            acc |= lt;
+            while (eq) {
+                const int bit = __ffs(eq) - 1;
+                eq &= eq - 1;
+                uint32_t t24 = 0;
+#pragma unroll
+                for (int q = 0; q < 10; ++q)
+                    if (q < nq && ((M[q] >> bit) & 1u)) t24 = T[q] & 0x00ffffffu;
+                const uint4 r2 = philox4x32_10(
+                    make_uint4((uint32_t)w * 32u + (uint32_t)bit, ctr1, (uint32_t)slot, 1u), A.rk);
+                if ((r2.x >> 8) < t24) acc |= 1u << bit;
+            }
+        }
+    }
+    const uint32_t Sn = S ^ acc;
+    if (acc) own[w] = Sn;
+    if (stats) {  // colour-1 pass: absolute (S, Bond) of the new configuration
+        const int kk = __popc((a ^ acc) & valid) + __popc((b ^ acc) & valid) + __popc((c ^ acc) & valid) +
+                       __popc((d ^ acc) & valid);
+        const int nv = __popc(valid);
+        sumB += 2 * kk - 4 * nv;
+        sumS += 2 * (__popc(Sn & valid) + __popc(oth[w] & valid)) - 2 * nv;
+    }
+}
+
+constexpr int kMaxLatPerBlock = 64;
+
+// Block b owns the contiguous lattices [lo, hi) and sweeps them together:
+// work items (lattice, word) are spread over all threads, __syncthreads
+// separates the colours, per-lattice (S, Bond) accumulate in shared memory.
+template <bool kFast, bool kFerro>
+__global__ void __launch_bounds__(256) cb_resident_kernel(ResidentArgs A) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ int s_slot[kMaxLatPerBlock];
+    __shared__ int s_S[kMaxLatPerBlock], s_B[kMaxLatPerBlock];
+    const int R = A.R, W = A.W;
+    const int lo = (int)((int64_t)R * blockIdx.x / gridDim.x);
+    const int hi = (int)((int64_t)R * (blockIdx.x + 1) / gridDim.x);
+    const int nl = hi - lo;
+    const int items = nl * W;
+    int buf = A.buf;
+    for (int64_t t = A.first_sweep; t < A.first_sweep + A.n_sweeps; ++t) {
+        const int64_t done = t + 1;
+        const bool rec = A.record_every > 0 && done % A.record_every == 0;
+        const bool exch = A.swap_every > 0 && done % A.swap_every == 0 && done < A.total_sweeps;
+        const bool need_stats = rec || exch || t + 1 == A.first_sweep + A.n_sweeps;
+        for (int i = threadIdx.x; i < nl; i += blockDim.x) {
+            s_slot[i] = A.r2s[buf][lo + i];
+            s_S[i] = 0;
+            s_B[i] = 0;
+        }
+        __syncthreads();
+        for (int color = 0; color < 2; ++color) {
+            const uint32_t ctr1 = (uint32_t)(2 * t + color);
+            const bool st = color == 1 && need_stats;
+            for (int it = threadIdx.x; it < items; it += blockDim.x) {
+                const int li = it / W, w = it - li * W;
+                uint32_t* c0 = A.packed + (int64_t)(lo + li) * 2 * W;
+                uint32_t* own = color ? c0 + W : c0;
+                const uint32_t* oth = color ? c0 : c0 + W;
+                int sS = 0, sB = 0;
+                resident_word<kFast, kFerro>(A, own, oth, w, color, s_slot[li], ctr1, sS, sB, st);
+                if (st) {
+                    atomicAdd(&s_S[li], sS);
+                    atomicAdd(&s_B[li], sB);
+                }
+            }
+            __syncthreads();
+        }
+        if (need_stats) {
+            for (int i = threadIdx.x; i < nl; i += blockDim.x) {
+                const long long S = s_S[i], Bd = s_B[i];
+                A.stats[2 * (lo + i)] = S;
+                A.stats[2 * (lo + i) + 1] = Bd;
+                if (rec) {  // by slot, before the round (executor.py order)
+                    const int64_t col = done / A.record_every - 1;
+                    A.obs_e[(int64_t)s_slot[i] * A.ncols + col] =
+                        __dsub_rn(__dmul_rn(A.B, (double)S), __dmul_rn(A.J, (double)Bd));
+                    A.obs_m[(int64_t)s_slot[i] * A.ncols + col] = __ddiv_rn((double)S, (double)A.L * A.L);
+                }
+            }
+        }
+        if (!exch) continue;
+        grid.sync();  // every lattice's (S, Bond) is final
+        // ---- exchange round: the owner of lattice r decides the pair of its slot
+        const int64_t round = done / A.swap_every - 1;
+        const int first = (int)(round % 2);
+        const int n_pairs = (R - first) / 2;
+        for (int li = threadIdx.x; li < nl; li += blockDim.x) {
+            const int r = lo + li;
+            const int k = s_slot[li];
+            int nk = k;
+            if (k >= first && (k - first) / 2 < n_pairs) {
+                const int p = (k - first) / 2;
+                const int i = first + 2 * p, j = i + 1;
+                const int64_t ri = A.s2r[buf][i], rj = A.s2r[buf][j];
+                const double Ei = __dsub_rn(__dmul_rn(A.B, (double)A.stats[2 * ri]),
+                                            __dmul_rn(A.J, (double)A.stats[2 * ri + 1]));
+                const double Ej = __dsub_rn(__dmul_rn(A.B, (double)A.stats[2 * rj]),
+                                            __dmul_rn(A.J, (double)A.stats[2 * rj + 1]));
+                const double u = stream_uniform(A.seed, (uint64_t)(R + p), (uint64_t)round);
+                const double x = __dmul_rn(__dsub_rn(A.betas[i], A.betas[j]), __dsub_rn(Ei, Ej));
+                double prob;
+                if (x >= 0.0) {
+                    prob = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-x)));
+                } else {
+                    const double ex = exp(x);
+                    prob = __ddiv_rn(ex, __dadd_rn(1.0, ex));
+                }
+                const bool acc = u < prob;
+                if (acc) nk = (k == i) ? j : i;
+                if (k == i) {
+                    if (acc) atomicAdd((unsigned long long*)&A.counters[0], 1ull);
+                    if (fabs(u - prob) <= 4.0 * 2.220446049250313e-16 * fmax(prob, 2.2250738585072014e-308))
+                        atomicAdd((unsigned long long*)&A.counters[1], 1ull);
+                }
+            }
+            A.r2s[buf ^ 1][r] = nk;
+            A.s2r[buf ^ 1][nk] = r;
+        }
+        buf ^= 1;
+        __syncthreads();  // next sweep reads r2s[buf] of this block's lattices
+    }
+}
+
+template <bool kFast, bool kFerro>
+static int launch_resident_t(const ResidentArgs& a, cudaStream_t s) {
+    const int threads = 256;
+    int dev = 0, sms = 0, per_sm = 0;
+    PTMH_CUDA(cudaGetDevice(&dev));
+    PTMH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    PTMH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cb_resident_kernel<kFast, kFerro>,
+                                                            threads, 0));
+    // enough blocks to fill the GPU, few enough that no block owns more
+    // lattices than its shared-memory tables hold
+    int grid = std::min(a.R, sms * std::max(1, per_sm));
+    if ((a.R + grid - 1) / grid > kMaxLatPerBlock) {
+        set_error("resident kernel: too many lattices per block for this grid");
+        return PTMH_ERR_ARG;
+    }
+    ResidentArgs args = a;
+    void* kargs[] = {&args};
+    PTMH_CUDA(cudaLaunchCooperativeKernel((const void*)cb_resident_kernel<kFast, kFerro>, grid, threads,
+                                          kargs, 0, s));
+    return PTMH_OK;
+}
+
+int launch_cb_resident(const ResidentArgs& a, bool fast, cudaStream_t s, int* grid_out) {
+    (void)grid_out;
+    if (fast) return a.ferro ? launch_resident_t<true, true>(a, s) : launch_resident_t<true, false>(a, s);
+    return a.ferro ? launch_resident_t<false, true>(a, s) : launch_resident_t<false, false>(a, s);
+}
+
+}  // namespace ptmh

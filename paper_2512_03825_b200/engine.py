@@ -19,6 +19,8 @@ Exchanges permute slot_to_row / row_to_slot only -- lattices never move
 
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 import torch
 
@@ -194,6 +196,28 @@ class CheckerboardEngine(_Base):
                       round_index, first, 0, n_pairs, _P(self.counters),
                       self.counters.data_ptr() + 8, _P(self.row_to_slot), s)
         return n_pairs
+
+    def run_resident(self, first_sweep: int, n_sweeps: int, total_sweeps: int, swap_every: int,
+                     record_every: int = 0, obs_e=None, obs_m=None) -> None:
+        """Sweeps first..first+n-1 of a run of total_sweeps, with its swap
+        rounds and observations, in ONE persistent launch (csrc/resident.cu).
+        Single device only (every lattice local)."""
+        if self.rows != self.R:
+            raise ValueError("the resident kernel needs every lattice on one device")
+        if getattr(self, "_s2r2", None) is None:
+            self._s2r2 = torch.empty((2, self.R), dtype=torch.int64, device=self.dev)
+            self._r2s2 = torch.empty((2, self.R), dtype=torch.int32, device=self.dev)
+        self._s2r2[0].copy_(self.slot_to_row)
+        self._r2s2[0].copy_(self.row_to_slot)
+        out = ctypes.c_int(0)
+        ncols = obs_e.shape[1] if obs_e is not None else 0
+        _lib.call("ptmh_cb_run_resident", _P(self.packed), self.R, self.L, _P(self._s2r2),
+                  _P(self._r2s2), 0, _P(self.thr), self.always, self.seed, self.J, self.B,
+                  _P(self.betas), _P(self.stats), _P(self.counters), _P(obs_e), _P(obs_m), ncols,
+                  first_sweep, n_sweeps, total_sweeps, swap_every, record_every,
+                  ctypes.byref(out), self._s())
+        self.slot_to_row.copy_(self._s2r2[out.value])
+        self.row_to_slot.copy_(self._r2s2[out.value])
 
     def observe(self, obs_e: torch.Tensor, obs_m: torch.Tensor, col: int) -> None:
         _lib.call("ptmh_cb_observe", _P(self.stats), _P(self.slot_to_row), self.R, self.L,

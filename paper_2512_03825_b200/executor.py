@@ -32,6 +32,7 @@ from .tempering import build_ladder
 
 RECORD_MODES = ("none", "observables", "full_states")
 SWEEP_MODES = ("exact", "checkerboard")
+KERNELS = ("auto", "sweep", "resident")
 MASK64 = (1 << 64) - 1
 
 
@@ -58,6 +59,7 @@ class SimulationConfig:
     record_every: int = 1
     device: int | None = None
     return_final_state: bool = False
+    kernel: str = "auto"  # checkerboard: "sweep" (2 launches/sweep), "resident" (1 launch/run)
 
     def validate(self) -> None:
         if self.side < 2:
@@ -84,6 +86,8 @@ class SimulationConfig:
             if t.shape != (self.replicas,) or not np.all(t > 0) or not np.all(np.isfinite(t)):
                 raise ConfigurationError(
                     "temperatures must be `replicas` positive finite values")
+        if self.kernel not in KERNELS:
+            raise ConfigurationError(f"kernel must be one of {KERNELS}, got {self.kernel!r}")
         if self.record_every < 1:
             raise ConfigurationError(f"record_every must be >= 1, got {self.record_every}")
         if self.sweep_mode == "checkerboard":
@@ -157,6 +161,12 @@ def _interval_plan(iterations: int, interval: int) -> list[tuple[int, int | None
             k += 1
     plan.append((iterations, None))
     return plan
+
+
+def _resident_wins(L: int, swap_every_sweeps: int) -> bool:
+    """Persistent launch for small lattices or per-sweep exchanges, where the
+    two-launches-per-sweep path is launch-latency bound."""
+    return L <= 256 or swap_every_sweeps == 1
 
 
 def _sync(dev):
@@ -265,7 +275,21 @@ def _run_checkerboard(config: SimulationConfig) -> RunRecord:
         n_rounds = sum(1 for _, ri in plan if ri is not None)
         snaps = np.zeros((n_rounds, R), dtype=np.int64) if record and n_rounds else None
         done = rounds = attempted = 0
+        use_resident = config.kernel == "resident" or (config.kernel == "auto" and _resident_wins(L, every_sw))
         try:
+            if use_resident:
+                # the whole run in one persistent launch; the schedule is replayed
+                # on the host only for the bookkeeping fields
+                eng.run_resident(0, sweeps, sweeps, every_sw,
+                                 config.record_every if record else 0, obs_e, obs_m)
+                for target, ri in plan:
+                    if ri is None:
+                        continue
+                    if snaps is not None:
+                        snaps[ri, :] = target * n_sites
+                    rounds += 1
+                    attempted += max(0, (R - ri % 2) // 2)
+                plan = []
             for target, ri in plan:
                 while done < target:
                     if record:

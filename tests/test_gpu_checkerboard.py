@@ -166,3 +166,62 @@ def test_one_lattice_matches_oracle_at_1024(mods):
         oracle.cb_sweep(ref, np.arange(R, dtype=np.int64), thr, always, 5, t, stats)
     assert np.array_equal(eng.final_spins(), ref)
     assert np.array_equal(eng.local_stats.cpu().numpy(), stats)
+
+
+@pytest.mark.parametrize("L,R,sweeps,every,seed,J,B,rec_every", [
+    (64, 6, 20, 2, 42, 1.0, 0.0, 1),
+    (64, 37, 15, 1, 8, 1.0, 0.0, 1),    # odd R, exchange every sweep
+    (32, 8, 30, 1, 3, 1.0, 0.0, 3),     # generic gather (L % 64 != 0)
+    (128, 5, 12, 5, 4, 1.0, 0.1, 2),    # field: class plan
+    (256, 3, 6, 2, 9, -1.0, 0.0, 1),    # antiferromagnet
+    (2, 7, 50, 3, 5, 1.0, 0.0, 1),
+    (6, 4, 25, 0, 6, 0.5, -0.5, 5),     # no exchanges
+])
+def test_resident_run_matches_oracle(mods, L, R, sweeps, every, seed, J, B, rec_every):
+    p = mods[0]
+    cfg = p.SimulationConfig(side=L, replicas=R, iterations=sweeps * L * L,
+                             swap_interval=every * L * L, seed=seed,
+                             params=p.IsingParams(J=J, B=B), sweep_mode="checkerboard",
+                             record_every=rec_every, return_final_state=True, kernel="resident")
+    rec = p.run(cfg)
+    assert rec.valid, rec.error
+    ref = oracle.run_checkerboard(L, R, sweeps, every, seed, J=J, B=B, record_every=rec_every)
+    assert np.array_equal(rec.final_spins, ref.final_spins)
+    assert np.array_equal(rec.slot_to_row, ref.slot_to_row)
+    assert np.array_equal(rec.energies, ref.energies)
+    assert np.array_equal(rec.magnetizations, ref.magnetizations)
+    assert (rec.swap_rounds, rec.swaps_attempted, rec.swaps_accepted) == \
+        (ref.swap_rounds, ref.swaps_attempted, ref.swaps_accepted)
+    if ref.round_entry_iterations is not None:
+        assert np.array_equal(rec.round_entry_iterations[:, 0], ref.round_entry_iterations * L * L)
+
+
+def test_resident_segments_compose(mods):
+    """Two resident segments == one resident run == the sweep-kernel path."""
+    p, engine, _, _ = mods
+    L, R, total, every = 64, 9, 12, 3
+    temps = p.build_ladder(R)
+    outs = []
+    for mode in ("one", "two", "sweep"):
+        eng = engine.CheckerboardEngine(L, R, temps, 77, 1.0, 0.0, 0.5, 0)
+        eng.init_state()
+        if mode == "one":
+            eng.run_resident(0, total, total, every)
+        elif mode == "two":
+            eng.run_resident(0, 5, total, every)
+            eng.run_resident(5, total - 5, total, every)
+        else:
+            from paper_2512_03825_b200.executor import _interval_plan
+            done = 0
+            for target, ri in _interval_plan(total, every):
+                eng.sweeps(done, target - done)
+                done = target
+                if ri is not None:
+                    eng.exchange(ri)
+        outs.append((eng.final_spins(), eng.slot_to_row.cpu().numpy(), eng.swap_counts()[0],
+                     eng.local_stats.cpu().numpy()))
+    for o in outs[1:]:
+        assert np.array_equal(o[0], outs[0][0])
+        assert np.array_equal(o[1], outs[0][1])
+        assert o[2] == outs[0][2]
+        assert np.array_equal(o[3], outs[0][3])
