@@ -166,6 +166,8 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the multi-GPU coordinator (NCCL all_gather) even at one rank")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -222,10 +224,11 @@ def main():
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    if world > 1:
+    sharded = world > 1 or args.sharded
+    if sharded:
         dist.init_process_group("nccl", device_id=dev)
     temps = geometric_ladder(R) if args.config == "c1" else build_ladder(R)
-    if world > 1:
+    if sharded:
         drv = ShardedCheckerboard(L, R, temps, SEED, device=local_rank)
         eng = drv.eng
         drv.init_state()
@@ -239,7 +242,7 @@ def main():
 
     state = {"sweep": 0, "round": 0}
     from paper_2512_03825_b200.executor import _resident_wins
-    resident = world == 1 and _resident_wins(L, every)
+    resident = not sharded and _resident_wins(L, every)
     big = 1 << 30  # run length for the resident kernel: every interval ends in a round
 
     def step(sweep_events=None):
@@ -279,7 +282,7 @@ def main():
             ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                   for _ in range(1 if resident else every)]
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            if world > 1:
+            if sharded:
                 dist.barrier()
             torch.cuda.synchronize()
             s0.record(stream)
@@ -289,7 +292,7 @@ def main():
             step_ms.append(s0.elapsed_time(s1))
             sweep_ms.extend(a.elapsed_time(b) for a, b in ev)
     total_ms = sum(step_ms)
-    if world > 1:
+    if sharded:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
@@ -306,11 +309,11 @@ def main():
         kernel_name = "cb_half_sweep_ferro<8,0|1>"
     achieved = bytes_per_launch / (launch_ms / 1e3) / 1e9
     peak, peak_kind = _peaks()
-    traffic = _traffic(args.config) if world == 1 else None
+    traffic = _traffic(args.config) if not sharded and not resident else None
 
     # ---- end to end through the host-buffer plugin (rank 0, single device)
     e2e = None
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e and not sharded:
         spins_h = eng.final_spins()
         pinned = torch.from_numpy(spins_h).pin_memory()
         sp = pinned.numpy()
@@ -336,7 +339,7 @@ def main():
                "path": "kernels.cb_interval -> ptmh_host_cb_interval (pinned int8 lattices)"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and not sharded and not args.no_cpu:
         threads = host_cores()
         per_slot = max(1000, int(1.5e8 // R))
         rate, n, dt = cpu_reference_rate(L, R, per_slot, threads)
@@ -360,7 +363,7 @@ def main():
                 "gpu_launches": args.steps * (1 if resident else 2 * every + 2),
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if sharded:
         dist.barrier()
         dist.destroy_process_group()
 

@@ -116,6 +116,21 @@ int ptmh_advance_block(int8_t *spins, int64_t L, const int64_t *slot_to_row,
                        int64_t nsteps, double *obs_e, double *obs_m,
                        int64_t ncols, int record, int8_t *states, void *stream);
 
+/* Two-phase advance_block (record 0 or 1; obs_e == NULL means record 0):
+ * phase 1 computes every attempt's draws, site, per-class acceptance bits and
+ * window dependencies fully in parallel into `workspace`
+ * (ptmh_advance_workspace_bytes(hi-lo, nsteps) bytes); phase 2 commits them
+ * warp-per-slot.  Results identical to ptmh_advance_block. */
+int64_t ptmh_advance_workspace_bytes(int64_t nslots, int64_t nsteps);
+int ptmh_advance_block_ws(int8_t *spins, int64_t L, const int64_t *slot_to_row,
+                          int64_t lo, int64_t hi, const double *tbl,
+                          const double *dcls, int int_energy, double *energies,
+                          int64_t *spin_sums, uint64_t *positions,
+                          int64_t *iters_done, uint64_t seed, int64_t start_iter,
+                          int64_t nsteps, double *obs_e, double *obs_m,
+                          int64_t ncols, void *workspace, int64_t ws_bytes,
+                          void *stream);
+
 /* swap_chunk on device arrays; accepted[0] += accepted pairs, near_ties[0] +=
  * decisions with |u - p| <= 4 ulp(p) (device exp vs host libm guard band).
  * If row_to_slot is non-NULL it is rebuilt from slot_to_row afterwards. */

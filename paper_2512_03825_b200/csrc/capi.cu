@@ -161,6 +161,24 @@ int ptmh_advance_block(int8_t* spins, int64_t L, const int64_t* slot_to_row, int
     return launch_advance(a, as_stream(stream));
 }
 
+int64_t ptmh_advance_workspace_bytes(int64_t nslots, int64_t nsteps) {
+    return advance_ws_bytes(nslots, nsteps);
+}
+
+int ptmh_advance_block_ws(int8_t* spins, int64_t L, const int64_t* slot_to_row, int64_t lo, int64_t hi,
+                          const double* tbl, const double* dcls, int int_energy, double* energies,
+                          int64_t* spin_sums, uint64_t* positions, int64_t* iters_done, uint64_t seed,
+                          int64_t start_iter, int64_t nsteps, double* obs_e, double* obs_m, int64_t ncols,
+                          void* workspace, int64_t ws_bytes, void* stream) {
+    PTMH_CHECK_ARG(L >= 2 && L * L < (1LL << 31), "advance_block: need 2 <= L, L*L < 2^31");
+    PTMH_CHECK_ARG(lo >= 0 && hi >= lo && nsteps >= 0 && start_iter >= 0, "advance_block range");
+    PTMH_CHECK_ARG(obs_e == nullptr || start_iter + nsteps <= ncols, "advance_block: obs columns");
+    AdvanceArgs a{spins, L, slot_to_row, lo, hi, tbl, dcls, int_energy, energies, spin_sums,
+                  positions, iters_done, seed, start_iter, nsteps, obs_e, obs_m, ncols,
+                  obs_e ? 1 : 0, nullptr};
+    return launch_advance_2phase(a, workspace, ws_bytes, as_stream(stream));
+}
+
 int ptmh_swap_chunk(int64_t* slot_to_row, double* energies, int64_t* spin_sums, const double* betas,
                     int64_t R, uint64_t seed, int64_t stream_base, int64_t round_index, int64_t first,
                     int64_t pair_lo, int64_t pair_hi, int64_t* accepted, int64_t* near_ties,
@@ -334,7 +352,14 @@ int ptmh_host_advance_block(int8_t* spins, int64_t rows, int64_t L, const int64_
     if (record == 2) PTMH_TRY(ws_get(g_ws, 10, (size_t)R * ncols * nsite, &d_states));
     AdvanceArgs a{d_spins, L, d_s2r, lo, hi, d_tbl, d_dcls, int_energy, d_e, d_sums, d_pos, d_iters, seed,
                   start_iter, nsteps, d_oe, d_om, ncols, record, d_states};
-    PTMH_TRY(launch_advance(a, s));
+    if (record <= 1) {
+        const int64_t wsb = advance_ws_bytes(hi - lo, nsteps);
+        void* d_ws = nullptr;
+        PTMH_TRY(ws_get(g_ws, 17, (size_t)wsb, reinterpret_cast<int8_t**>(&d_ws)));
+        PTMH_TRY(launch_advance_2phase(a, d_ws, wsb, s));
+    } else {
+        PTMH_TRY(launch_advance(a, s));
+    }
     PTMH_CUDA(cudaMemcpyAsync(spins, d_spins, (size_t)rows * nsite, cudaMemcpyDeviceToHost, s));
     PTMH_CUDA(cudaMemcpyAsync(energies + lo, d_e + lo, (hi - lo) * 8, cudaMemcpyDeviceToHost, s));
     PTMH_CUDA(cudaMemcpyAsync(spin_sums + lo, d_sums + lo, (hi - lo) * 8, cudaMemcpyDeviceToHost, s));

@@ -21,6 +21,8 @@
 // intrinsics where contraction would otherwise be possible.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "launchers.cuh"
 #include "philox.cuh"
@@ -216,6 +218,239 @@ __global__ void advance_kernel(AdvanceArgs A) {
         A.positions[slot] = pos0 + 2 * (uint64_t)A.nsteps;
         A.iters_done[slot] = A.start_iter + A.nsteps;
     }
+}
+
+// ---------------------------------------------- two-phase advance (draws) --
+// Phase 1: one thread per attempt.  Everything about an attempt that does not
+// depend on the lattice state is computed here, fully parallel over slots and
+// attempts: the two Philox4x64-10 words (kernels.py:84-87), the site
+// (kernels.py:88-90), one acceptance bit per uphill class
+// (u_acc < exp(-beta*dE_c), kernels.py:95-98) and the mask of earlier
+// attempts of the same 32-attempt window whose site is the site or one of its
+// neighbours (the dependencies phase 2 must respect).
+struct DrawArgs {
+    int64_t lo, nslots, L;
+    const double* tbl;
+    const double* dcls;
+    uint64_t seed;
+    const uint64_t* positions;  // call-start positions (by slot)
+    int64_t a0, n, stride;      // attempts [a0, a0+n) of the call; record stride
+    int32_t* rec_site;
+    uint32_t* rec_acc;
+    uint32_t* rec_conf;
+};
+
+__global__ void __launch_bounds__(256) draw_kernel(DrawArgs D) {
+    const int64_t npad = (D.n + 31) & ~int64_t(31);
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t s = tid / npad;
+    if (s >= D.nslots) return;  // whole warps (npad % 32 == 0)
+    const int64_t a = tid - s * npad;
+    const int lane = threadIdx.x & 31;
+    const int64_t slot = D.lo + s;
+    const int64_t L = D.L;
+    const uint64_t p = D.positions[slot] + 2 * (uint64_t)(D.a0 + a);
+    const double u_site = stream_uniform(D.seed, (uint64_t)slot, p);
+    const double u_acc = stream_uniform(D.seed, (uint64_t)slot, p + 1);
+    const int64_t site = (int64_t)__dmul_rn(u_site, (double)(L * L));
+    const int64_t r = site / L, c = site - r * L;
+    uint32_t accm = 0;
+    const double* tb = D.tbl + slot * 10;
+#pragma unroll
+    for (int q = 0; q < 10; ++q)
+        if (D.dcls[q] > 0.0 && u_acc < tb[q]) accm |= 1u << q;
+    // conflicts with earlier attempts of the window: a shifted-2x2-bucket
+    // filter (two sites at Chebyshev distance <= 1 share one of 4 buckets),
+    // exact neighbour test only where the filter fires
+    const unsigned lt_mask = (1u << lane) - 1u;
+    bool full = (L & 1) || L <= 8;
+    unsigned cand = 0xffffffffu;
+    if (!full) {
+        const int r1 = (int)(r >> 1), c1 = (int)(c >> 1);
+        const int r2 = (int)(((r + 1) % L) >> 1), c2 = (int)(((c + 1) % L) >> 1);
+        cand = __match_any_sync(0xffffffffu, (r1 << 16) | c1) | __match_any_sync(0xffffffffu, (r2 << 16) | c1) |
+               __match_any_sync(0xffffffffu, (r1 << 16) | c2) | __match_any_sync(0xffffffffu, (r2 << 16) | c2);
+    }
+    cand &= lt_mask;
+    unsigned conf = 0;
+    if (__any_sync(0xffffffffu, cand != 0)) {
+        const int64_t up = ((r + 1) % L) * L + c, dn = ((r - 1 + L) % L) * L + c;
+        const int64_t rt = r * L + (c + 1) % L, lf = r * L + (c - 1 + L) % L;
+#pragma unroll 4
+        for (int k = 0; k < 32; ++k) {
+            const int64_t s2 = __shfl_sync(0xffffffffu, site, k);
+            const bool hit = (s2 == site) | (s2 == up) | (s2 == dn) | (s2 == rt) | (s2 == lf);
+            conf |= (hit && ((cand >> k) & 1u)) ? (1u << k) : 0u;
+        }
+    }
+    if (a < D.n) {
+        const int64_t o = s * D.stride + a;
+        D.rec_site[o] = (int32_t)site;
+        D.rec_acc[o] = accm;
+        D.rec_conf[o] = conf;
+    }
+}
+
+// Phase 2: warp per slot, windows of 32 attempts committed in dependency
+// levels from the phase-1 records; energies summed in attempt order exactly
+// as advance_kernel does.
+struct CommitArgs {
+    AdvanceArgs A;
+    int64_t a0, n, stride;
+    const int32_t* rec_site;
+    const uint32_t* rec_acc;
+    const uint32_t* rec_conf;
+    int last;
+};
+
+__global__ void __launch_bounds__(128) commit_kernel(CommitArgs C) {
+    const AdvanceArgs& A = C.A;
+    const int lane = threadIdx.x & 31;
+    const int64_t s = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t slot = A.lo + s;
+    if (slot >= A.hi) return;
+    const int64_t L = A.L, n_sites = L * L;
+    int8_t* lat = A.spins + A.slot_to_row[slot] * n_sites;
+    double e = A.energies[slot];
+    long long ssum = A.spin_sums[slot];
+    const double nsd = (double)n_sites;
+    const int32_t* rs = C.rec_site + s * C.stride;
+    const uint32_t* ra = C.rec_acc + s * C.stride;
+    const uint32_t* rc = C.rec_conf + s * C.stride;
+    // software pipeline: window w+1's records are loaded, and its lattice
+    // lines prefetched into L1, while window w commits (records never depend
+    // on the state; a prefetch never changes what a later load returns)
+    auto prefetch_site = [&](int64_t st) {
+        const int64_t r = st / L, c = st - r * L;
+        const int8_t* b = lat + r * L;
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(b + c));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(lat + ((r + 1) % L) * L + c));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(lat + ((r - 1 + L) % L) * L + c));
+    };
+    int64_t n_site = 0;
+    uint32_t n_acc = 0u, n_conf = 0u;
+    if (lane < C.n) {
+        n_site = rs[lane];
+        n_acc = ra[lane];
+        n_conf = rc[lane];
+        prefetch_site(n_site);
+    }
+    for (int64_t w0 = 0; w0 < C.n; w0 += 32) {
+        const int64_t a = w0 + lane;
+        const bool valid = a < C.n;
+        const int nvalid = (int)min((int64_t)32, C.n - w0);
+        const int64_t site = valid ? n_site : 0;
+        const uint32_t accm = valid ? n_acc : 0u;
+        const unsigned conf = valid ? n_conf : 0u;
+        if (a + 32 < C.n) {
+            n_site = rs[a + 32];
+            n_acc = ra[a + 32];
+            n_conf = rc[a + 32];
+            prefetch_site(n_site);
+        }
+        const int64_t r = site / L, c = site - r * L;
+        const int64_t up = ((r + 1) % L) * L + c, dn = ((r - 1 + L) % L) * L + c;
+        const int64_t rt = r * L + (c + 1) % L, lf = r * L + (c - 1 + L) % L;
+        unsigned pending = __ballot_sync(0xffffffffu, valid);
+        double my_d = 0.0;
+        int my_ds = 0;
+        bool my_acc = false;
+        while (pending) {
+            const bool ready = ((pending >> lane) & 1u) && ((conf & pending) == 0u);
+            if (ready) {
+                const int sp = lat[site];
+                const int nb = lat[up] + lat[dn] + lat[rt] + lat[lf];
+                const int cls = (sp > 0 ? 5 : 0) + (nb + 4) / 2;
+                const double d = A.dcls[cls];
+                if ((d <= 0.0) || ((accm >> cls) & 1u)) {
+                    lat[site] = (int8_t)(-sp);
+                    my_d = d;
+                    my_ds = -2 * sp;
+                    my_acc = true;
+                }
+            }
+            __syncwarp();
+            pending &= ~__ballot_sync(0xffffffffu, ready);
+        }
+        const unsigned accmask = __ballot_sync(0xffffffffu, my_acc && valid);
+        int ds_scan = my_ds;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, ds_scan, o);
+            if (lane >= o) ds_scan += v;
+        }
+        const long long ssum_lane = ssum + ds_scan;
+        double e_lane;
+        if (A.int_energy) {
+            double d_scan = my_d;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double v = __shfl_up_sync(0xffffffffu, d_scan, o);
+                if (lane >= o) d_scan = __dadd_rn(d_scan, v);
+            }
+            const bool any_before = (accmask & ((2u << lane) - 1u)) != 0u;
+            e_lane = any_before ? __dadd_rn(e, d_scan) : e;
+        } else {
+            double run = e;
+            e_lane = e;
+            for (int k = 0; k < nvalid; ++k) {
+                const double dk = __shfl_sync(0xffffffffu, my_d, k);
+                if ((accmask >> k) & 1u) run = __dadd_rn(run, dk);
+                if (lane == k) e_lane = run;
+            }
+        }
+        if (A.record >= 1 && valid) {
+            const int64_t col = A.start_iter + C.a0 + a;
+            A.obs_e[slot * A.ncols + col] = e_lane;
+            A.obs_m[slot * A.ncols + col] = __ddiv_rn((double)ssum_lane, nsd);
+        }
+        e = __shfl_sync(0xffffffffu, e_lane, nvalid - 1);
+        ssum = __shfl_sync(0xffffffffu, ssum_lane, nvalid - 1);
+    }
+    if (lane == 0) {
+        A.energies[slot] = e;
+        A.spin_sums[slot] = ssum;
+        if (C.last) {
+            A.positions[slot] += 2 * (uint64_t)(C.a0 + C.n);
+            A.iters_done[slot] = A.start_iter + C.a0 + C.n;
+        }
+    }
+}
+
+int64_t advance_chunk(int64_t nslots) {
+    // attempts per slot per phase-1/phase-2 pass: ~16M records (192 MiB)
+    int64_t c = (int64_t(1) << 24) / std::max<int64_t>(1, nslots);
+    c = std::max<int64_t>(1024, std::min<int64_t>(c, 1 << 16));
+    return c & ~int64_t(31);
+}
+
+int64_t advance_ws_bytes(int64_t nslots, int64_t nsteps) {
+    const int64_t stride = std::min(advance_chunk(nslots), (nsteps + 31) & ~int64_t(31));
+    return nslots * stride * 12;
+}
+
+int launch_advance_2phase(const AdvanceArgs& a, void* ws, int64_t ws_bytes, cudaStream_t s) {
+    const int64_t nslots = a.hi - a.lo;
+    if (nslots <= 0 || a.nsteps <= 0) return PTMH_OK;
+    const int64_t stride = std::min(advance_chunk(nslots), (a.nsteps + 31) & ~int64_t(31));
+    if (ws_bytes < nslots * stride * 12) {
+        set_error("advance workspace too small");
+        return PTMH_ERR_ARG;
+    }
+    int32_t* rs = static_cast<int32_t*>(ws);
+    uint32_t* ra = reinterpret_cast<uint32_t*>(rs + nslots * stride);
+    uint32_t* rc = ra + nslots * stride;
+    for (int64_t a0 = 0; a0 < a.nsteps; a0 += stride) {
+        const int64_t n = std::min(stride, a.nsteps - a0);
+        DrawArgs D{a.lo, nslots, a.L, a.tbl, a.dcls, a.seed, a.positions, a0, n, stride, rs, ra, rc};
+        const int64_t npad = (n + 31) & ~int64_t(31);
+        draw_kernel<<<ceil_div(nslots * npad, 256), 256, 0, s>>>(D);
+        PTMH_LAUNCH_CHECK();
+        CommitArgs C{a, a0, n, stride, rs, ra, rc, a0 + n >= a.nsteps};
+        commit_kernel<<<ceil_div(nslots, 4), 128, 0, s>>>(C);
+        PTMH_LAUNCH_CHECK();
+    }
+    return PTMH_OK;
 }
 
 // ------------------------------------------------------------------- swap --

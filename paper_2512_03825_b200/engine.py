@@ -111,6 +111,18 @@ class ExactEngine(_Base):
         """kernels.py:62-113 over slots [lo, hi)."""
         hi = self.R if hi is None else hi
         ncols = obs_e.shape[1] if obs_e is not None else 0
+        if record <= 1 and nsteps > 0 and hi > lo:
+            # two-phase: parallel draws + dependency masks, then a light commit
+            need = int(_lib.LIB.ptmh_advance_workspace_bytes(hi - lo, nsteps))
+            if getattr(self, "_ws", None) is None or self._ws.numel() < need:
+                self._ws = torch.empty(need, dtype=torch.uint8, device=self.dev)
+            _lib.call("ptmh_advance_block_ws", _P(self.spins), self.L, _P(self.slot_to_row), lo,
+                      hi, _P(self.tbl), _P(self.dcls), self.int_energy, _P(self.energies),
+                      _P(self.spin_sums), _P(self.positions), _P(self.iters_done), self.seed,
+                      start_iter, nsteps, _P(obs_e) if record else None,
+                      _P(obs_m) if record else None, ncols, _P(self._ws), self._ws.numel(),
+                      self._s())
+            return
         _lib.call("ptmh_advance_block", _P(self.spins), self.L, _P(self.slot_to_row), lo, hi,
                   _P(self.tbl), _P(self.dcls), self.int_energy, _P(self.energies),
                   _P(self.spin_sums), _P(self.positions), _P(self.iters_done), self.seed,
