@@ -146,7 +146,7 @@ __global__ void advance_kernel(AdvanceArgs A) {
         }
         // --- commit in dependency levels (kernels.py:88-102)
         unsigned pending = __ballot_sync(kFull, valid);
-        double my_d = 0.0;
+        double my_d = -0.0;  // IEEE identity: keeps a reference -0.0 energy intact
         int my_ds = 0;
         bool my_acc = false;
         while (pending) {
@@ -314,6 +314,8 @@ __global__ void __launch_bounds__(128) commit_kernel(CommitArgs C) {
     double e = A.energies[slot];
     long long ssum = A.spin_sums[slot];
     const double nsd = (double)n_sites;
+    double acc_d = -0.0;  // int_energy && record == 0: per-lane partial sums (-0.0: identity)
+    long long acc_ds = 0;
     const int32_t* rs = C.rec_site + s * C.stride;
     const uint32_t* ra = C.rec_acc + s * C.stride;
     const uint32_t* rc = C.rec_conf + s * C.stride;
@@ -352,7 +354,7 @@ __global__ void __launch_bounds__(128) commit_kernel(CommitArgs C) {
         const int64_t up = ((r + 1) % L) * L + c, dn = ((r - 1 + L) % L) * L + c;
         const int64_t rt = r * L + (c + 1) % L, lf = r * L + (c - 1 + L) % L;
         unsigned pending = __ballot_sync(0xffffffffu, valid);
-        double my_d = 0.0;
+        double my_d = -0.0;  // IEEE identity: keeps a reference -0.0 energy intact
         int my_ds = 0;
         bool my_acc = false;
         while (pending) {
@@ -371,6 +373,13 @@ __global__ void __launch_bounds__(128) commit_kernel(CommitArgs C) {
             }
             __syncwarp();
             pending &= ~__ballot_sync(0xffffffffu, ready);
+        }
+        if (A.int_energy && A.record == 0) {
+            // integer increments, nothing recorded: order-free per-lane sums,
+            // reduced once after the last window
+            acc_d = __dadd_rn(acc_d, my_d);
+            acc_ds += my_ds;
+            continue;
         }
         const unsigned accmask = __ballot_sync(0xffffffffu, my_acc && valid);
         int ds_scan = my_ds;
@@ -406,6 +415,14 @@ __global__ void __launch_bounds__(128) commit_kernel(CommitArgs C) {
         }
         e = __shfl_sync(0xffffffffu, e_lane, nvalid - 1);
         ssum = __shfl_sync(0xffffffffu, ssum_lane, nvalid - 1);
+    }
+    if (A.int_energy && A.record == 0) {
+        for (int o = 16; o > 0; o >>= 1) {
+            acc_d = __dadd_rn(acc_d, __shfl_down_sync(0xffffffffu, acc_d, o));
+            acc_ds += __shfl_down_sync(0xffffffffu, acc_ds, o);
+        }
+        e = __dadd_rn(e, acc_d);  // exact (integer-valued); -0.0 when nothing changed
+        ssum += acc_ds;
     }
     if (lane == 0) {
         A.energies[slot] = e;
