@@ -170,8 +170,8 @@ constexpr int kMaxLatPerBlock = 64;
 // Block b owns the contiguous lattices [lo, hi) and sweeps them together:
 // work items (lattice, word) are spread over all threads, __syncthreads
 // separates the colours, per-lattice (S, Bond) accumulate in shared memory.
-template <bool kFast, bool kFerro>
-__global__ void __launch_bounds__(256) cb_resident_kernel(ResidentArgs A) {
+template <bool kFast, bool kFerro, int kThreads>
+__global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
     cg::grid_group grid = cg::this_grid();
     __shared__ int s_slot[kMaxLatPerBlock];
     __shared__ int s_S[kMaxLatPerBlock], s_B[kMaxLatPerBlock];
@@ -265,32 +265,39 @@ __global__ void __launch_bounds__(256) cb_resident_kernel(ResidentArgs A) {
     }
 }
 
-template <bool kFast, bool kFerro>
-static int launch_resident_t(const ResidentArgs& a, cudaStream_t s) {
-    const int threads = 256;
-    int dev = 0, sms = 0, per_sm = 0;
-    PTMH_CUDA(cudaGetDevice(&dev));
-    PTMH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    PTMH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cb_resident_kernel<kFast, kFerro>,
-                                                            threads, 0));
+template <bool kFast, bool kFerro, int kThreads>
+static int launch_resident_t(const ResidentArgs& a, int sms, cudaStream_t s) {
+    int per_sm = 0;
+    PTMH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cb_resident_kernel<kFast, kFerro, kThreads>,
+                                                            kThreads, 0));
     // enough blocks to fill the GPU, few enough that no block owns more
     // lattices than its shared-memory tables hold
-    int grid = std::min(a.R, sms * std::max(1, per_sm));
+    const int grid = std::min(a.R, sms * std::max(1, per_sm));
     if ((a.R + grid - 1) / grid > kMaxLatPerBlock) {
         set_error("resident kernel: too many lattices per block for this grid");
         return PTMH_ERR_ARG;
     }
     ResidentArgs args = a;
     void* kargs[] = {&args};
-    PTMH_CUDA(cudaLaunchCooperativeKernel((const void*)cb_resident_kernel<kFast, kFerro>, grid, threads,
-                                          kargs, 0, s));
+    PTMH_CUDA(cudaLaunchCooperativeKernel((const void*)cb_resident_kernel<kFast, kFerro, kThreads>, grid,
+                                          kThreads, kargs, 0, s));
     return PTMH_OK;
+}
+
+template <bool kFast, bool kFerro>
+static int launch_resident_sized(const ResidentArgs& a, cudaStream_t s) {
+    int dev = 0, sms = 0;
+    PTMH_CUDA(cudaGetDevice(&dev));
+    PTMH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    // fewer lattices than SMs and big lattices: one wide CTA per lattice
+    if (a.R < sms && a.W >= 1024) return launch_resident_t<kFast, kFerro, 1024>(a, sms, s);
+    return launch_resident_t<kFast, kFerro, 256>(a, sms, s);
 }
 
 int launch_cb_resident(const ResidentArgs& a, bool fast, cudaStream_t s, int* grid_out) {
     (void)grid_out;
-    if (fast) return a.ferro ? launch_resident_t<true, true>(a, s) : launch_resident_t<true, false>(a, s);
-    return a.ferro ? launch_resident_t<false, true>(a, s) : launch_resident_t<false, false>(a, s);
+    if (fast) return a.ferro ? launch_resident_sized<true, true>(a, s) : launch_resident_sized<true, false>(a, s);
+    return a.ferro ? launch_resident_sized<false, true>(a, s) : launch_resident_sized<false, false>(a, s);
 }
 
 }  // namespace ptmh

@@ -167,8 +167,44 @@ def run_vectors():
                                        rec.swaps_accepted], dtype=np.int64))
 
 
+def cli_vectors():
+    """The reference CLI on small sweeps: observables.csv digests and the
+    timings columns that do not depend on wall time."""
+    import hashlib
+    import tempfile
+    from isingpt import cli
+    out = {}
+    cases = {
+        "single": ["--size", "8", "--replicas", "4", "--iters", "2000", "--swap-interval", "50",
+                   "--seed", "7", "--record", "observables"],
+        "replica_sweep": ["--size", "6", "--iters", "1500", "--swap-interval", "30",
+                          "--sweep", "replica_scaling", "--axis", "2,3", "--reps", "2",
+                          "--record", "observables"],
+        "worker_sweep": ["--size", "6", "--replicas", "3", "--iters", "800",
+                         "--sweep", "worker_scaling", "--axis", "1,2", "--record", "none"],
+    }
+    for name, argv in cases.items():
+        with tempfile.TemporaryDirectory() as d:
+            rc = cli.main(argv + ["--out", d])
+            files = sorted(os.listdir(d))
+            digests = {f: hashlib.sha256(open(os.path.join(d, f), "rb").read()).hexdigest()
+                       for f in files if f.startswith("observables")}
+            rows = open(os.path.join(d, "timings.csv")).read().splitlines()
+            hdr = rows[0].split(",")
+            keep = [i for i, c in enumerate(hdr) if c not in ("init_s", "exec_s", "total_s")]
+            stable = [",".join(r.split(",")[i] for i in keep) for r in rows]
+            out[name] = {"argv": argv, "rc": rc, "files": files, "digests": digests,
+                         "timings_stable": stable}
+    seeds = {f"{m}|{p}|{r}": cli.derive_seed(m, p, r)
+             for m in (0, 42, 2 ** 40) for p in ("", "single", "R=16", "L=8") for r in (0, 1, 5)}
+    import json
+    with open(os.path.join(OUT, "cli.json"), "w") as f:
+        json.dump({"cases": out, "seeds": seeds}, f, indent=1)
+
+
 if __name__ == "__main__":
     kernels.warm_kernels()
+    cli_vectors()
     philox_vectors()
     kernel_vectors()
     run_vectors()
