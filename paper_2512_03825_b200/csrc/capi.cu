@@ -72,12 +72,16 @@ struct Buf {
     size_t n = 0;
 };
 
+constexpr int kComputeStreams = 4;
+
 struct Workspace {
     std::mutex mu;
     int device = -1;
     std::vector<Buf> bufs;
     cudaStream_t s[3] = {nullptr, nullptr, nullptr};
+    cudaStream_t cs[kComputeStreams] = {};  // concurrent chunk compute
     cudaEvent_t ev_in[64], ev_out[64];  // >= chunks per pipelined call
+    cudaEvent_t ev_t0, ev_tab;
     bool events = false;
 };
 
@@ -89,16 +93,22 @@ static int ws_prepare(Workspace& w) {
     if (w.device != dev) {
         w.bufs.clear();  // a device switch leaks the old buffers on purpose
         for (auto& st : w.s) st = nullptr;
+        for (auto& st : w.cs) st = nullptr;
         w.events = false;
         w.device = dev;
     }
     for (auto& st : w.s)
         if (!st) PTMH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    for (auto& st : w.cs)
+        if (!st) PTMH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     if (!w.events) {
         for (int k = 0; k < 64; ++k) {
-            PTMH_CUDA(cudaEventCreateWithFlags(&w.ev_in[k], cudaEventDisableTiming));
-            PTMH_CUDA(cudaEventCreateWithFlags(&w.ev_out[k], cudaEventDisableTiming));
+            const unsigned fl = getenv("PTMH_TRACE") ? cudaEventDefault : cudaEventDisableTiming;
+            PTMH_CUDA(cudaEventCreateWithFlags(&w.ev_in[k], fl));
+            PTMH_CUDA(cudaEventCreateWithFlags(&w.ev_out[k], fl));
         }
+        PTMH_CUDA(cudaEventCreate(&w.ev_t0));
+        PTMH_CUDA(cudaEventCreateWithFlags(&w.ev_tab, cudaEventDisableTiming));
         w.events = true;
     }
     return PTMH_OK;
@@ -457,7 +467,8 @@ int ptmh_host_cb_interval(int8_t* spins, int64_t R, int64_t L, int64_t* slot_to_
     // pipeline over replica chunks: all H2D copies are issued first, then the
     // compute chain (each chunk waits for its copy), then the D2H copies (each
     // waits for its chunk), so no queue ever blocks behind a later dependency
-    const int64_t nch = std::min<int64_t>(R, 8);
+    const int64_t nch = std::min<int64_t>(R, 16);
+    if (getenv("PTMH_TRACE")) PTMH_CUDA(cudaEventRecord(g_ws.ev_t0, sin));
     auto chunk = [&](int64_t c, int64_t& lo, int64_t& n) {
         lo = R * c / nch;
         n = R * (c + 1) / nch - lo;
@@ -469,16 +480,21 @@ int ptmh_host_cb_interval(int8_t* spins, int64_t R, int64_t L, int64_t* slot_to_
                                   cudaMemcpyHostToDevice, sin));
         PTMH_CUDA(cudaEventRecord(g_ws.ev_in[c], sin));
     }
+    // the small tables above are on sc: every compute stream starts after them
+    PTMH_CUDA(cudaEventRecord(g_ws.ev_tab, sc));
     for (int64_t c = 0; c < nch; ++c) {
         int64_t lo, n;
         chunk(c, lo, n);
-        PTMH_CUDA(cudaStreamWaitEvent(sc, g_ws.ev_in[c], 0));
-        PTMH_TRY(launch_cb_pack(d_spins + lo * nsite, n, L, d_packed + lo * 2 * W, sc));
-        PTMH_TRY(launch_cb_row_stats(d_packed + lo * 2 * W, n, L, d_stats + 2 * lo, sc));
+        cudaStream_t cst = g_ws.cs[c % kComputeStreams];  // a chunk alone does not fill the GPU
+        PTMH_CUDA(cudaStreamWaitEvent(cst, g_ws.ev_tab, 0));
+        PTMH_CUDA(cudaStreamWaitEvent(cst, g_ws.ev_in[c], 0));
+        PTMH_TRY(launch_cb_pack(d_spins + lo * nsite, n, L, d_packed + lo * 2 * W, cst));
+        PTMH_TRY(launch_cb_row_stats(d_packed + lo * 2 * W, n, L, d_stats + 2 * lo, cst));
         PTMH_TRY(launch_cb_sweeps(d_packed + lo * 2 * W, n, L, d_r2s + lo, d_thr, always, seed, first_sweep,
-                                  n_sweeps, d_stats + 2 * lo, sc));
-        PTMH_TRY(launch_cb_unpack(d_packed + lo * 2 * W, n, L, d_spins + lo * nsite, sc));
-        PTMH_CUDA(cudaEventRecord(g_ws.ev_out[c], sc));
+                                  n_sweeps, d_stats + 2 * lo, cst));
+        PTMH_TRY(launch_cb_unpack(d_packed + lo * 2 * W, n, L, d_spins + lo * nsite, cst));
+        PTMH_CUDA(cudaEventRecord(g_ws.ev_out[c], cst));
+        PTMH_CUDA(cudaStreamWaitEvent(sc, g_ws.ev_out[c], 0));  // the exchange needs every chunk
     }
     for (int64_t c = 0; c < nch; ++c) {
         int64_t lo, n;
@@ -486,6 +502,17 @@ int ptmh_host_cb_interval(int8_t* spins, int64_t R, int64_t L, int64_t* slot_to_
         PTMH_CUDA(cudaStreamWaitEvent(sout, g_ws.ev_out[c], 0));
         PTMH_CUDA(cudaMemcpyAsync(spins + lo * nsite, d_spins + lo * nsite, (size_t)(n * nsite),
                                   cudaMemcpyDeviceToHost, sout));
+    }
+    if (getenv("PTMH_TRACE")) {  // per-chunk timeline (tools/ only)
+        PTMH_CUDA(cudaStreamSynchronize(sout));
+        PTMH_CUDA(cudaStreamSynchronize(sc));
+        float t_in = 0, t_out = 0;
+        for (int64_t c = 0; c < nch; ++c) {
+            PTMH_CUDA(cudaEventElapsedTime(&t_in, g_ws.ev_t0, g_ws.ev_in[c]));
+            PTMH_CUDA(cudaEventElapsedTime(&t_out, g_ws.ev_t0, g_ws.ev_out[c]));
+            fprintf(stderr, "ptmh trace chunk %ld: h2d done %.3f ms, compute done %.3f ms\n", (long)c, t_in,
+                    t_out);
+        }
     }
     PTMH_TRY(launch_cb_slot_energies(d_stats, d_s2r, R, J, B, d_e, d_sums, sc));
     if (round_index >= 0) {

@@ -277,14 +277,20 @@ __global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_half_sweep_ferro(
             const uint4 r1 = philox4x32_10(make_uint4(2u * w32 + 1u, ctr1, (uint32_t)slot, 0u), rk);
             const uint32_t U[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
             acc |= K2 & ~U[0];  // neutral: u < 2^31 <=> top bit clear
-            uint32_t lt = 0, eq = upm;
+            // byte compare u < t as the borrow of u - t, LSB plane first
+            // (borrow' = MAJ(~u, t, borrow): one LOP3), plus the equality
+            // chain for the ties; K4 pinned in a register so the per-site
+            // threshold plane is a single select
+            uint32_t K4r = K4;
+            asm volatile("" : "+r"(K4r));
+            uint32_t bor = 0, eq = upm;
 #pragma unroll
-            for (int p = 0; p < 8; ++p) {
-                const uint32_t Tm = (K4 & TB[p]) | (~K4 & TA[p]);
-                lt |= eq & ~U[p] & Tm;
+            for (int p = 7; p >= 0; --p) {
+                const uint32_t Tm = (K4r & TB[p]) | (~K4r & TA[p]);
+                bor = (~U[p] & Tm) | (~U[p] & bor) | (Tm & bor);
                 eq &= ~(U[p] ^ Tm);
             }
-            acc |= lt;
+            acc |= bor & upm;
             // ties (top byte equal): bookkeeping only, resolved after the loop
             tie_m[warp][rr][lane] = eq;
             tie_k4[warp][rr][lane] = eq & K4;

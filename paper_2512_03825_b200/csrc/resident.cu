@@ -87,15 +87,17 @@ __device__ __forceinline__ void resident_word(const ResidentArgs& A, uint32_t* o
         const uint4 r1 = philox4x32_10(make_uint4(2u * (uint32_t)w + 1u, ctr1, (uint32_t)slot, 0u), A.rk);
         const uint32_t U[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
         acc |= K2 & ~U[0];
-        uint32_t lt = 0, eq = upm;
+        uint32_t K4r = K4;
+        asm volatile("" : "+r"(K4r));
+        uint32_t bor = 0, eq = upm;  // borrow of u - t (LSB first) + ties
 #pragma unroll
-        for (int p = 0; p < 8; ++p) {
+        for (int p = 7; p >= 0; --p) {
             const uint32_t TA = 0u - ((t3 >> (31 - p)) & 1u), TB = 0u - ((t4 >> (31 - p)) & 1u);
-            const uint32_t Tm = (K4 & TB) | (~K4 & TA);
-            lt |= eq & ~U[p] & Tm;
+            const uint32_t Tm = (K4r & TB) | (~K4r & TA);
+            bor = (~U[p] & Tm) | (~U[p] & bor) | (Tm & bor);
             eq &= ~(U[p] ^ Tm);
         }
-        acc |= lt;
+        acc |= bor & upm;
         while (eq) {
             const int bit = __ffs(eq) - 1;
             eq &= eq - 1;
