@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(256) cb_half_sweep_fast(
 // colour-1 pass recomputes them from the new configuration -- S from both
 // colours' words, Bond = sum over colour-1 sites of s*nb (every bond has
 // exactly one colour-1 end) -- plus the deltas of its own tie flips.
-constexpr int kQCap = 128;
+constexpr int kQCap = 64;
 #ifndef PTMH_FERRO_MINB
 #define PTMH_FERRO_MINB 1
 #endif
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_half_sweep_ferro(
     uint32_t ctr1, int color, int64_t* __restrict__ stats) {
     constexpr int kWarps = 8;
     __shared__ uint32_t q_gw[kWarps][kQCap], q_h[kWarps][kQCap], q_sl[kWarps][kQCap], q_info[kWarps][kQCap];
-    __shared__ uint32_t tie_m[kWarps][kRows][32], tie_k4[kWarps][kRows][32], tie_s[kWarps][kRows][32];
+    __shared__ uint32_t tie_m[kWarps][kRows][32], tie_k4[kWarps][kRows][32];
     __shared__ int extra_s[kWarps][32], extra_b[kWarps][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -294,7 +294,6 @@ __global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_half_sweep_ferro(
             // ties (top byte equal): bookkeeping only, resolved after the loop
             tie_m[warp][rr][lane] = eq;
             tie_k4[warp][rr][lane] = eq & K4;
-            tie_s[warp][rr][lane] = eq & S;
             any_tie |= eq;
             const uint32_t Sn = S ^ acc;
             if (acc) own[row + k] = Sn;
@@ -334,8 +333,10 @@ __global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_half_sweep_ferro(
         if (cnt) {
             for (int rr = 0; rr < kRows; ++rr) {
                 uint32_t m = tie_m[warp][rr][lane];
-                const uint32_t mk4 = tie_k4[warp][rr][lane], ms = tie_s[warp][rr][lane];
+                const uint32_t mk4 = tie_k4[warp][rr][lane];
                 const uint32_t w32 = (uint32_t)((i0 + rr) * WR + k);
+                // a tie site was not flipped in the row pass: its spin is in the stored word
+                const uint32_t ms = m ? packed[own_base + w32] : 0u;
                 while (m) {
                     const int bit = __ffs(m) - 1;
                     m &= m - 1;
@@ -576,7 +577,10 @@ void fill_class_plan(uint32_t always_mask, int* n_up, int* k, int* sf, int* cls,
     *ferro = (always_mask & kSymmetricFlag) && (always_mask & 0x3ffu) == 0x078u;
 }
 
-constexpr int kFastRows = 8;
+#ifndef PTMH_FERRO_ROWS
+#define PTMH_FERRO_ROWS 8
+#endif
+constexpr int kFastRows = PTMH_FERRO_ROWS;
 
 int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* row_to_slot,
                      const uint32_t* thresh, uint32_t always_mask, uint64_t seed, int64_t first_sweep,
@@ -592,7 +596,16 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
     for (int64_t t = first_sweep; t < first_sweep + n_sweeps; ++t) {
         for (int color = 0; color < 2; ++color) {
             const uint32_t ctr1 = (uint32_t)(2 * t + color);
-            if (fast && ferro) {
+            if (fast && ferro && L >= 2048) {  // long rows: amortise the per-thread setup over 16
+                const int WR = (int)(L / 64);
+                const int64_t threads = rows * (L / 16) * WR;
+                if (color == 0)
+                    cb_half_sweep_ferro<16, false><<<ceil_div(threads, 256), 256, 0, s>>>(
+                        packed, rows, (int)L, WR, W, row_to_slot, thresh, rk, ctr1, color, stats);
+                else
+                    cb_half_sweep_ferro<16, true><<<ceil_div(threads, 256), 256, 0, s>>>(
+                        packed, rows, (int)L, WR, W, row_to_slot, thresh, rk, ctr1, color, stats);
+            } else if (fast && ferro) {
                 const int WR = (int)(L / 64);
                 const int64_t threads = rows * (L / kFastRows) * WR;
                 if (color == 0)

@@ -225,3 +225,20 @@ def test_resident_segments_compose(mods):
         assert np.array_equal(o[1], outs[0][1])
         assert o[2] == outs[0][2]
         assert np.array_equal(o[3], outs[0][3])
+
+
+def test_sweeps_match_oracle_at_2048(mods):
+    """L >= 2048 takes the 16-rows-per-thread fast-path instantiation."""
+    p, engine, _, _ = mods
+    L, R = 2048, 2
+    temps = np.array([1.8, 2.6])
+    eng = engine.CheckerboardEngine(L, R, temps, 21, 1.0, 0.0, 0.5, 0)
+    eng.init_state()
+    sp0 = eng.final_spins()
+    eng.sweeps(0, 1)
+    ref = sp0.copy()
+    stats = oracle.row_stats(ref)
+    thr, always = oracle.cb_tables(1.0 / temps, 1.0, 0.0)
+    oracle.cb_sweep(ref, np.arange(R, dtype=np.int64), thr, always, 21, 0, stats)
+    assert np.array_equal(eng.final_spins(), ref)
+    assert np.array_equal(eng.local_stats.cpu().numpy(), stats)
