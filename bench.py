@@ -62,6 +62,15 @@ def _peaks():
         return 6650.0, "fallback"
 
 
+def _issue(cfg_name):
+    """IPC / ALU-pipe share of the hot kernel from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_sweep_summary.json")) as f:
+            return json.load(f)[cfg_name].get("issue")
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def _traffic(cfg_name):
     """dram bytes per half-sweep launch from the committed ncu --set full
     capture summary (profiles/), or None."""
@@ -358,7 +367,8 @@ def main():
                              "frac": achieved / peak, "traffic": traffic,
                              "kernel": kernel_name, "launch_ms": launch_ms,
                              "alg_bytes_per_launch": bytes_per_launch, "peak_kind": peak_kind,
-                             "note": "issue-bound (Philox + bit-sliced logic), see DESIGN.md 5"},
+                             "note": "issue-bound (Philox + bit-sliced logic), see DESIGN.md 5",
+                             "issue_from_ncu": _issue(args.config) if not resident else None},
                 "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": args.steps * (1 if resident else 2 * every + 2),
                 "clocks": clk.summary()}
