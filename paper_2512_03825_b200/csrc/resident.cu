@@ -38,12 +38,12 @@ __device__ __forceinline__ uint32_t resident_bit(const uint32_t* p, int h) {
 template <bool kFast, bool kFerro>
 __device__ __forceinline__ void resident_word(const ResidentArgs& A, uint32_t* own, const uint32_t* oth,
                                               int w, int color, int slot, uint32_t ctr1, int& sumS,
-                                              int& sumB, bool stats) {
+                                              int& sumB, bool stats, const uint32_t* masks, int wr_shift) {
     const int L = A.L;
     uint32_t S = own[w], n1, n2, n3, n4, valid;
     if (kFast) {
         const int WR = A.WR;
-        const int i = w / WR, k = w - i * WR;
+        const int i = wr_shift >= 0 ? (w >> wr_shift) : w / WR, k = w - i * WR;
         const int iu = (i == 0) ? L - 1 : i - 1, id = (i == L - 1) ? 0 : i + 1;
         const uint32_t mid = oth[w];
         n1 = oth[iu * WR + k];
@@ -81,7 +81,7 @@ __device__ __forceinline__ void resident_word(const ResidentArgs& A, uint32_t* o
     if (kFerro) {
         // J > 0, B = 0: k <= 1 always, k = 2 with probability 1/2, k = 3, 4 thresholds
         const uint32_t K4 = k2, upm = ((k1 & k0) | k2) & valid, K2 = k1 & ~k0 & valid;
-        const uint32_t t3 = __ldg(thr + 8), t4 = __ldg(thr + 9);
+        const uint32_t t3 = masks[16], t4 = masks[17];  // per-lattice, in shared memory
         acc = ~(k1 | k2) & valid;
         const uint4 r0 = philox4x32_10(make_uint4(2u * (uint32_t)w, ctr1, (uint32_t)slot, 0u), A.rk);
         const uint4 r1 = philox4x32_10(make_uint4(2u * (uint32_t)w + 1u, ctr1, (uint32_t)slot, 0u), A.rk);
@@ -92,8 +92,7 @@ __device__ __forceinline__ void resident_word(const ResidentArgs& A, uint32_t* o
         uint32_t bor = 0, eq = upm;  // borrow of u - t (LSB first) + ties
 #pragma unroll
         for (int p = 7; p >= 0; --p) {
-            const uint32_t TA = 0u - ((t3 >> (31 - p)) & 1u), TB = 0u - ((t4 >> (31 - p)) & 1u);
-            const uint32_t Tm = (K4r & TB) | (~K4r & TA);
+            const uint32_t Tm = (K4r & masks[8 + p]) | (~K4r & masks[p]);
             bor = (~U[p] & Tm) | (~U[p] & bor) | (Tm & bor);
             eq &= ~(U[p] ^ Tm);
         }
@@ -174,9 +173,11 @@ constexpr int kMaxLatPerBlock = 64;
 // separates the colours, per-lattice (S, Bond) accumulate in shared memory.
 template <bool kFast, bool kFerro, int kThreads>
 __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
-    cg::grid_group grid = cg::this_grid();
     __shared__ int s_slot[kMaxLatPerBlock];
     __shared__ int s_S[kMaxLatPerBlock], s_B[kMaxLatPerBlock];
+    __shared__ double s_u[kMaxLatPerBlock];
+    __shared__ uint32_t s_mask[kFerro ? kMaxLatPerBlock : 1][18];  // TA[8], TB[8], t3, t4
+    const int wr_shift = (A.WR > 0 && (A.WR & (A.WR - 1)) == 0) ? __ffs(A.WR) - 1 : -1;
     const int R = A.R, W = A.W;
     const int lo = (int)((int64_t)R * blockIdx.x / gridDim.x);
     const int hi = (int)((int64_t)R * (blockIdx.x + 1) / gridDim.x);
@@ -189,24 +190,61 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
         const bool exch = A.swap_every > 0 && done % A.swap_every == 0 && done < A.total_sweeps;
         const bool need_stats = rec || exch || t + 1 == A.first_sweep + A.n_sweeps;
         for (int i = threadIdx.x; i < nl; i += blockDim.x) {
-            s_slot[i] = A.r2s[buf][lo + i];
+            const int sl = A.r2s[buf][lo + i];
+            s_slot[i] = sl;
             s_S[i] = 0;
             s_B[i] = 0;
+            if (kFerro) {
+                const uint32_t t3 = __ldg(A.thresh + sl * 10 + 8), t4 = __ldg(A.thresh + sl * 10 + 9);
+                for (int p = 0; p < 8; ++p) {
+                    s_mask[i][p] = 0u - ((t3 >> (31 - p)) & 1u);
+                    s_mask[i][8 + p] = 0u - ((t4 >> (31 - p)) & 1u);
+                }
+                s_mask[i][16] = t3;
+                s_mask[i][17] = t4;
+            }
         }
         __syncthreads();
         for (int color = 0; color < 2; ++color) {
             const uint32_t ctr1 = (uint32_t)(2 * t + color);
             const bool st = color == 1 && need_stats;
-            for (int it = threadIdx.x; it < items; it += blockDim.x) {
-                const int li = it / W, w = it - li * W;
-                uint32_t* c0 = A.packed + (int64_t)(lo + li) * 2 * W;
-                uint32_t* own = color ? c0 + W : c0;
-                const uint32_t* oth = color ? c0 : c0 + W;
+            // whole warps iterate together so the stats can be warp-reduced
+            const int items_pad = (items + 31) & ~31;
+            // (li, w) of item `it`, advanced incrementally (no division in the loop)
+            int li_c = (int)threadIdx.x / W, w_c = (int)threadIdx.x - li_c * W;
+            const int step_l = (int)blockDim.x / W, step_w = (int)blockDim.x - step_l * W;
+            for (int it = threadIdx.x; it < items_pad; it += blockDim.x) {
+                const bool on = it < items;
+                const int li = on ? li_c : 0, w = on ? w_c : 0;
+                li_c += step_l;
+                w_c += step_w;
+                if (w_c >= W) {
+                    w_c -= W;
+                    ++li_c;
+                }
                 int sS = 0, sB = 0;
-                resident_word<kFast, kFerro>(A, own, oth, w, color, s_slot[li], ctr1, sS, sB, st);
+                if (on) {
+                    uint32_t* c0 = A.packed + (int64_t)(lo + li) * 2 * W;
+                    uint32_t* own = color ? c0 + W : c0;
+                    const uint32_t* oth = color ? c0 : c0 + W;
+                    resident_word<kFast, kFerro>(A, own, oth, w, color, s_slot[li], ctr1, sS, sB, st,
+                                                 kFerro ? s_mask[li] : nullptr, wr_shift);
+                }
                 if (st) {
-                    atomicAdd(&s_S[li], sS);
-                    atomicAdd(&s_B[li], sB);
+                    const int li0 = __shfl_sync(0xffffffffu, li, 0);
+                    if (__all_sync(0xffffffffu, li == li0 || !on)) {  // one lattice: one atomic
+                        for (int o = 16; o > 0; o >>= 1) {
+                            sS += __shfl_down_sync(0xffffffffu, sS, o);
+                            sB += __shfl_down_sync(0xffffffffu, sB, o);
+                        }
+                        if ((threadIdx.x & 31) == 0) {
+                            atomicAdd(&s_S[li0], sS);
+                            atomicAdd(&s_B[li0], sB);
+                        }
+                    } else if (on) {
+                        atomicAdd(&s_S[li], sS);
+                        atomicAdd(&s_B[li], sB);
+                    }
                 }
             }
             __syncthreads();
@@ -225,11 +263,20 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
             }
         }
         if (!exch) continue;
-        grid.sync();  // every lattice's (S, Bond) is final
-        // ---- exchange round: the owner of lattice r decides the pair of its slot
+        // the swap draw depends only on (round, pair): draw it before the barrier
         const int64_t round = done / A.swap_every - 1;
         const int first = (int)(round % 2);
         const int n_pairs = (R - first) / 2;
+        for (int li = threadIdx.x; li < nl; li += blockDim.x) {
+            const int k = s_slot[li];
+            s_u[li] = (k >= first && (k - first) / 2 < n_pairs)
+                          ? stream_uniform(A.seed, (uint64_t)(R + (k - first) / 2), (uint64_t)round)
+                          : 0.0;
+        }
+        // every lattice's (S, Bond) is final.  (A point-to-point flag scheme
+        // without this barrier was measured slower: DESIGN.md 5.)
+        cg::this_grid().sync();
+        // ---- exchange round: the owner of lattice r decides the pair of its slot
         for (int li = threadIdx.x; li < nl; li += blockDim.x) {
             const int r = lo + li;
             const int k = s_slot[li];
@@ -242,7 +289,7 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
                                             __dmul_rn(A.J, (double)A.stats[2 * ri + 1]));
                 const double Ej = __dsub_rn(__dmul_rn(A.B, (double)A.stats[2 * rj]),
                                             __dmul_rn(A.J, (double)A.stats[2 * rj + 1]));
-                const double u = stream_uniform(A.seed, (uint64_t)(R + p), (uint64_t)round);
+                const double u = s_u[li];
                 const double x = __dmul_rn(__dsub_rn(A.betas[i], A.betas[j]), __dsub_rn(Ei, Ej));
                 double prob;
                 if (x >= 0.0) {
