@@ -197,7 +197,6 @@ __global__ void __launch_bounds__(256) cb_half_sweep_fast(
 // colour-1 pass recomputes them from the new configuration -- S from both
 // colours' words, Bond = sum over colour-1 sites of s*nb (every bond has
 // exactly one colour-1 end) -- plus the deltas of its own tie flips.
-constexpr int kQCap = 64;
 #ifndef PTMH_FERRO_MINB
 #define PTMH_FERRO_MINB 1
 #endif
@@ -208,9 +207,7 @@ __global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_half_sweep_ferro(
     const int32_t* __restrict__ row_to_slot, const uint32_t* __restrict__ thresh, const RoundKeys32 rk,
     uint32_t ctr1, int color, int64_t* __restrict__ stats) {
     constexpr int kWarps = 8;
-    __shared__ uint32_t q_gw[kWarps][kQCap], q_h[kWarps][kQCap], q_sl[kWarps][kQCap], q_info[kWarps][kQCap];
     __shared__ uint32_t tie_m[kWarps][kRows][32], tie_k4[kWarps][kRows][32];
-    __shared__ int extra_s[kWarps][32], extra_b[kWarps][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -226,7 +223,7 @@ __global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_half_sweep_ferro(
     int slot = 0;
     uint32_t t3 = 0, t4 = 0;
     int sumS = 0, sumB = 0;
-    uint32_t any_tie = 0;
+    uint32_t tie_rows = 0;  // bit rr: row rr has ties
     if (active) {
         if (!kStats && rem == 0) {  // colour-0 pass: reset, colour-1 pass recomputes
             stats[2 * lat] = 0;
@@ -294,7 +291,7 @@ __global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_half_sweep_ferro(
             // ties (top byte equal): bookkeeping only, resolved after the loop
             tie_m[warp][rr][lane] = eq;
             tie_k4[warp][rr][lane] = eq & K4;
-            any_tie |= eq;
+            tie_rows |= (eq != 0u ? 1u : 0u) << rr;
             const uint32_t Sn = S ^ acc;
             if (acc) own[row + k] = Sn;
             if (kStats) {
@@ -310,83 +307,44 @@ __global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_half_sweep_ferro(
             adj = adj_n;
         }
     }
-    // ---- tie resolution: build one warp queue, 32 secondary draws per pass
-    if (kStats) {
-        extra_s[warp][lane] = 0;
-        extra_b[warp][lane] = 0;
-    }
-    if (__any_sync(kFullMask, any_tie != 0)) {
-        int cnt = 0;
-        if (any_tie) {
-#pragma unroll
-            for (int rr = 0; rr < kRows; ++rr) cnt += __popc(tie_m[warp][rr][lane]);
-        }
-        int off = cnt;  // inclusive scan -> exclusive offset
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_up_sync(kFullMask, off, o);
-            if (lane >= o) off += v;
-        }
-        const int total = __shfl_sync(kFullMask, off, 31);
-        off -= cnt;
-        const bool queued = total <= kQCap;
-        if (cnt) {
-            for (int rr = 0; rr < kRows; ++rr) {
-                uint32_t m = tie_m[warp][rr][lane];
-                const uint32_t mk4 = tie_k4[warp][rr][lane];
-                const uint32_t w32 = (uint32_t)((i0 + rr) * WR + k);
-                // a tie site was not flipped in the row pass: its spin is in the stored word
-                const uint32_t ms = m ? packed[own_base + w32] : 0u;
-                while (m) {
-                    const int bit = __ffs(m) - 1;
-                    m &= m - 1;
-                    const uint32_t k4 = (mk4 >> bit) & 1u, sb = (ms >> bit) & 1u;
-                    const uint32_t t24 = (k4 ? t4 : t3) & 0x00ffffffu;
-                    const uint32_t info = t24 | (k4 << 24) | (sb << 25) | ((uint32_t)lane << 26);
-                    if (queued) {
-                        q_gw[warp][off] = own_base + w32;
-                        q_h[warp][off] = w32 * 32u + (uint32_t)bit;
-                        q_sl[warp][off] = (uint32_t)slot;
-                        q_info[warp][off] = info;
-                        ++off;
-                    } else {  // more ties than the queue holds: resolve in place
-                        const uint4 r2 =
-                            philox4x32_10(make_uint4(w32 * 32u + (uint32_t)bit, ctr1, (uint32_t)slot, 1u), rk);
-                        if ((r2.x >> 8) < t24) {
-                            atomicXor(packed + own_base + w32, 1u << bit);
-                            if (kStats) {
-                                sumS += sb ? -2 : 2;
-                                sumB += k4 ? -8 : -4;
-                            }
-                        }
-                    }
-                }
+    // ---- tie resolution: every lane walks its own ties (top byte equal)
+    // across all its rows; the warp iterates max-ties-per-lane times.  The
+    // lane owns its words, so accepted ties flip them with a plain
+    // read-modify-write, and it accounts their (S, Bond) deltas itself.
+    {
+        int rr = -1;
+        uint32_t m = 0, mk4 = 0, Sw = 0, w32 = 0;
+        bool dirty = false;
+        while (__any_sync(kFullMask, tie_rows != 0 || m != 0)) {
+            if (m == 0 && tie_rows != 0) {
+                rr = __ffs(tie_rows) - 1;
+                tie_rows &= tie_rows - 1;
+                m = tie_m[warp][rr][lane];
+                mk4 = tie_k4[warp][rr][lane];
+                w32 = (uint32_t)((i0 + rr) * WR + k);
+                Sw = packed[own_base + w32];
+                dirty = false;
             }
-        }
-        __syncwarp();
-        const int nq = queued ? total : 0;
-        for (int base = 0; base < nq; base += 32) {
-            const int e = base + lane;
-            if (e < nq) {
-                const uint32_t h = q_h[warp][e], info = q_info[warp][e];
-                const uint4 r2 = philox4x32_10(make_uint4(h, ctr1, q_sl[warp][e], 1u), rk);
-                if ((r2.x >> 8) < (info & 0x00ffffffu)) {
-                    atomicXor(packed + q_gw[warp][e], 1u << (h & 31u));
+            if (m != 0) {
+                const int bit = __ffs(m) - 1;
+                m &= m - 1;
+                const uint32_t k4 = (mk4 >> bit) & 1u;
+                const uint32_t t24 = (k4 ? t4 : t3) & 0x00ffffffu;
+                const uint4 r2 =
+                    philox4x32_10(make_uint4(w32 * 32u + (uint32_t)bit, ctr1, (uint32_t)slot, 1u), rk);
+                if ((r2.x >> 8) < t24) {
                     if (kStats) {
-                        const uint32_t owner = info >> 26;
-                        atomicAdd(&extra_s[warp][owner], ((info >> 25) & 1u) ? -2 : 2);
-                        atomicAdd(&extra_b[warp][owner], ((info >> 24) & 1u) ? -8 : -4);
+                        sumS += ((Sw >> bit) & 1u) ? -2 : 2;
+                        sumB += k4 ? -8 : -4;
                     }
+                    Sw ^= 1u << bit;
+                    dirty = true;
                 }
+                if (m == 0 && dirty) packed[own_base + w32] = Sw;
             }
         }
     }
-    if (kStats) {
-        __syncwarp();
-        sumS += extra_s[warp][lane];
-        sumB += extra_b[warp][lane];
-        flush_stats(stats, lat, active, sumS, sumB);
-    }
+    if (kStats) flush_stats(stats, lat, active, sumS, sumB);
 }
 
 // ------------------------------------------------------- generic even L --
@@ -596,7 +554,7 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
     for (int64_t t = first_sweep; t < first_sweep + n_sweeps; ++t) {
         for (int color = 0; color < 2; ++color) {
             const uint32_t ctr1 = (uint32_t)(2 * t + color);
-            if (fast && ferro && L >= 2048) {  // long rows: amortise the per-thread setup over 16
+            if (fast && ferro && L >= 1024) {  // long rows: amortise the per-thread setup over 16
                 const int WR = (int)(L / 64);
                 const int64_t threads = rows * (L / 16) * WR;
                 if (color == 0)

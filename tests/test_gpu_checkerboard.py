@@ -228,7 +228,7 @@ def test_resident_segments_compose(mods):
 
 
 def test_sweeps_match_oracle_at_2048(mods):
-    """L >= 2048 takes the 16-rows-per-thread fast-path instantiation."""
+    """L >= 1024 takes the 16-rows-per-thread fast-path instantiation (also at 2048)."""
     p, engine, _, _ = mods
     L, R = 2048, 2
     temps = np.array([1.8, 2.6])
