@@ -131,6 +131,23 @@ int ptmh_advance_block_ws(int8_t *spins, int64_t L, const int64_t *slot_to_row,
                           int64_t ncols, void *workspace, int64_t ws_bytes,
                           void *stream);
 
+/* Bit-packed exact-chain lattices: site x of row r is bit (x & 31) of word
+ * bits[r*ceil(L*L/32) + (x >> 5)], set <=> +1.  ptmh_advance_block_bits is
+ * ptmh_advance_block_ws on that representation (same results; 1 bit per spin
+ * keeps large lattice sets L2-resident for the random-site commits). */
+int ptmh_bits_pack(const int8_t *spins, int64_t rows, int64_t L, uint32_t *bits,
+                   void *stream);
+int ptmh_bits_unpack(const uint32_t *bits, int64_t rows, int64_t L,
+                     int8_t *spins, void *stream);
+int ptmh_advance_block_bits(uint32_t *bits, int64_t L, const int64_t *slot_to_row,
+                            int64_t lo, int64_t hi, const double *tbl,
+                            const double *dcls, int int_energy,
+                            double *energies, int64_t *spin_sums,
+                            uint64_t *positions, int64_t *iters_done,
+                            uint64_t seed, int64_t start_iter, int64_t nsteps,
+                            double *obs_e, double *obs_m, int64_t ncols,
+                            void *workspace, int64_t ws_bytes, void *stream);
+
 /* swap_chunk on device arrays; accepted[0] += accepted pairs, near_ties[0] +=
  * decisions with |u - p| <= 4 ulp(p) (device exp vs host libm guard band).
  * If row_to_slot is non-NULL it is rebuilt from slot_to_row afterwards. */

@@ -189,6 +189,30 @@ int ptmh_advance_block_ws(int8_t* spins, int64_t L, const int64_t* slot_to_row, 
     return launch_advance_2phase(a, workspace, ws_bytes, as_stream(stream));
 }
 
+int ptmh_bits_pack(const int8_t* spins, int64_t rows, int64_t L, uint32_t* bits, void* stream) {
+    PTMH_CHECK_ARG(rows >= 0 && L >= 1, "bits_pack shape");
+    return launch_bits_pack(spins, rows, L, bits, as_stream(stream));
+}
+
+int ptmh_bits_unpack(const uint32_t* bits, int64_t rows, int64_t L, int8_t* spins, void* stream) {
+    PTMH_CHECK_ARG(rows >= 0 && L >= 1, "bits_unpack shape");
+    return launch_bits_unpack(bits, rows, L, spins, as_stream(stream));
+}
+
+int ptmh_advance_block_bits(uint32_t* bits, int64_t L, const int64_t* slot_to_row, int64_t lo, int64_t hi,
+                            const double* tbl, const double* dcls, int int_energy, double* energies,
+                            int64_t* spin_sums, uint64_t* positions, int64_t* iters_done, uint64_t seed,
+                            int64_t start_iter, int64_t nsteps, double* obs_e, double* obs_m, int64_t ncols,
+                            void* workspace, int64_t ws_bytes, void* stream) {
+    PTMH_CHECK_ARG(L >= 2 && L * L < (1LL << 31), "advance_block: need 2 <= L, L*L < 2^31");
+    PTMH_CHECK_ARG(lo >= 0 && hi >= lo && nsteps >= 0 && start_iter >= 0, "advance_block range");
+    PTMH_CHECK_ARG(obs_e == nullptr || start_iter + nsteps <= ncols, "advance_block: obs columns");
+    AdvanceArgs a{nullptr, L, slot_to_row, lo, hi, tbl, dcls, int_energy, energies, spin_sums,
+                  positions, iters_done, seed, start_iter, nsteps, obs_e, obs_m, ncols,
+                  obs_e ? 1 : 0, nullptr, bits};
+    return launch_advance_2phase(a, workspace, ws_bytes, as_stream(stream));
+}
+
 int ptmh_swap_chunk(int64_t* slot_to_row, double* energies, int64_t* spin_sums, const double* betas,
                     int64_t R, uint64_t seed, int64_t stream_base, int64_t round_index, int64_t first,
                     int64_t pair_lo, int64_t pair_hi, int64_t* accepted, int64_t* near_ties,
@@ -362,11 +386,16 @@ int ptmh_host_advance_block(int8_t* spins, int64_t rows, int64_t L, const int64_
     if (record == 2) PTMH_TRY(ws_get(g_ws, 10, (size_t)R * ncols * nsite, &d_states));
     AdvanceArgs a{d_spins, L, d_s2r, lo, hi, d_tbl, d_dcls, int_energy, d_e, d_sums, d_pos, d_iters, seed,
                   start_iter, nsteps, d_oe, d_om, ncols, record, d_states};
-    if (record <= 1) {
+    if (record <= 1) {  // bit-packed lattices: L2-resident random-site commits
         const int64_t wsb = advance_ws_bytes(hi - lo, nsteps);
         void* d_ws = nullptr;
+        uint32_t* d_bits = nullptr;
         PTMH_TRY(ws_get(g_ws, 17, (size_t)wsb, reinterpret_cast<int8_t**>(&d_ws)));
+        PTMH_TRY(ws_get(g_ws, 18, (size_t)rows * (size_t)((nsite + 31) / 32), &d_bits));
+        PTMH_TRY(launch_bits_pack(d_spins, rows, L, d_bits, s));
+        a.bits = d_bits;
         PTMH_TRY(launch_advance_2phase(a, d_ws, wsb, s));
+        PTMH_TRY(launch_bits_unpack(d_bits, rows, L, d_spins, s));
     } else {
         PTMH_TRY(launch_advance(a, s));
     }

@@ -303,6 +303,7 @@ struct CommitArgs {
     int last;
 };
 
+template <bool kBits>
 __global__ void __launch_bounds__(128) commit_kernel(CommitArgs C) {
     const AdvanceArgs& A = C.A;
     const int lane = threadIdx.x & 31;
@@ -310,7 +311,14 @@ __global__ void __launch_bounds__(128) commit_kernel(CommitArgs C) {
     const int64_t slot = A.lo + s;
     if (slot >= A.hi) return;
     const int64_t L = A.L, n_sites = L * L;
-    int8_t* lat = A.spins + A.slot_to_row[slot] * n_sites;
+    const int64_t nwords = (n_sites + 31) >> 5;
+    int8_t* lat = kBits ? nullptr : A.spins + A.slot_to_row[slot] * n_sites;
+    uint32_t* latw = kBits ? A.bits + A.slot_to_row[slot] * nwords : nullptr;
+    // spin (+1/-1) at site x; flip of site x
+    auto spin = [&](int64_t x) -> int {
+        if (kBits) return 2 * (int)((latw[x >> 5] >> (x & 31)) & 1u) - 1;
+        return lat[x];
+    };
     double e = A.energies[slot];
     long long ssum = A.spin_sums[slot];
     const double nsd = (double)n_sites;
@@ -324,10 +332,13 @@ __global__ void __launch_bounds__(128) commit_kernel(CommitArgs C) {
     // on the state; a prefetch never changes what a later load returns)
     auto prefetch_site = [&](int64_t st) {
         const int64_t r = st / L, c = st - r * L;
-        const int8_t* b = lat + r * L;
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(b + c));
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(lat + ((r + 1) % L) * L + c));
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(lat + ((r - 1 + L) % L) * L + c));
+        const int64_t xs[3] = {st, ((r + 1) % L) * L + c, ((r - 1 + L) % L) * L + c};
+        for (int q = 0; q < 3; ++q) {
+            if (kBits)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(latw + (xs[q] >> 5)));
+            else
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(lat + xs[q]));
+        }
     };
     int64_t n_site = 0;
     uint32_t n_acc = 0u, n_conf = 0u;
@@ -360,12 +371,15 @@ __global__ void __launch_bounds__(128) commit_kernel(CommitArgs C) {
         while (pending) {
             const bool ready = ((pending >> lane) & 1u) && ((conf & pending) == 0u);
             if (ready) {
-                const int sp = lat[site];
-                const int nb = lat[up] + lat[dn] + lat[rt] + lat[lf];
+                const int sp = spin(site);
+                const int nb = spin(up) + spin(dn) + spin(rt) + spin(lf);
                 const int cls = (sp > 0 ? 5 : 0) + (nb + 4) / 2;
                 const double d = A.dcls[cls];
                 if ((d <= 0.0) || ((accm >> cls) & 1u)) {
-                    lat[site] = (int8_t)(-sp);
+                    if (kBits)  // lanes of one level may flip different bits of one word
+                        atomicXor(&latw[site >> 5], 1u << (site & 31));
+                    else
+                        lat[site] = (int8_t)(-sp);
                     my_d = d;
                     my_ds = -2 * sp;
                     my_acc = true;
@@ -464,9 +478,53 @@ int launch_advance_2phase(const AdvanceArgs& a, void* ws, int64_t ws_bytes, cuda
         draw_kernel<<<ceil_div(nslots * npad, 256), 256, 0, s>>>(D);
         PTMH_LAUNCH_CHECK();
         CommitArgs C{a, a0, n, stride, rs, ra, rc, a0 + n >= a.nsteps};
-        commit_kernel<<<ceil_div(nslots, 4), 128, 0, s>>>(C);
+        if (a.bits)
+            commit_kernel<true><<<ceil_div(nslots, 4), 128, 0, s>>>(C);
+        else
+            commit_kernel<false><<<ceil_div(nslots, 4), 128, 0, s>>>(C);
         PTMH_LAUNCH_CHECK();
     }
+    return PTMH_OK;
+}
+
+// ----------------------------------------------- bit-packed exact lattices --
+// Row-major bits (site x -> bit x & 31 of word x >> 5): 1 bit per spin keeps
+// the C3 lattices (256 x 1 MiB int8) L2-resident (32 MiB) for the commit.
+__global__ void bits_pack_kernel(const int8_t* __restrict__ spins, int64_t rows, int64_t n, int64_t nw,
+                                 uint32_t* __restrict__ bits) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= rows * nw) return;
+    const int64_t row = t / nw, w = t - row * nw;
+    const int8_t* s = spins + row * n;
+    uint32_t word = 0;
+    for (int b = 0; b < 32; ++b) {
+        const int64_t x = w * 32 + b;
+        if (x < n && s[x] > 0) word |= 1u << b;
+    }
+    bits[t] = word;
+}
+
+__global__ void bits_unpack_kernel(const uint32_t* __restrict__ bits, int64_t rows, int64_t n, int64_t nw,
+                                   int8_t* __restrict__ spins) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= rows * n) return;
+    const int64_t row = t / n, x = t - row * n;
+    spins[t] = ((bits[row * nw + (x >> 5)] >> (x & 31)) & 1u) ? 1 : -1;
+}
+
+int launch_bits_pack(const int8_t* spins, int64_t rows, int64_t L, uint32_t* bits, cudaStream_t s) {
+    const int64_t n = L * L, nw = (n + 31) >> 5;
+    if (rows == 0) return PTMH_OK;
+    bits_pack_kernel<<<ceil_div(rows * nw, 256), 256, 0, s>>>(spins, rows, n, nw, bits);
+    PTMH_LAUNCH_CHECK();
+    return PTMH_OK;
+}
+
+int launch_bits_unpack(const uint32_t* bits, int64_t rows, int64_t L, int8_t* spins, cudaStream_t s) {
+    const int64_t n = L * L, nw = (n + 31) >> 5;
+    if (rows == 0) return PTMH_OK;
+    bits_unpack_kernel<<<ceil_div(rows * n, 256), 256, 0, s>>>(bits, rows, n, nw, spins);
+    PTMH_LAUNCH_CHECK();
     return PTMH_OK;
 }
 

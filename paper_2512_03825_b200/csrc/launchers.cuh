@@ -27,6 +27,7 @@ struct AdvanceArgs {
     int64_t ncols;
     int record;
     int8_t* states;
+    uint32_t* bits;  // bit-packed lattices (row-major bits, ceil(L*L/32) words per row) or null
 };
 
 // exact.cu (n = sites per lattice row)
@@ -36,6 +37,8 @@ int launch_row_stats(const int8_t* spins, int64_t rows, int64_t L, int64_t* stat
 int launch_advance(const AdvanceArgs& a, cudaStream_t s);
 int launch_advance_2phase(const AdvanceArgs& a, void* ws, int64_t ws_bytes, cudaStream_t s);
 int64_t advance_ws_bytes(int64_t nslots, int64_t nsteps);
+int launch_bits_pack(const int8_t* spins, int64_t rows, int64_t L, uint32_t* bits, cudaStream_t s);
+int launch_bits_unpack(const uint32_t* bits, int64_t rows, int64_t L, int8_t* spins, cudaStream_t s);
 int launch_swap(int64_t* slot_to_row, double* energies, int64_t* spin_sums, const double* betas,
                 int64_t R, uint64_t seed, int64_t stream_base, int64_t round_index, int64_t first,
                 int64_t pair_lo, int64_t pair_hi, int64_t* accepted, int64_t* near_ties,

@@ -81,7 +81,10 @@ class ExactEngine(_Base):
         if self.rows != self.R:
             raise ValueError("the exact chain runs unsharded (one device)")
         d, R, L = self.dev, self.R, self.L
+        # canonical state: 1 bit per spin (L2-resident commits); int8 only at
+        # the boundaries (init, full_states recording, final_spins)
         self.spins = torch.empty((R, L, L), dtype=torch.int8, device=d)
+        self.bits = torch.zeros((R, (L * L + 31) // 32), dtype=torch.int32, device=d)
         self.positions = torch.zeros(R, dtype=torch.int64, device=d)
         self.energies = torch.zeros(R, dtype=torch.float64, device=d)
         self.spin_sums = torch.zeros(R, dtype=torch.int64, device=d)
@@ -105,6 +108,7 @@ class ExactEngine(_Base):
         self.spin_sums.copy_(torch.from_numpy(st[:, 0].copy()))
         self.positions.fill_(L * L - 1)  # fill_lattice consumes L^2-1 draws
         self.int_energy = int(integer_energy_ok(self.J, self.B, e))
+        _lib.call("ptmh_bits_pack", _P(self.spins), R, L, _P(self.bits), s)
 
     def advance(self, start_iter: int, nsteps: int, obs_e=None, obs_m=None, record: int = 0,
                 states=None, lo: int = 0, hi: int | None = None) -> None:
@@ -116,17 +120,20 @@ class ExactEngine(_Base):
             need = int(_lib.LIB.ptmh_advance_workspace_bytes(hi - lo, nsteps))
             if getattr(self, "_ws", None) is None or self._ws.numel() < need:
                 self._ws = torch.empty(need, dtype=torch.uint8, device=self.dev)
-            _lib.call("ptmh_advance_block_ws", _P(self.spins), self.L, _P(self.slot_to_row), lo,
+            _lib.call("ptmh_advance_block_bits", _P(self.bits), self.L, _P(self.slot_to_row), lo,
                       hi, _P(self.tbl), _P(self.dcls), self.int_energy, _P(self.energies),
                       _P(self.spin_sums), _P(self.positions), _P(self.iters_done), self.seed,
                       start_iter, nsteps, _P(obs_e) if record else None,
                       _P(obs_m) if record else None, ncols, _P(self._ws), self._ws.numel(),
                       self._s())
             return
+        # full_states: the per-attempt snapshot kernel works on int8 lattices
+        _lib.call("ptmh_bits_unpack", _P(self.bits), self.R, self.L, _P(self.spins), self._s())
         _lib.call("ptmh_advance_block", _P(self.spins), self.L, _P(self.slot_to_row), lo, hi,
                   _P(self.tbl), _P(self.dcls), self.int_energy, _P(self.energies),
                   _P(self.spin_sums), _P(self.positions), _P(self.iters_done), self.seed,
                   start_iter, nsteps, _P(obs_e), _P(obs_m), ncols, record, _P(states), self._s())
+        _lib.call("ptmh_bits_pack", _P(self.spins), self.R, self.L, _P(self.bits), self._s())
 
     def exchange(self, round_index: int) -> int:
         """One swap round (executor.py:250-262, kernels.py:116-148); returns
@@ -141,6 +148,7 @@ class ExactEngine(_Base):
         return n_pairs
 
     def final_spins(self) -> np.ndarray:
+        _lib.call("ptmh_bits_unpack", _P(self.bits), self.R, self.L, _P(self.spins), self._s())
         return self.spins.cpu().numpy()
 
 
