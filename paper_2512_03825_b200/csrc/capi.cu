@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -85,18 +86,25 @@ struct Workspace {
     bool events = false;
 };
 
-static Workspace g_ws;
+// one workspace per device (buffers, streams and events are device-bound),
+// each behind its own mutex; created on first use, kept for the process
+static std::mutex g_ws_registry_mu;
+static std::vector<std::unique_ptr<Workspace>> g_ws_registry;
 
-static int ws_prepare(Workspace& w) {
+static int device_workspace(Workspace** out) {
     int dev = 0;
     PTMH_CUDA(cudaGetDevice(&dev));
-    if (w.device != dev) {
-        w.bufs.clear();  // a device switch leaks the old buffers on purpose
-        for (auto& st : w.s) st = nullptr;
-        for (auto& st : w.cs) st = nullptr;
-        w.events = false;
-        w.device = dev;
+    std::lock_guard<std::mutex> lk(g_ws_registry_mu);
+    if ((int)g_ws_registry.size() <= dev) g_ws_registry.resize(dev + 1);
+    if (!g_ws_registry[dev]) {
+        g_ws_registry[dev].reset(new Workspace());
+        g_ws_registry[dev]->device = dev;
     }
+    *out = g_ws_registry[dev].get();
+    return PTMH_OK;
+}
+
+static int ws_prepare(Workspace& w) {
     for (auto& st : w.s)
         if (!st) PTMH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     for (auto& st : w.cs)
@@ -311,6 +319,9 @@ int ptmh_cb_observe(const int64_t* stats_all, const int64_t* slot_to_row, int64_
 int ptmh_host_fill_lattice(int8_t* out, int64_t n, int64_t up_count, uint64_t seed, uint64_t stream,
                            uint64_t position, uint64_t* new_position) {
     PTMH_CHECK_ARG(n >= 1 && up_count >= 0, "fill_lattice shape");
+    Workspace* wsp = nullptr;
+    PTMH_TRY(device_workspace(&wsp));
+    Workspace& g_ws = *wsp;
     std::lock_guard<std::mutex> lk(g_ws.mu);
     PTMH_TRY(ws_prepare(g_ws));
     cudaStream_t s = g_ws.s[1];
@@ -325,6 +336,9 @@ int ptmh_host_fill_lattice(int8_t* out, int64_t n, int64_t up_count, uint64_t se
 
 int ptmh_host_lattice_energy(const int8_t* spins, int64_t L, double J, double B, double* energy) {
     PTMH_CHECK_ARG(L >= 1 && energy, "lattice_energy shape");
+    Workspace* wsp = nullptr;
+    PTMH_TRY(device_workspace(&wsp));
+    Workspace& g_ws = *wsp;
     std::lock_guard<std::mutex> lk(g_ws.mu);
     PTMH_TRY(ws_prepare(g_ws));
     cudaStream_t s = g_ws.s[1];
@@ -357,6 +371,9 @@ int ptmh_host_advance_block(int8_t* spins, int64_t rows, int64_t L, const int64_
     exact_tables(betas, R, J, B, tbl, dcls);
     int int_energy = integral(J) && integral(B) && std::fabs(J) <= 1e6 && std::fabs(B) <= 1e6;
     for (int64_t k = lo; k < hi && int_energy; ++k) int_energy = integral(energies[k]);
+    Workspace* wsp = nullptr;
+    PTMH_TRY(device_workspace(&wsp));
+    Workspace& g_ws = *wsp;
     std::lock_guard<std::mutex> lk(g_ws.mu);
     PTMH_TRY(ws_prepare(g_ws));
     cudaStream_t s = g_ws.s[1];
@@ -429,6 +446,9 @@ int ptmh_host_swap_chunk(int64_t* slot_to_row, double* energies, int64_t* spin_s
                    "swap_chunk pairs");
     if (accepted) *accepted = 0;
     if (pair_hi == pair_lo) return PTMH_OK;
+    Workspace* wsp = nullptr;
+    PTMH_TRY(device_workspace(&wsp));
+    Workspace& g_ws = *wsp;
     std::lock_guard<std::mutex> lk(g_ws.mu);
     PTMH_TRY(ws_prepare(g_ws));
     cudaStream_t s = g_ws.s[1];
@@ -467,6 +487,9 @@ int ptmh_host_cb_interval(int8_t* spins, int64_t R, int64_t L, int64_t* slot_to_
         PTMH_CHECK_ARG(slot_to_row[k] >= 0 && slot_to_row[k] < R, "slot_to_row out of range");
         r2s[(size_t)slot_to_row[k]] = (int32_t)k;
     }
+    Workspace* wsp = nullptr;
+    PTMH_TRY(device_workspace(&wsp));
+    Workspace& g_ws = *wsp;
     std::lock_guard<std::mutex> lk(g_ws.mu);
     PTMH_TRY(ws_prepare(g_ws));
     cudaStream_t sin = g_ws.s[0], sc = g_ws.s[1], sout = g_ws.s[2];
