@@ -188,7 +188,7 @@ int ptmh_advance_block_ws(int8_t* spins, int64_t L, const int64_t* slot_to_row, 
                           int64_t* spin_sums, uint64_t* positions, int64_t* iters_done, uint64_t seed,
                           int64_t start_iter, int64_t nsteps, double* obs_e, double* obs_m, int64_t ncols,
                           void* workspace, int64_t ws_bytes, void* stream) {
-    PTMH_CHECK_ARG(L >= 2 && L * L < (1LL << 31), "advance_block: need 2 <= L, L*L < 2^31");
+    PTMH_CHECK_ARG(L >= 2 && L <= 4096, "two-phase advance: need 2 <= L <= 4096 (float site rows)");
     PTMH_CHECK_ARG(lo >= 0 && hi >= lo && nsteps >= 0 && start_iter >= 0, "advance_block range");
     PTMH_CHECK_ARG(obs_e == nullptr || start_iter + nsteps <= ncols, "advance_block: obs columns");
     AdvanceArgs a{spins, L, slot_to_row, lo, hi, tbl, dcls, int_energy, energies, spin_sums,
@@ -212,7 +212,7 @@ int ptmh_advance_block_bits(uint32_t* bits, int64_t L, const int64_t* slot_to_ro
                             int64_t* spin_sums, uint64_t* positions, int64_t* iters_done, uint64_t seed,
                             int64_t start_iter, int64_t nsteps, double* obs_e, double* obs_m, int64_t ncols,
                             void* workspace, int64_t ws_bytes, void* stream) {
-    PTMH_CHECK_ARG(L >= 2 && L * L < (1LL << 31), "advance_block: need 2 <= L, L*L < 2^31");
+    PTMH_CHECK_ARG(L >= 2 && L <= 4096, "two-phase advance: need 2 <= L <= 4096 (float site rows)");
     PTMH_CHECK_ARG(lo >= 0 && hi >= lo && nsteps >= 0 && start_iter >= 0, "advance_block range");
     PTMH_CHECK_ARG(obs_e == nullptr || start_iter + nsteps <= ncols, "advance_block: obs columns");
     AdvanceArgs a{nullptr, L, slot_to_row, lo, hi, tbl, dcls, int_energy, energies, spin_sums,
@@ -403,7 +403,7 @@ int ptmh_host_advance_block(int8_t* spins, int64_t rows, int64_t L, const int64_
     if (record == 2) PTMH_TRY(ws_get(g_ws, 10, (size_t)R * ncols * nsite, &d_states));
     AdvanceArgs a{d_spins, L, d_s2r, lo, hi, d_tbl, d_dcls, int_energy, d_e, d_sums, d_pos, d_iters, seed,
                   start_iter, nsteps, d_oe, d_om, ncols, record, d_states};
-    if (record <= 1) {  // bit-packed lattices: L2-resident random-site commits
+    if (record <= 1 && L <= 4096) {  // bit-packed lattices: L2-resident random-site commits
         const int64_t wsb = advance_ws_bytes(hi - lo, nsteps);
         void* d_ws = nullptr;
         uint32_t* d_bits = nullptr;

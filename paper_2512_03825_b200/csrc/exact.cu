@@ -225,9 +225,23 @@ __global__ void advance_kernel(AdvanceArgs A) {
 // depend on the lattice state is computed here, fully parallel over slots and
 // attempts: the two Philox4x64-10 words (kernels.py:84-87), the site
 // (kernels.py:88-90), one acceptance bit per uphill class
-// (u_acc < exp(-beta*dE_c), kernels.py:95-98) and the mask of earlier
-// attempts of the same 32-attempt window whose site is the site or one of its
-// neighbours (the dependencies phase 2 must respect).
+// (u_acc < exp(-beta*dE_c), kernels.py:95-98), the mask of earlier attempts of
+// the same 32-attempt window whose site is the site or one of its neighbours,
+// and per 128-attempt super-window a flag "no two of its sites are within
+// Chebyshev distance 1" (then its attempts commute and phase 2 applies them
+// in one parallel pass).
+// row of site x (0 <= x < L*L <= 2^24 for the two-phase kernels): float
+// reciprocal estimate, then an exact +-1 correction
+__device__ __forceinline__ int site_row(int x, int L, float invL) {
+    int r = (int)__fmul_rn((float)x, invL);
+    r -= (r * L > x);
+    r += ((r + 1) * L <= x);
+    return r;
+}
+
+constexpr int kSW = 128;       // attempts per super-window (4 windows)
+constexpr int kHashSlots = 512;
+
 struct DrawArgs {
     int64_t lo, nslots, L;
     const double* tbl;
@@ -238,68 +252,99 @@ struct DrawArgs {
     int32_t* rec_site;
     uint32_t* rec_acc;
     uint32_t* rec_conf;
+    uint32_t* rec_indep;        // (nslots, stride / kSW)
 };
 
 __global__ void __launch_bounds__(256) draw_kernel(DrawArgs D) {
-    const int64_t npad = (D.n + 31) & ~int64_t(31);
+    __shared__ uint32_t h_tab[2][4][kHashSlots];
+    __shared__ int h_dep[2];
+    const int64_t npad = (D.n + kSW - 1) / kSW * kSW;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t s = tid / npad;
-    if (s >= D.nslots) return;  // whole warps (npad % 32 == 0)
-    const int64_t a = tid - s * npad;
-    const int lane = threadIdx.x & 31;
-    const int64_t slot = D.lo + s;
+    const bool in_slot = s < D.nslots;  // no early return: block barriers below
+    const int64_t a = in_slot ? tid - s * npad : 0;
+    const int lane = threadIdx.x & 31, half = threadIdx.x / kSW;
+    for (int k = threadIdx.x; k < 2 * 4 * kHashSlots; k += blockDim.x) (&h_tab[0][0][0])[k] = 0xffffffffu;
+    if (threadIdx.x < 2) h_dep[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t slot = D.lo + (in_slot ? s : 0);
     const int64_t L = D.L;
     const uint64_t p = D.positions[slot] + 2 * (uint64_t)(D.a0 + a);
     const double u_site = stream_uniform(D.seed, (uint64_t)slot, p);
     const double u_acc = stream_uniform(D.seed, (uint64_t)slot, p + 1);
-    const int64_t site = (int64_t)__dmul_rn(u_site, (double)(L * L));
-    const int64_t r = site / L, c = site - r * L;
+    const int Li = (int)L;
+    const int site = (int)__dmul_rn(u_site, (double)(L * L));
+    const int r = site_row(site, Li, 1.0f / (float)Li), c = site - r * Li;
     uint32_t accm = 0;
     const double* tb = D.tbl + slot * 10;
 #pragma unroll
     for (int q = 0; q < 10; ++q)
         if (D.dcls[q] > 0.0 && u_acc < tb[q]) accm |= 1u << q;
-    // conflicts with earlier attempts of the window: a shifted-2x2-bucket
-    // filter (two sites at Chebyshev distance <= 1 share one of 4 buckets),
-    // exact neighbour test only where the filter fires
+    // window dependencies: shifted-2x2-bucket filter (two sites at Chebyshev
+    // distance <= 1 share one of 4 buckets), exact neighbour test where it fires
     const unsigned lt_mask = (1u << lane) - 1u;
-    bool full = (L & 1) || L <= 8;
+    const bool full = (L & 1) || L <= 8;
+    const int rp = (r + 1 == Li) ? 0 : r + 1, cp = (c + 1 == Li) ? 0 : c + 1;
+    const int r1 = r >> 1, c1 = c >> 1, r2 = rp >> 1, c2 = cp >> 1;
+    const uint32_t keys[4] = {(uint32_t)((r1 << 16) | c1), (uint32_t)((r2 << 16) | c1),
+                              (uint32_t)((r1 << 16) | c2), (uint32_t)((r2 << 16) | c2)};
     unsigned cand = 0xffffffffu;
-    if (!full) {
-        const int r1 = (int)(r >> 1), c1 = (int)(c >> 1);
-        const int r2 = (int)(((r + 1) % L) >> 1), c2 = (int)(((c + 1) % L) >> 1);
-        cand = __match_any_sync(0xffffffffu, (r1 << 16) | c1) | __match_any_sync(0xffffffffu, (r2 << 16) | c1) |
-               __match_any_sync(0xffffffffu, (r1 << 16) | c2) | __match_any_sync(0xffffffffu, (r2 << 16) | c2);
-    }
+    if (!full)
+        cand = __match_any_sync(0xffffffffu, keys[0]) | __match_any_sync(0xffffffffu, keys[1]) |
+               __match_any_sync(0xffffffffu, keys[2]) | __match_any_sync(0xffffffffu, keys[3]);
     cand &= lt_mask;
     unsigned conf = 0;
     if (__any_sync(0xffffffffu, cand != 0)) {
-        const int64_t up = ((r + 1) % L) * L + c, dn = ((r - 1 + L) % L) * L + c;
-        const int64_t rt = r * L + (c + 1) % L, lf = r * L + (c - 1 + L) % L;
+        const int up = rp * Li + c, dn = (r == 0 ? Li - 1 : r - 1) * Li + c;
+        const int rt = r * Li + cp, lf = r * Li + (c == 0 ? Li - 1 : c - 1);
 #pragma unroll 4
         for (int k = 0; k < 32; ++k) {
-            const int64_t s2 = __shfl_sync(0xffffffffu, site, k);
+            const int s2 = __shfl_sync(0xffffffffu, site, k);
             const bool hit = (s2 == site) | (s2 == up) | (s2 == dn) | (s2 == rt) | (s2 == lf);
             conf |= (hit && ((cand >> k) & 1u)) ? (1u << k) : 0u;
         }
     }
-    if (a < D.n) {
+    // super-window independence: insert the 4 bucket keys, any repeat => dependent
+    const bool valid = in_slot && a < D.n;
+    if (full) {
+        if (threadIdx.x % kSW == 0) h_dep[half] = 1;
+    } else if (valid) {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+            uint32_t h = (keys[g] * 0x9E3779B1u) >> (32 - 9);
+            while (true) {
+                const uint32_t old = atomicCAS(&h_tab[half][g][h], 0xffffffffu, keys[g]);
+                if (old == 0xffffffffu) break;
+                if (old == keys[g]) {
+                    h_dep[half] = 1;
+                    break;
+                }
+                h = (h + 1) & (kHashSlots - 1);
+            }
+        }
+    }
+    if (valid) {
         const int64_t o = s * D.stride + a;
-        D.rec_site[o] = (int32_t)site;
+        D.rec_site[o] = site;
         D.rec_acc[o] = accm;
         D.rec_conf[o] = conf;
     }
+    __syncthreads();
+    if (in_slot && threadIdx.x % kSW == 0 && a < D.n)
+        D.rec_indep[s * (D.stride / kSW) + a / kSW] = h_dep[half] ? 0u : 1u;
 }
 
-// Phase 2: warp per slot, windows of 32 attempts committed in dependency
-// levels from the phase-1 records; energies summed in attempt order exactly
-// as advance_kernel does.
+// Phase 2: warp per slot.  An independent super-window (and integer J, B and
+// no recording, so the energy sum is order-free) is applied in one pass, four
+// attempts per lane; otherwise its windows of 32 are committed in dependency
+// levels with the energies summed in attempt order exactly as advance_kernel.
 struct CommitArgs {
     AdvanceArgs A;
     int64_t a0, n, stride;
     const int32_t* rec_site;
     const uint32_t* rec_acc;
     const uint32_t* rec_conf;
+    const uint32_t* rec_indep;
     int last;
 };
 
@@ -314,123 +359,141 @@ __global__ void __launch_bounds__(128) commit_kernel(CommitArgs C) {
     const int64_t nwords = (n_sites + 31) >> 5;
     int8_t* lat = kBits ? nullptr : A.spins + A.slot_to_row[slot] * n_sites;
     uint32_t* latw = kBits ? A.bits + A.slot_to_row[slot] * nwords : nullptr;
-    // spin (+1/-1) at site x; flip of site x
-    auto spin = [&](int64_t x) -> int {
+    auto spin = [&](int64_t x) -> int {  // +1 / -1
         if (kBits) return 2 * (int)((latw[x >> 5] >> (x & 31)) & 1u) - 1;
         return lat[x];
+    };
+    auto flip = [&](int64_t x, int sp) {
+        if (kBits)  // lanes may flip different bits of one word at once
+            atomicXor(&latw[x >> 5], 1u << (x & 31));
+        else
+            lat[x] = (int8_t)(-sp);
+    };
+    const int Li = (int)L;
+    const float invL = 1.0f / (float)Li;
+    auto neighbours = [&](int64_t x, int64_t& up, int64_t& dn, int64_t& rt, int64_t& lf) {
+        const int xi = (int)x, r = site_row(xi, Li, invL), c = xi - r * Li;
+        up = (r + 1 == Li ? 0 : r + 1) * Li + c;
+        dn = (r == 0 ? Li - 1 : r - 1) * Li + c;
+        rt = r * Li + (c + 1 == Li ? 0 : c + 1);
+        lf = r * Li + (c == 0 ? Li - 1 : c - 1);
     };
     double e = A.energies[slot];
     long long ssum = A.spin_sums[slot];
     const double nsd = (double)n_sites;
-    double acc_d = -0.0;  // int_energy && record == 0: per-lane partial sums (-0.0: identity)
+    const bool unordered = A.int_energy && A.record == 0;  // order-free sums
+    double acc_d = -0.0;  // per-lane partial sums (-0.0: the IEEE identity)
     long long acc_ds = 0;
     const int32_t* rs = C.rec_site + s * C.stride;
     const uint32_t* ra = C.rec_acc + s * C.stride;
     const uint32_t* rc = C.rec_conf + s * C.stride;
-    // software pipeline: window w+1's records are loaded, and its lattice
-    // lines prefetched into L1, while window w commits (records never depend
-    // on the state; a prefetch never changes what a later load returns)
-    auto prefetch_site = [&](int64_t st) {
-        const int64_t r = st / L, c = st - r * L;
-        const int64_t xs[3] = {st, ((r + 1) % L) * L + c, ((r - 1 + L) % L) * L + c};
-        for (int q = 0; q < 3; ++q) {
-            if (kBits)
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(latw + (xs[q] >> 5)));
-            else
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(lat + xs[q]));
-        }
-    };
-    int64_t n_site = 0;
-    uint32_t n_acc = 0u, n_conf = 0u;
-    if (lane < C.n) {
-        n_site = rs[lane];
-        n_acc = ra[lane];
-        n_conf = rc[lane];
-        prefetch_site(n_site);
-    }
-    for (int64_t w0 = 0; w0 < C.n; w0 += 32) {
-        const int64_t a = w0 + lane;
-        const bool valid = a < C.n;
-        const int nvalid = (int)min((int64_t)32, C.n - w0);
-        const int64_t site = valid ? n_site : 0;
-        const uint32_t accm = valid ? n_acc : 0u;
-        const unsigned conf = valid ? n_conf : 0u;
-        if (a + 32 < C.n) {
-            n_site = rs[a + 32];
-            n_acc = ra[a + 32];
-            n_conf = rc[a + 32];
-            prefetch_site(n_site);
-        }
-        const int64_t r = site / L, c = site - r * L;
-        const int64_t up = ((r + 1) % L) * L + c, dn = ((r - 1 + L) % L) * L + c;
-        const int64_t rt = r * L + (c + 1) % L, lf = r * L + (c - 1 + L) % L;
-        unsigned pending = __ballot_sync(0xffffffffu, valid);
-        double my_d = -0.0;  // IEEE identity: keeps a reference -0.0 energy intact
-        int my_ds = 0;
-        bool my_acc = false;
-        while (pending) {
-            const bool ready = ((pending >> lane) & 1u) && ((conf & pending) == 0u);
-            if (ready) {
-                const int sp = spin(site);
-                const int nb = spin(up) + spin(dn) + spin(rt) + spin(lf);
-                const int cls = (sp > 0 ? 5 : 0) + (nb + 4) / 2;
+    const uint32_t* ri = C.rec_indep + s * (C.stride / kSW);
+    for (int64_t sw0 = 0; sw0 < C.n; sw0 += kSW) {
+        if (unordered && ri[sw0 / kSW]) {
+            // the super-window's attempts touch disjoint neighbourhoods: apply all
+            int64_t st[4];
+            uint32_t am[4];
+            bool on[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int64_t a = sw0 + q * 32 + lane;
+                on[q] = a < C.n;
+                st[q] = on[q] ? rs[a] : 0;
+                am[q] = on[q] ? ra[a] : 0u;
+            }
+            int sp[4], nb[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                int64_t up, dn, rt, lf;
+                neighbours(st[q], up, dn, rt, lf);
+                sp[q] = spin(st[q]);
+                nb[q] = spin(up) + spin(dn) + spin(rt) + spin(lf);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int cls = (sp[q] > 0 ? 5 : 0) + (nb[q] + 4) / 2;
                 const double d = A.dcls[cls];
-                if ((d <= 0.0) || ((accm >> cls) & 1u)) {
-                    if (kBits)  // lanes of one level may flip different bits of one word
-                        atomicXor(&latw[site >> 5], 1u << (site & 31));
-                    else
-                        lat[site] = (int8_t)(-sp);
-                    my_d = d;
-                    my_ds = -2 * sp;
-                    my_acc = true;
+                if (on[q] && ((d <= 0.0) || ((am[q] >> cls) & 1u))) {
+                    flip(st[q], sp[q]);
+                    acc_d = __dadd_rn(acc_d, d);
+                    acc_ds += -2 * sp[q];
                 }
             }
             __syncwarp();
-            pending &= ~__ballot_sync(0xffffffffu, ready);
-        }
-        if (A.int_energy && A.record == 0) {
-            // integer increments, nothing recorded: order-free per-lane sums,
-            // reduced once after the last window
-            acc_d = __dadd_rn(acc_d, my_d);
-            acc_ds += my_ds;
             continue;
         }
-        const unsigned accmask = __ballot_sync(0xffffffffu, my_acc && valid);
-        int ds_scan = my_ds;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_up_sync(0xffffffffu, ds_scan, o);
-            if (lane >= o) ds_scan += v;
-        }
-        const long long ssum_lane = ssum + ds_scan;
-        double e_lane;
-        if (A.int_energy) {
-            double d_scan = my_d;
+        for (int64_t w0 = sw0; w0 < min(C.n, sw0 + kSW); w0 += 32) {
+            const int64_t a = w0 + lane;
+            const bool valid = a < C.n;
+            const int nvalid = (int)min((int64_t)32, C.n - w0);
+            const int64_t site = valid ? rs[a] : 0;
+            const uint32_t accm = valid ? ra[a] : 0u;
+            const unsigned conf = valid ? rc[a] : 0u;
+            int64_t up, dn, rt, lf;
+            neighbours(site, up, dn, rt, lf);
+            unsigned pending = __ballot_sync(0xffffffffu, valid);
+            double my_d = -0.0;
+            int my_ds = 0;
+            bool my_acc = false;
+            while (pending) {
+                const bool ready = ((pending >> lane) & 1u) && ((conf & pending) == 0u);
+                if (ready) {
+                    const int sp = spin(site);
+                    const int nbs = spin(up) + spin(dn) + spin(rt) + spin(lf);
+                    const int cls = (sp > 0 ? 5 : 0) + (nbs + 4) / 2;
+                    const double d = A.dcls[cls];
+                    if ((d <= 0.0) || ((accm >> cls) & 1u)) {
+                        flip(site, sp);
+                        my_d = d;
+                        my_ds = -2 * sp;
+                        my_acc = true;
+                    }
+                }
+                __syncwarp();
+                pending &= ~__ballot_sync(0xffffffffu, ready);
+            }
+            if (unordered) {
+                acc_d = __dadd_rn(acc_d, my_d);
+                acc_ds += my_ds;
+                continue;
+            }
+            const unsigned accmask = __ballot_sync(0xffffffffu, my_acc && valid);
+            int ds_scan = my_ds;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const double v = __shfl_up_sync(0xffffffffu, d_scan, o);
-                if (lane >= o) d_scan = __dadd_rn(d_scan, v);
+                const int v = __shfl_up_sync(0xffffffffu, ds_scan, o);
+                if (lane >= o) ds_scan += v;
             }
-            const bool any_before = (accmask & ((2u << lane) - 1u)) != 0u;
-            e_lane = any_before ? __dadd_rn(e, d_scan) : e;
-        } else {
-            double run = e;
-            e_lane = e;
-            for (int k = 0; k < nvalid; ++k) {
-                const double dk = __shfl_sync(0xffffffffu, my_d, k);
-                if ((accmask >> k) & 1u) run = __dadd_rn(run, dk);
-                if (lane == k) e_lane = run;
+            const long long ssum_lane = ssum + ds_scan;
+            double e_lane;
+            if (A.int_energy) {
+                double d_scan = my_d;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const double v = __shfl_up_sync(0xffffffffu, d_scan, o);
+                    if (lane >= o) d_scan = __dadd_rn(d_scan, v);
+                }
+                const bool any_before = (accmask & ((2u << lane) - 1u)) != 0u;
+                e_lane = any_before ? __dadd_rn(e, d_scan) : e;
+            } else {
+                double run = e;
+                e_lane = e;
+                for (int k = 0; k < nvalid; ++k) {
+                    const double dk = __shfl_sync(0xffffffffu, my_d, k);
+                    if ((accmask >> k) & 1u) run = __dadd_rn(run, dk);
+                    if (lane == k) e_lane = run;
+                }
             }
+            if (A.record >= 1 && valid) {
+                const int64_t col = A.start_iter + C.a0 + a;
+                A.obs_e[slot * A.ncols + col] = e_lane;
+                A.obs_m[slot * A.ncols + col] = __ddiv_rn((double)ssum_lane, nsd);
+            }
+            e = __shfl_sync(0xffffffffu, e_lane, nvalid - 1);
+            ssum = __shfl_sync(0xffffffffu, ssum_lane, nvalid - 1);
         }
-        if (A.record >= 1 && valid) {
-            const int64_t col = A.start_iter + C.a0 + a;
-            A.obs_e[slot * A.ncols + col] = e_lane;
-            A.obs_m[slot * A.ncols + col] = __ddiv_rn((double)ssum_lane, nsd);
-        }
-        e = __shfl_sync(0xffffffffu, e_lane, nvalid - 1);
-        ssum = __shfl_sync(0xffffffffu, ssum_lane, nvalid - 1);
     }
-    if (A.int_energy && A.record == 0) {
+    if (unordered) {
         for (int o = 16; o > 0; o >>= 1) {
             acc_d = __dadd_rn(acc_d, __shfl_down_sync(0xffffffffu, acc_d, o));
             acc_ds += __shfl_down_sync(0xffffffffu, acc_ds, o);
@@ -449,35 +512,40 @@ __global__ void __launch_bounds__(128) commit_kernel(CommitArgs C) {
 }
 
 int64_t advance_chunk(int64_t nslots) {
-    // attempts per slot per phase-1/phase-2 pass: ~16M records (192 MiB)
+    // attempts per slot per phase-1/phase-2 pass: ~16M records (~200 MiB)
     int64_t c = (int64_t(1) << 24) / std::max<int64_t>(1, nslots);
     c = std::max<int64_t>(1024, std::min<int64_t>(c, 1 << 16));
-    return c & ~int64_t(31);
+    return c & ~int64_t(kSW - 1);
+}
+
+static int64_t advance_stride(int64_t nslots, int64_t nsteps) {
+    return std::min(advance_chunk(nslots), (nsteps + kSW - 1) / kSW * kSW);
 }
 
 int64_t advance_ws_bytes(int64_t nslots, int64_t nsteps) {
-    const int64_t stride = std::min(advance_chunk(nslots), (nsteps + 31) & ~int64_t(31));
-    return nslots * stride * 12;
+    const int64_t stride = advance_stride(nslots, nsteps);
+    return nslots * stride * 12 + nslots * (stride / kSW) * 4;
 }
 
 int launch_advance_2phase(const AdvanceArgs& a, void* ws, int64_t ws_bytes, cudaStream_t s) {
     const int64_t nslots = a.hi - a.lo;
     if (nslots <= 0 || a.nsteps <= 0) return PTMH_OK;
-    const int64_t stride = std::min(advance_chunk(nslots), (a.nsteps + 31) & ~int64_t(31));
-    if (ws_bytes < nslots * stride * 12) {
+    const int64_t stride = advance_stride(nslots, a.nsteps);
+    if (ws_bytes < advance_ws_bytes(nslots, a.nsteps)) {
         set_error("advance workspace too small");
         return PTMH_ERR_ARG;
     }
     int32_t* rs = static_cast<int32_t*>(ws);
     uint32_t* ra = reinterpret_cast<uint32_t*>(rs + nslots * stride);
     uint32_t* rc = ra + nslots * stride;
+    uint32_t* rind = rc + nslots * stride;
     for (int64_t a0 = 0; a0 < a.nsteps; a0 += stride) {
         const int64_t n = std::min(stride, a.nsteps - a0);
-        DrawArgs D{a.lo, nslots, a.L, a.tbl, a.dcls, a.seed, a.positions, a0, n, stride, rs, ra, rc};
-        const int64_t npad = (n + 31) & ~int64_t(31);
+        DrawArgs D{a.lo, nslots, a.L, a.tbl, a.dcls, a.seed, a.positions, a0, n, stride, rs, ra, rc, rind};
+        const int64_t npad = (n + kSW - 1) / kSW * kSW;
         draw_kernel<<<ceil_div(nslots * npad, 256), 256, 0, s>>>(D);
         PTMH_LAUNCH_CHECK();
-        CommitArgs C{a, a0, n, stride, rs, ra, rc, a0 + n >= a.nsteps};
+        CommitArgs C{a, a0, n, stride, rs, ra, rc, rind, a0 + n >= a.nsteps};
         if (a.bits)
             commit_kernel<true><<<ceil_div(nslots, 4), 128, 0, s>>>(C);
         else

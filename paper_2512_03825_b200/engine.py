@@ -115,7 +115,7 @@ class ExactEngine(_Base):
         """kernels.py:62-113 over slots [lo, hi)."""
         hi = self.R if hi is None else hi
         ncols = obs_e.shape[1] if obs_e is not None else 0
-        if record <= 1 and nsteps > 0 and hi > lo:
+        if record <= 1 and nsteps > 0 and hi > lo and self.L <= 4096:
             # two-phase: parallel draws + dependency masks, then a light commit
             need = int(_lib.LIB.ptmh_advance_workspace_bytes(hi - lo, nsteps))
             if getattr(self, "_ws", None) is None or self._ws.numel() < need:
