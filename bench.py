@@ -190,6 +190,7 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-exact", action="store_true", help="skip the exact-chain side measurement")
     ap.add_argument("--sharded", action="store_true",
                     help="use the multi-GPU coordinator (NCCL all_gather) even at one rank")
     args = ap.parse_args()
@@ -362,6 +363,31 @@ def main():
                "d2h_bytes_per_step": int(R * L * L + R * 8 * 3 + 16),
                "path": "kernels.cb_interval -> ptmh_host_cb_interval (pinned int8 lattices)"}
 
+    # the bit-exact reference chain (sweep_mode="exact") on the same shape
+    exact = None
+    if rank == 0 and not sharded and not args.no_exact and L <= 4096:
+        from paper_2512_03825_b200.engine import ExactEngine
+        del eng
+        torch.cuda.empty_cache()
+        ex = ExactEngine(L, R, temps, SEED, 1.0, 0.0, 0.5, local_rank)
+        ex.init_state()
+        n_att = max(32, int(2e8 // R))
+        done = 1
+        t0 = time.perf_counter()
+        while time.perf_counter() - t0 < 0.3:  # warm, clocks up
+            ex.advance(done, n_att)
+            done += n_att
+            torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        ex.advance(done, n_att)
+        b.record(stream)
+        torch.cuda.synchronize()
+        exact = {"value": R * n_att / (a.elapsed_time(b) / 1e3), "unit": "attempts/s",
+                 "chain": "reference random-site chain, bit-exact with isingpt (two-phase kernels)",
+                 "sample": f"{R} slots x {n_att} attempts, record none"}
+        del ex
+
     cpu = None
     if rank == 0 and not sharded and not args.no_cpu:
         threads = host_cores()
@@ -384,7 +410,7 @@ def main():
                              "alg_bytes_per_launch": bytes_per_launch, "peak_kind": peak_kind,
                              "note": "issue-bound (Philox + bit-sliced logic), see DESIGN.md 5",
                              "issue_from_ncu": _issue(args.config) if not resident else None},
-                "cpu_baseline": cpu, "e2e": e2e,
+                "cpu_baseline": cpu, "e2e": e2e, "exact_chain": exact,
                 "gpu_launches": args.steps * (1 if resident else 2 * every + 2),
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)

@@ -1,9 +1,9 @@
-"""Time the checkerboard sweep kernels alone (CUDA events), per config.
-
-    python tools/time_sweep.py c3 c5 ...
-"""
+"""Time the checkerboard sweep kernels alone (CUDA events): ~0.3 s warm-up,
+median of 5 repetitions.    python tools/time_sweep.py c3 c5 ..."""
 import os
+import statistics
 import sys
+import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
@@ -18,15 +18,23 @@ for name in (sys.argv[1:] or ["c3"]):
     eng = CheckerboardEngine(L, R, build_ladder(R), 42, 1.0, 0.0, 0.5, 0)
     eng.init_state()
     n = max(2, min(200, int(4e9 // (R * L * L))))
-    eng.sweeps(0, 2)
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    eng.sweeps(2, n)
-    b.record()
-    torch.cuda.synchronize()
-    ms = a.elapsed_time(b)
-    print(f"{name}: L={L} R={R} {n} sweeps {ms:.3f} ms -> {n * R * L * L / ms / 1e9:.4g} G attempts/s "
-          f"({ms / n * 1e3:.1f} us/sweep)", flush=True)
+    t = 0
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < 0.3:
+        eng.sweeps(t, n)
+        t += n
+        torch.cuda.synchronize()
+    ms_all = []
+    for _ in range(5):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        eng.sweeps(t, n)
+        b.record()
+        torch.cuda.synchronize()
+        t += n
+        ms_all.append(a.elapsed_time(b))
+    ms = statistics.median(ms_all)
+    print(f"{name}: L={L} R={R} {n} sweeps {ms:.3f} ms -> {n * R * L * L / ms / 1e9:.4g} T attempts/s "
+          f"({ms / n * 1e3:.1f} us/sweep; min {min(ms_all):.3f} max {max(ms_all):.3f} ms)", flush=True)
     del eng
     torch.cuda.empty_cache()
