@@ -98,6 +98,16 @@ int ptmh_fill_lattices(int8_t *spins, int64_t rows, int64_t L,
                        int64_t up_count, uint64_t seed, uint64_t stream0,
                        uint64_t pos0, void *stream);
 
+/* The same lattices as ptmh_fill_lattices, bit for bit, computed in parallel
+ * (csrc/init.cu: every draw at once, the swaps resolved through per-position
+ * writer lists).  workspace: ptmh_fill_workspace_bytes(L, k) bytes processes
+ * k rows per pass. */
+int64_t ptmh_fill_workspace_bytes(int64_t L, int64_t rows_per_batch);
+int ptmh_fill_lattices_parallel(int8_t *spins, int64_t rows, int64_t L,
+                                int64_t up_count, uint64_t seed, uint64_t stream0,
+                                uint64_t pos0, void *workspace, int64_t ws_bytes,
+                                void *stream);
+
 /* stats[2r] = sum(s), stats[2r+1] = sum(s*(down+right)) of each int8 lattice
  * (the integer accumulators of kernels.py:48-59). */
 int ptmh_row_stats(const int8_t *spins, int64_t rows, int64_t L,

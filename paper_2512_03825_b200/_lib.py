@@ -42,6 +42,8 @@ def _load():
         # device-resident ABI
         "ptmh_fill_lattices": ([P, i64, i64, i64, u64, u64, u64, P], i32),
         "ptmh_row_stats": ([P, i64, i64, P, P], i32),
+        "ptmh_fill_workspace_bytes": ([i64, i64], i64),
+        "ptmh_fill_lattices_parallel": ([P, i64, i64, i64, u64, u64, u64, P, i64, P], i32),
         "ptmh_advance_block": ([P, i64, P, i64, i64, P, P, i32, P, P, P, P, u64, i64, i64,
                                 P, P, i64, i32, P, P], i32),
         "ptmh_advance_workspace_bytes": ([i64, i64], i64),

@@ -160,6 +160,18 @@ int ptmh_fill_lattices(int8_t* spins, int64_t rows, int64_t L, int64_t up_count,
     return launch_fill(spins, rows, L * L, up_count, seed, stream0, pos0, as_stream(stream));
 }
 
+int64_t ptmh_fill_workspace_bytes(int64_t L, int64_t rows_per_batch) {
+    return fill_ws_bytes(L * L, rows_per_batch);
+}
+
+int ptmh_fill_lattices_parallel(int8_t* spins, int64_t rows, int64_t L, int64_t up_count, uint64_t seed,
+                                uint64_t stream0, uint64_t pos0, void* workspace, int64_t ws_bytes,
+                                void* stream) {
+    PTMH_CHECK_ARG(rows >= 0 && L >= 1 && up_count >= 0 && up_count <= L * L, "fill_lattices shape");
+    return launch_fill_parallel(spins, rows, L * L, up_count, seed, stream0, pos0, workspace, ws_bytes,
+                                as_stream(stream));
+}
+
 int ptmh_row_stats(const int8_t* spins, int64_t rows, int64_t L, int64_t* stats, void* stream) {
     PTMH_CHECK_ARG(rows >= 0 && L >= 1, "row_stats shape");
     return launch_row_stats(spins, rows, L, stats, as_stream(stream));

@@ -34,6 +34,10 @@ struct AdvanceArgs {
 int launch_fill(int8_t* spins, int64_t rows, int64_t n, int64_t up_count, uint64_t seed,
                 uint64_t stream0, uint64_t pos0, cudaStream_t s);
 int launch_row_stats(const int8_t* spins, int64_t rows, int64_t L, int64_t* stats, cudaStream_t s);
+// init.cu (n = sites per lattice row)
+int64_t fill_ws_bytes(int64_t n, int64_t rows_per_batch);
+int launch_fill_parallel(int8_t* spins, int64_t rows, int64_t n, int64_t up_count, uint64_t seed,
+                         uint64_t stream0, uint64_t pos0, void* ws, int64_t ws_bytes, cudaStream_t s);
 int launch_advance(const AdvanceArgs& a, cudaStream_t s);
 int launch_advance_2phase(const AdvanceArgs& a, void* ws, int64_t ws_bytes, cudaStream_t s);
 int64_t advance_ws_bytes(int64_t nslots, int64_t nsteps);

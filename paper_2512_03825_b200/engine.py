@@ -34,6 +34,29 @@ def _stream(device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
+PARALLEL_FILL_MIN_SITES = 1 << 16  # below: the warp-sequential kernel (shared memory) wins
+PARALLEL_FILL_WS_BYTES = 2 << 30
+
+
+def fill_lattices(spins: torch.Tensor, L: int, up_count: int, seed: int, stream0: int,
+                  stream: int) -> None:
+    """Exact-count init of every lattice in `spins` (rows, L, L) int8 from
+    stream stream0 + r, position 0 (executor.py:203-205, kernels.py:26-45)."""
+    rows = spins.shape[0]
+    if rows == 0:
+        return
+    if L * L < PARALLEL_FILL_MIN_SITES:
+        _lib.call("ptmh_fill_lattices", _P(spins), rows, L, up_count, seed, stream0, 0, stream)
+        return
+    per_row = int(_lib.LIB.ptmh_fill_workspace_bytes(L, 1))
+    k = max(1, min(rows, PARALLEL_FILL_WS_BYTES // per_row))
+    ws = torch.empty(int(_lib.LIB.ptmh_fill_workspace_bytes(L, k)), dtype=torch.uint8,
+                     device=spins.device)
+    _lib.call("ptmh_fill_lattices_parallel", _P(spins), rows, L, up_count, seed, stream0, 0,
+              _P(ws), ws.numel(), stream)
+    del ws
+
+
 def require_cuda(device=None) -> torch.device:
     if not torch.cuda.is_available():
         raise RuntimeError("paper_2512_03825_b200 needs a CUDA device (B200, sm_100a); "
@@ -98,7 +121,7 @@ class ExactEngine(_Base):
         """executor.py:203-207: row r from stream r, position 0."""
         s = self._s()
         R, L = self.R, self.L
-        _lib.call("ptmh_fill_lattices", _P(self.spins), R, L, self.up_count, self.seed, 0, 0, s)
+        fill_lattices(self.spins, L, self.up_count, self.seed, 0, s)
         stats = torch.empty((R, 2), dtype=torch.int64, device=self.dev)
         _lib.call("ptmh_row_stats", _P(self.spins), R, L, _P(stats), s)
         st = stats.cpu().numpy()
@@ -182,8 +205,7 @@ class CheckerboardEngine(_Base):
         if self.rows == 0:
             return
         spins = torch.empty((self.rows, self.L, self.L), dtype=torch.int8, device=self.dev)
-        _lib.call("ptmh_fill_lattices", _P(spins), self.rows, self.L, self.up_count, self.seed,
-                  self.row_lo, 0, s)
+        fill_lattices(spins, self.L, self.up_count, self.seed, self.row_lo, s)
         _lib.call("ptmh_row_stats", _P(spins), self.rows, self.L, _P(self.local_stats), s)
         _lib.call("ptmh_cb_pack", _P(spins), self.rows, self.L, _P(self.packed), s)
         del spins
