@@ -176,6 +176,11 @@ int ptmh_cb_pack(const int8_t *spins, int64_t rows, int64_t L, uint32_t *packed,
 int ptmh_cb_unpack(const uint32_t *packed, int64_t rows, int64_t L,
                    int8_t *spins, void *stream);
 
+/* out (R, L, L) int8: lattice slot_to_row[k] unpacked into out[k] (by slot;
+ * full_states recording). */
+int ptmh_cb_unpack_slots(const uint32_t *packed, const int64_t *slot_to_row,
+                         int64_t R, int64_t L, int8_t *out, void *stream);
+
 /* n_sweeps checkerboard sweeps (colour 0 then 1) of rows [0, rows) starting
  * at global sweep first_sweep.  Row r is at slot row_to_slot[r] (global slot
  * index; row_offset is the global index of local row 0, unused by the

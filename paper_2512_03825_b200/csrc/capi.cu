@@ -311,6 +311,12 @@ int ptmh_cb_run_resident(uint32_t* packed, int64_t R, int64_t L, int64_t* slot_t
     return launch_cb_resident(a, a.WR > 0, as_stream(stream), nullptr);
 }
 
+int ptmh_cb_unpack_slots(const uint32_t* packed, const int64_t* slot_to_row, int64_t R, int64_t L,
+                         int8_t* out, void* stream) {
+    PTMH_CHECK_ARG(L >= 2 && L % 2 == 0 && R >= 0, "cb_unpack_slots shape");
+    return launch_cb_unpack_slots(packed, slot_to_row, R, L, out, as_stream(stream));
+}
+
 int ptmh_cb_row_stats(const uint32_t* packed, int64_t rows, int64_t L, int64_t* stats, void* stream) {
     PTMH_CHECK_ARG(L >= 2 && L % 2 == 0, "checkerboard needs even L");
     return launch_cb_row_stats(packed, rows, L, stats, as_stream(stream));

@@ -431,6 +431,20 @@ __global__ void cb_unpack_kernel(const uint32_t* __restrict__ packed, int64_t ro
     spins[tid] = bit ? 1 : -1;
 }
 
+// lattices in slot order: out[k] = lattice slot_to_row[k] (full_states recording)
+__global__ void cb_unpack_slots_kernel(const uint32_t* __restrict__ packed, const int64_t* __restrict__ s2r,
+                                       int64_t R, int L, int64_t W, int8_t* __restrict__ out) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n = (int64_t)L * L;
+    if (tid >= R * n) return;
+    const int64_t k = tid / n, site = tid - k * n;
+    const int64_t lat = s2r[k];
+    const int i = (int)(site / L), j = (int)(site - (int64_t)i * L);
+    const int color = (i + j) & 1;
+    const int64_t h = (int64_t)i * (L / 2) + (j >> 1);
+    out[tid] = ((packed[(lat * 2 + color) * W + (h >> 5)] >> (h & 31)) & 1u) ? 1 : -1;
+}
+
 // Audit reduction from the packed state: S over both colours, Bond as the sum
 // over colour-0 sites of s*nb = 2k - 4 (every bond has one colour-0 end).
 __global__ void cb_row_stats_kernel(const uint32_t* __restrict__ packed, int64_t rows, int L, int64_t W,
@@ -601,6 +615,15 @@ int launch_cb_unpack(const uint32_t* packed, int64_t rows, int64_t L, int8_t* sp
     const int64_t W = cb_words(L), n = rows * L * L;
     if (n == 0) return PTMH_OK;
     cb_unpack_kernel<<<ceil_div(n, 256), 256, 0, s>>>(packed, rows, (int)L, W, spins);
+    PTMH_LAUNCH_CHECK();
+    return PTMH_OK;
+}
+
+int launch_cb_unpack_slots(const uint32_t* packed, const int64_t* s2r, int64_t R, int64_t L, int8_t* out,
+                           cudaStream_t s) {
+    const int64_t n = R * L * L;
+    if (n == 0) return PTMH_OK;
+    cb_unpack_slots_kernel<<<ceil_div(n, 256), 256, 0, s>>>(packed, s2r, R, (int)L, cb_words(L), out);
     PTMH_LAUNCH_CHECK();
     return PTMH_OK;
 }

@@ -56,6 +56,8 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
 int launch_cb_pack(const int8_t* spins, int64_t rows, int64_t L, uint32_t* packed, cudaStream_t s);
 int launch_cb_unpack(const uint32_t* packed, int64_t rows, int64_t L, int8_t* spins, cudaStream_t s);
 int launch_cb_row_stats(const uint32_t* packed, int64_t rows, int64_t L, int64_t* stats, cudaStream_t s);
+int launch_cb_unpack_slots(const uint32_t* packed, const int64_t* s2r, int64_t R, int64_t L, int8_t* out,
+                           cudaStream_t s);
 int launch_cb_slot_energies(const int64_t* stats, const int64_t* s2r, int64_t R, double J, double B,
                             double* energies, int64_t* sums, cudaStream_t s);
 int launch_cb_observe(const int64_t* stats, const int64_t* s2r, int64_t R, int64_t L, double J, double B,

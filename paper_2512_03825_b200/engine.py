@@ -265,6 +265,11 @@ class CheckerboardEngine(_Base):
         _lib.call("ptmh_cb_observe", _P(self.stats), _P(self.slot_to_row), self.R, self.L,
                   self.J, self.B, _P(obs_e), _P(obs_m), obs_e.shape[1], col, self._s())
 
+    def snapshot_by_slot(self, out: torch.Tensor) -> None:
+        """out (R, L, L) int8 <- every lattice, in slot order (full_states)."""
+        _lib.call("ptmh_cb_unpack_slots", _P(self.packed), _P(self.slot_to_row), self.R, self.L,
+                  _P(out), self._s())
+
     def audit_stats(self) -> torch.Tensor:
         """(S, Bond) recomputed from the packed lattices (local rows)."""
         out = torch.empty((self.rows, 2), dtype=torch.int64, device=self.dev)

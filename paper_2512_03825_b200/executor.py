@@ -99,9 +99,6 @@ class SimulationConfig:
                 raise ConfigurationError(
                     "iterations and swap_interval must be whole sweeps (multiples of side**2) "
                     "in checkerboard mode")
-            if self.record_mode == "full_states":
-                raise ConfigurationError(
-                    "record_mode 'full_states' is only available with sweep_mode='exact'")
             if (self.iterations // n) // self.record_every < 1 and self.record_mode != "none":
                 raise ConfigurationError("record_every exceeds the number of sweeps")
 
@@ -167,6 +164,34 @@ def _resident_wins(L: int, swap_every_sweeps: int) -> bool:
     """Persistent launch for small lattices or per-sweep exchanges, where the
     two-launches-per-sweep path is launch-latency bound."""
     return L <= 256 or swap_every_sweeps == 1
+
+
+class _StateStream:
+    """full_states recording for the checkerboard chain: each sample is
+    unpacked on the device in slot order into one of two staging buffers and
+    copied asynchronously into a pinned host array (R, n_samples, L, L), so
+    the copy of sample c overlaps the sweeps towards sample c+1."""
+
+    def __init__(self, R: int, n: int, L: int, dev):
+        self.host = torch.empty((R, n, L, L), dtype=torch.int8, pin_memory=True)
+        self.stage = [torch.empty((R, L, L), dtype=torch.int8, device=dev) for _ in range(2)]
+        self.done = [torch.cuda.Event(), torch.cuda.Event()]
+        self.copy = torch.cuda.Stream(dev)
+        self.k = 0
+
+    def push(self, eng, col: int) -> None:
+        b = self.k & 1
+        self.done[b].synchronize()  # the copy that last used this buffer finished
+        eng.snapshot_by_slot(self.stage[b])
+        self.copy.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(self.copy):
+            self.host[:, col].copy_(self.stage[b], non_blocking=True)
+            self.done[b].record(self.copy)
+        self.k += 1
+
+    def result(self) -> np.ndarray:
+        self.copy.synchronize()
+        return self.host.numpy()
 
 
 def _sync(dev):
@@ -267,6 +292,8 @@ def _run_checkerboard(config: SimulationConfig) -> RunRecord:
         n_samples = sweeps // config.record_every if record else 0
         obs_e = torch.empty((R, n_samples), dtype=torch.float64, device=dev) if record else None
         obs_m = torch.empty((R, n_samples), dtype=torch.float64, device=dev) if record else None
+        full = config.record_mode == "full_states"
+        states = _StateStream(R, n_samples, L, dev) if full else None
         _sync(dev)
         init_seconds = time.perf_counter() - t0
 
@@ -275,7 +302,8 @@ def _run_checkerboard(config: SimulationConfig) -> RunRecord:
         n_rounds = sum(1 for _, ri in plan if ri is not None)
         snaps = np.zeros((n_rounds, R), dtype=np.int64) if record and n_rounds else None
         done = rounds = attempted = 0
-        use_resident = config.kernel == "resident" or (config.kernel == "auto" and _resident_wins(L, every_sw))
+        use_resident = not full and (config.kernel == "resident" or
+                                     (config.kernel == "auto" and _resident_wins(L, every_sw)))
         try:
             if use_resident:
                 # the whole run in one persistent launch; the schedule is replayed
@@ -300,6 +328,8 @@ def _run_checkerboard(config: SimulationConfig) -> RunRecord:
                     done = nxt
                     if record and done % config.record_every == 0:
                         eng.observe(obs_e, obs_m, done // config.record_every - 1)
+                        if full:
+                            states.push(eng, done // config.record_every - 1)
                 if ri is None:
                     continue
                 if snaps is not None:
@@ -317,7 +347,8 @@ def _run_checkerboard(config: SimulationConfig) -> RunRecord:
         config=config, temperatures=temps,
         energies=obs_e.cpu().numpy() if (valid and record) else None,
         magnetizations=obs_m.cpu().numpy() if (valid and record) else None,
-        states=None, swap_rounds=rounds, swaps_attempted=attempted, swaps_accepted=accepted,
+        states=states.result() if (valid and full) else None, swap_rounds=rounds,
+        swaps_attempted=attempted, swaps_accepted=accepted,
         rng_positions=np.full(R, n_sites - 1, dtype=np.int64),
         round_entry_iterations=snaps, init_seconds=init_seconds, exec_seconds=exec_seconds,
         total_seconds=time.perf_counter() - t_start, valid=valid,

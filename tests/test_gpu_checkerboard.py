@@ -242,3 +242,19 @@ def test_sweeps_match_oracle_at_2048(mods):
     oracle.cb_sweep(ref, np.arange(R, dtype=np.int64), thr, always, 21, 0, stats)
     assert np.array_equal(eng.final_spins(), ref)
     assert np.array_equal(eng.local_stats.cpu().numpy(), stats)
+
+
+@pytest.mark.parametrize("L,R,sweeps,every,rec_every", [(4, 3, 40, 2, 1), (64, 4, 12, 3, 2),
+                                                        (6, 5, 30, 1, 3)])
+def test_full_states_match_oracle(mods, L, R, sweeps, every, rec_every):
+    p = mods[0]
+    rec = p.run(p.SimulationConfig(side=L, replicas=R, iterations=sweeps * L * L,
+                                   swap_interval=every * L * L, seed=31, sweep_mode="checkerboard",
+                                   record_mode="full_states", record_every=rec_every))
+    assert rec.valid, rec.error
+    ref = oracle.run_checkerboard(L, R, sweeps, every, 31, record_every=rec_every, record_states=True)
+    assert rec.states.shape == (R, sweeps // rec_every, L, L)
+    assert np.array_equal(rec.states, ref.states)
+    assert np.array_equal(rec.energies, ref.energies)
+    # magnetisations are the recorded states' means (reference test_executor.py:172-181)
+    assert np.array_equal(rec.magnetizations, rec.states.sum(axis=(2, 3)) / (L * L))

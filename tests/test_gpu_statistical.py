@@ -108,3 +108,16 @@ def test_checkerboard_phase_transition(p):
     assert np.all(mags[temps >= 3.5] < 0.3)
     k = int(np.argmax(mags[:-1] - mags[1:]))
     assert temps[k] >= 2.0 and temps[k + 1] <= 2.6
+
+
+def test_checkerboard_state_marginal_L2(p):
+    """reference tests/test_sampling.py:48-57 for the checkerboard chain: the
+    full-state marginal of slot 1 (T = 2.5) vs exact enumeration."""
+    sweeps = 200_000
+    rec = p.run(p.SimulationConfig(side=2, replicas=2, iterations=sweeps * 4, swap_interval=0,
+                                   seed=11, sweep_mode="checkerboard", record_mode="full_states"))
+    st = rec.states[1].reshape(-1, 4)
+    codes = ((st > 0).astype(np.int64) << np.arange(4)).sum(1)
+    emp = np.bincount(codes, minlength=16) / codes.size
+    _, _, _, w = exact_levels(2, 2.5)
+    assert tv(emp, w) < 0.01

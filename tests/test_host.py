@@ -122,8 +122,7 @@ class TestConfigValidation:  # reference tests/test_executor.py:217-224
         ok.validate()
         for kw in [dict(side=7, iterations=49, swap_interval=0),
                    dict(side=8, iterations=100, swap_interval=0),
-                   dict(side=8, iterations=640, swap_interval=10),
-                   dict(side=8, iterations=640, swap_interval=64, record_mode="full_states")]:
+                   dict(side=8, iterations=640, swap_interval=10)]:
             with pytest.raises(ConfigurationError):
                 SimulationConfig(replicas=2, sweep_mode="checkerboard", **kw).validate()
 
