@@ -302,10 +302,12 @@ def main():
         for _ in range(args.warmup):
             step()
         torch.cuda.synchronize()
-        for _ in range(args.steps):
+        for it in range(args.steps):
             flush.zero_()
+            # per-launch events in every 4th timed step (they cost ~1-2 us each)
+            probe = it % 4 == 0
             ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                  for _ in range(1 if resident else every)]
+                  for _ in range(1 if resident else every)] if probe else None
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             if sharded:
                 dist.barrier()
@@ -315,7 +317,8 @@ def main():
             s1.record(stream)
             torch.cuda.synchronize()
             step_ms.append(s0.elapsed_time(s1))
-            sweep_ms.extend(a.elapsed_time(b) for a, b in ev)
+            if probe:
+                sweep_ms.extend(a.elapsed_time(b) for a, b in ev)
     total_ms = sum(step_ms)
     if sharded:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -411,7 +414,7 @@ def main():
                              "note": "issue-bound (Philox + bit-sliced logic), see DESIGN.md 5",
                              "issue_from_ncu": _issue(args.config) if not resident else None},
                 "cpu_baseline": cpu, "e2e": e2e, "exact_chain": exact,
-                "gpu_launches": args.steps * (1 if resident else 2 * every + 2),
+                "gpu_launches": args.steps * (1 if resident else 2 * every + 1),
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if sharded:

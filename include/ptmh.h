@@ -167,6 +167,16 @@ int ptmh_swap_chunk(int64_t *slot_to_row, double *energies, int64_t *spin_sums,
                     int64_t pair_lo, int64_t pair_hi, int64_t *accepted,
                     int64_t *near_ties, int32_t *row_to_slot, void *stream);
 
+/* One checkerboard exchange round in one launch: energies[k] / spin_sums[k]
+ * of slot k from the per-lattice stats (as ptmh_cb_slot_energies), then the
+ * reference swap rule for round_index (as ptmh_swap_chunk with stream_base R,
+ * all pairs), then row_to_slot rebuilt. */
+int ptmh_cb_exchange(const int64_t *stats_all, int64_t *slot_to_row,
+                     int32_t *row_to_slot, int64_t R, double J, double B,
+                     const double *betas, uint64_t seed, int64_t round_index,
+                     double *energies, int64_t *spin_sums, int64_t *accepted,
+                     int64_t *near_ties, void *stream);
+
 /* Checkerboard (Mode F) storage: per lattice, colour c in {0,1}, half-lattice
  * site h = i*(L/2) + (j>>1) of colour (i+j)&1 is bit (h & 31) of word
  * packed[(row*2 + c)*W + (h >> 5)], W = ceil(L*L/64); bit set <=> spin +1. */

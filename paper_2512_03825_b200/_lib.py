@@ -55,6 +55,7 @@ def _load():
                                      P, P, i64, P, i64, P], i32),
         "ptmh_swap_chunk": ([P, P, P, P, i64, u64, i64, i64, i64, i64, i64, P, P, P, P], i32),
         "ptmh_cb_words_per_color": ([i64], i64),
+        "ptmh_cb_exchange": ([P, P, P, i64, f64, f64, P, u64, i64, P, P, P, P, P], i32),
         "ptmh_cb_pack": ([P, i64, i64, P, P], i32),
         "ptmh_cb_unpack": ([P, i64, i64, P, P], i32),
         "ptmh_cb_sweeps": ([P, i64, i64, P, P, u32, u64, i64, i64, P, P], i32),

@@ -242,6 +242,16 @@ int ptmh_swap_chunk(int64_t* slot_to_row, double* energies, int64_t* spin_sums, 
                        pair_lo, pair_hi, accepted, near_ties, row_to_slot, as_stream(stream));
 }
 
+int ptmh_cb_exchange(const int64_t* stats_all, int64_t* slot_to_row, int32_t* row_to_slot, int64_t R,
+                     double J, double B, const double* betas, uint64_t seed, int64_t round_index,
+                     double* energies, int64_t* spin_sums, int64_t* accepted, int64_t* near_ties,
+                     void* stream) {
+    PTMH_CHECK_ARG(R >= 1 && round_index >= 0, "cb_exchange args");
+    const int64_t first = round_index % 2, n_pairs = std::max<int64_t>(0, (R - first) / 2);
+    return launch_swap(slot_to_row, energies, spin_sums, betas, R, seed, R, round_index, first, 0, n_pairs,
+                       accepted, near_ties, row_to_slot, as_stream(stream), stats_all, J, B);
+}
+
 int64_t ptmh_cb_words_per_color(int64_t L) { return cb_words(L); }
 
 int ptmh_cb_pack(const int8_t* spins, int64_t rows, int64_t L, uint32_t* packed, void* stream) {
@@ -584,12 +594,12 @@ int ptmh_host_cb_interval(int8_t* spins, int64_t R, int64_t L, int64_t* slot_to_
                     t_out);
         }
     }
-    PTMH_TRY(launch_cb_slot_energies(d_stats, d_s2r, R, J, B, d_e, d_sums, sc));
-    if (round_index >= 0) {
+    if (round_index >= 0) {  // energies by slot + the round, one launch
         const int64_t first = round_index % 2, n_pairs = std::max<int64_t>(0, (R - first) / 2);
-        if (n_pairs > 0)
-            PTMH_TRY(launch_swap(d_s2r, d_e, d_sums, d_b, R, seed, R, round_index, first, 0, n_pairs, d_cnt,
-                                 d_cnt + 1, nullptr, sc));
+        PTMH_TRY(launch_swap(d_s2r, d_e, d_sums, d_b, R, seed, R, round_index, first, 0, n_pairs, d_cnt,
+                             d_cnt + 1, nullptr, sc, d_stats, J, B));
+    } else {
+        PTMH_TRY(launch_cb_slot_energies(d_stats, d_s2r, R, J, B, d_e, d_sums, sc));
     }
     int64_t cnt[2];
     PTMH_CUDA(cudaMemcpyAsync(slot_to_row, d_s2r, R * 8, cudaMemcpyDeviceToHost, sc));

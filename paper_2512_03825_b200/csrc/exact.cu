@@ -601,7 +601,17 @@ __global__ void swap_kernel(int64_t* __restrict__ slot_to_row, double* __restric
                             int64_t* __restrict__ spin_sums, const double* __restrict__ betas,
                             int64_t R, uint64_t seed, int64_t stream_base, int64_t round_index,
                             int64_t first, int64_t pair_lo, int64_t pair_hi,
-                            int64_t* accepted, int64_t* near_ties, int32_t* row_to_slot) {
+                            int64_t* accepted, int64_t* near_ties, int32_t* row_to_slot,
+                            const int64_t* __restrict__ stats, double J, double B) {
+    if (stats) {  // checkerboard chain: by-slot energies from per-lattice (S, Bond) first
+        for (int64_t k = threadIdx.x; k < R; k += blockDim.x) {
+            const int64_t row = slot_to_row[k];
+            const int64_t S = stats[2 * row], Bd = stats[2 * row + 1];
+            energies[k] = __dsub_rn(__dmul_rn(B, (double)S), __dmul_rn(J, (double)Bd));
+            spin_sums[k] = S;
+        }
+        __syncthreads();
+    }
     int acc = 0, ties = 0;
     for (int64_t p = pair_lo + threadIdx.x; p < pair_hi; p += blockDim.x) {
         const int64_t i = first + 2 * p, j = i + 1;
@@ -674,10 +684,10 @@ int launch_advance(const AdvanceArgs& a, cudaStream_t s) {
 int launch_swap(int64_t* slot_to_row, double* energies, int64_t* spin_sums, const double* betas,
                 int64_t R, uint64_t seed, int64_t stream_base, int64_t round_index, int64_t first,
                 int64_t pair_lo, int64_t pair_hi, int64_t* accepted, int64_t* near_ties,
-                int32_t* row_to_slot, cudaStream_t s) {
+                int32_t* row_to_slot, cudaStream_t s, const int64_t* stats, double J, double B) {
     swap_kernel<<<1, 1024, 0, s>>>(slot_to_row, energies, spin_sums, betas, R, seed, stream_base,
                                    round_index, first, pair_lo, pair_hi, accepted, near_ties,
-                                   row_to_slot);
+                                   row_to_slot, stats, J, B);
     PTMH_LAUNCH_CHECK();
     return PTMH_OK;
 }

@@ -46,7 +46,8 @@ int launch_bits_unpack(const uint32_t* bits, int64_t rows, int64_t L, int8_t* sp
 int launch_swap(int64_t* slot_to_row, double* energies, int64_t* spin_sums, const double* betas,
                 int64_t R, uint64_t seed, int64_t stream_base, int64_t round_index, int64_t first,
                 int64_t pair_lo, int64_t pair_hi, int64_t* accepted, int64_t* near_ties,
-                int32_t* row_to_slot, cudaStream_t s);
+                int32_t* row_to_slot, cudaStream_t s, const int64_t* stats = nullptr, double J = 0.0,
+                double B = 0.0);
 
 // checkerboard.cu
 int64_t cb_words(int64_t L);

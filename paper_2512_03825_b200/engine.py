@@ -227,17 +227,12 @@ class CheckerboardEngine(_Base):
     def exchange(self, round_index: int) -> int:
         """Swap round on the energies of every lattice (self.stats must hold
         all lattices: the distributed driver all-gathers them first)."""
-        s = self._s()
         first = round_index % 2
-        n_pairs = max(0, (self.R - first) // 2)
-        _lib.call("ptmh_cb_slot_energies", _P(self.stats), _P(self.slot_to_row), self.R, self.J,
-                  self.B, _P(self.energies), _P(self.spin_sums), s)
-        if n_pairs:
-            _lib.call("ptmh_swap_chunk", _P(self.slot_to_row), _P(self.energies),
-                      _P(self.spin_sums), _P(self.betas), self.R, self.seed, self.R,
-                      round_index, first, 0, n_pairs, _P(self.counters),
-                      self.counters.data_ptr() + 8, _P(self.row_to_slot), s)
-        return n_pairs
+        _lib.call("ptmh_cb_exchange", _P(self.stats), _P(self.slot_to_row), _P(self.row_to_slot),
+                  self.R, self.J, self.B, _P(self.betas), self.seed, round_index,
+                  _P(self.energies), _P(self.spin_sums), _P(self.counters),
+                  self.counters.data_ptr() + 8, self._s())
+        return max(0, (self.R - first) // 2)
 
     def run_resident(self, first_sweep: int, n_sweeps: int, total_sweeps: int, swap_every: int,
                      record_every: int = 0, obs_e=None, obs_m=None) -> None:
