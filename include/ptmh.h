@@ -210,16 +210,18 @@ int ptmh_cb_sweeps(uint32_t *packed, int64_t rows, int64_t L,
  * slot_to_row2 (2, R) int64 / row_to_slot2 (2, R) int32 are double buffers;
  * `buf` names the one holding the current permutation, *buf_out receives the
  * one holding it afterwards.  stats (R, 2) hold every lattice's (S, Bond)
- * after the segment.  Same chain and random numbers as ptmh_cb_sweeps. */
+ * after the segment.  slot_stats is caller-owned scratch of 4 * R int64 (the
+ * per-slot (S, Bond) table an exchange round reads, double-buffered by round
+ * parity).  Same chain and random numbers as ptmh_cb_sweeps. */
 int ptmh_cb_run_resident(uint32_t *packed, int64_t R, int64_t L,
                          int64_t *slot_to_row2, int32_t *row_to_slot2, int buf,
                          const uint32_t *thresh, uint32_t always_mask,
                          uint64_t seed, double J, double B, const double *betas,
-                         int64_t *stats, int64_t *counters, double *obs_e,
-                         double *obs_m, int64_t ncols, int64_t first_sweep,
-                         int64_t n_sweeps, int64_t total_sweeps,
-                         int64_t swap_every, int64_t record_every, int *buf_out,
-                         void *stream);
+                         int64_t *stats, int64_t *slot_stats,
+                         int64_t *counters, double *obs_e, double *obs_m,
+                         int64_t ncols, int64_t first_sweep, int64_t n_sweeps,
+                         int64_t total_sweeps, int64_t swap_every,
+                         int64_t record_every, int *buf_out, void *stream);
 
 /* Per-lattice (S, Bond) recomputed from the packed state (audit of the
  * incremental stats; L % 64 == 0 or any even L). */

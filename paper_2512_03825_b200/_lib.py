@@ -62,7 +62,7 @@ def _load():
         "ptmh_cb_row_stats": ([P, i64, i64, P, P], i32),
         "ptmh_cb_unpack_slots": ([P, P, i64, i64, P, P], i32),
         "ptmh_cb_run_resident": ([P, i64, i64, P, P, i32, P, u32, u64, f64, f64, P, P, P, P, P,
-                                  i64, i64, i64, i64, i64, i64, P, P], i32),
+                                  P, i64, i64, i64, i64, i64, i64, P, P], i32),
         "ptmh_cb_slot_energies": ([P, P, i64, f64, f64, P, P, P], i32),
         "ptmh_cb_observe": ([P, P, i64, i64, f64, f64, P, P, i64, i64, P], i32),
     }

@@ -276,11 +276,13 @@ int ptmh_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* row
 
 int ptmh_cb_run_resident(uint32_t* packed, int64_t R, int64_t L, int64_t* slot_to_row2, int32_t* row_to_slot2,
                          int buf, const uint32_t* thresh, uint32_t always_mask, uint64_t seed, double J, double B,
-                         const double* betas, int64_t* stats, int64_t* counters, double* obs_e, double* obs_m,
-                         int64_t ncols, int64_t first_sweep, int64_t n_sweeps, int64_t total_sweeps,
+                         const double* betas, int64_t* stats, int64_t* slot_stats, int64_t* counters,
+                         double* obs_e, double* obs_m, int64_t ncols, int64_t first_sweep, int64_t n_sweeps,
+                         int64_t total_sweeps,
                          int64_t swap_every, int64_t record_every, int* buf_out, void* stream) {
     PTMH_CHECK_ARG(L >= 2 && L % 2 == 0 && L <= 65536 && R >= 1 && R < (1LL << 26), "resident shape");
     PTMH_CHECK_ARG(buf == 0 || buf == 1, "resident buffer index");
+    PTMH_CHECK_ARG(slot_stats != nullptr || swap_every == 0, "resident slot_stats scratch");
     PTMH_CHECK_ARG(first_sweep >= 0 && n_sweeps >= 0 && first_sweep + n_sweeps <= total_sweeps &&
                        total_sweeps < (1LL << 31), "resident sweep range");
     PTMH_CHECK_ARG(record_every == 0 || (obs_e && obs_m && total_sweeps / record_every <= ncols),
@@ -302,6 +304,7 @@ int ptmh_cb_run_resident(uint32_t* packed, int64_t R, int64_t L, int64_t* slot_t
     a.r2s[0] = row_to_slot2;
     a.r2s[1] = row_to_slot2 + R;
     a.stats = stats;
+    a.slot_stats = slot_stats;
     a.counters = counters;
     a.obs_e = obs_e;
     a.obs_m = obs_m;

@@ -76,6 +76,7 @@ struct ResidentArgs {
     int64_t* s2r[2];   // double-buffered slot_to_row
     int32_t* r2s[2];   // double-buffered row_to_slot
     int64_t* stats;    // (R, 2)
+    int64_t* slot_stats;  // (2, R, 2): (S, Bond) by slot, buffer = round parity
     int64_t* counters; // accepted, near ties
     double* obs_e;
     double* obs_m;
@@ -86,6 +87,7 @@ struct ResidentArgs {
     int buf;               // permutation buffer holding the current mapping
     int n_up, up_k[10], up_sf[10], up_cls[10];
     int ferro;
+    uint32_t seg_lo, seg_even;  // L in {8, 16, 32}: bit 0 of each row segment, even-row segments
 };
 int launch_cb_resident(const ResidentArgs& a, bool fast, cudaStream_t s, int* grid_out);
 void fill_class_plan(uint32_t always_mask, int* n_up, int* k, int* sf, int* cls, int* ferro);

@@ -17,6 +17,7 @@
 // same random numbers, bit-exact with oracle/ptmh_oracle.c); ties are resolved
 // in place by the owning lane.
 #include <cooperative_groups.h>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -35,13 +36,17 @@ __device__ __forceinline__ uint32_t resident_bit(const uint32_t* p, int h) {
 
 // one colour-c word of a lattice: gather neighbour words, decide, store;
 // returns nothing, adds the colour-1 (S, Bond) contributions when `stats`
-template <bool kFast, bool kFerro>
+// gather modes: rows of 64+ sites (L % 64 == 0), whole rows per word
+// (L = 8, 16, 32: a word holds 64 / L rows of L/2 same-colour sites), any even L
+enum { kGatherGeneric = 0, kGatherRows = 1, kGatherSegments = 2 };
+
+template <int kMode, bool kFerro>
 __device__ __forceinline__ void resident_word(const ResidentArgs& A, uint32_t* own, const uint32_t* oth,
                                               int w, int color, int slot, uint32_t ctr1, int& sumS,
                                               int& sumB, bool stats, const uint32_t* masks, int wr_shift) {
     const int L = A.L;
     uint32_t S = own[w], n1, n2, n3, n4, valid;
-    if (kFast) {
+    if (kMode == kGatherRows) {
         const int WR = A.WR;
         const int i = wr_shift >= 0 ? (w >> wr_shift) : w / WR, k = w - i * WR;
         const int iu = (i == 0) ? L - 1 : i - 1, id = (i == L - 1) ? 0 : i + 1;
@@ -54,6 +59,21 @@ __device__ __forceinline__ void resident_word(const ResidentArgs& A, uint32_t* o
         } else {
             n4 = __funnelshift_r(mid, oth[i * WR + (k == WR - 1 ? 0 : k + 1)], 1);
         }
+        valid = 0xffffffffu;
+    } else if (kMode == kGatherSegments) {
+        // word w = rows w*q .. w*q+q-1 of this colour, q = 64 / L, seg = L / 2
+        // sites each; q is even, so segment s has row parity s & 1
+        const int seg = L >> 1, W = A.W;
+        const uint32_t mid = oth[w];
+        const uint32_t prev = oth[w == 0 ? W - 1 : w - 1], next = oth[w == W - 1 ? 0 : w + 1];
+        n1 = __funnelshift_l(prev, mid, seg);       // row above: previous segment
+        n2 = __funnelshift_r(mid, next, seg);       // row below: next segment
+        n3 = mid;
+        const uint32_t lo_bits = A.seg_lo, hi_bits = lo_bits << (seg - 1);  // bit 0 / top bit of each segment
+        const uint32_t rot_l = ((mid << 1) & ~lo_bits) | ((mid >> (seg - 1)) & lo_bits);  // site m-1
+        const uint32_t rot_r = ((mid >> 1) & ~hi_bits) | ((mid << (seg - 1)) & hi_bits);  // site m+1
+        const uint32_t even = color ? ~A.seg_even : A.seg_even;  // segments with (row + colour) even
+        n4 = (rot_l & even) | (rot_r & ~even);
         valid = 0xffffffffu;
     } else {
         const int Lh = L / 2, H = L * Lh;
@@ -168,10 +188,30 @@ __device__ __forceinline__ void resident_word(const ResidentArgs& A, uint32_t* o
 
 constexpr int kMaxLatPerBlock = 64;
 
+// lattice li of this block now holds `slot`: cache its slot and (ferro) the
+// threshold bit-plane masks in shared memory
+template <bool kFerro>
+__device__ __forceinline__ void resident_set_slot(const ResidentArgs& A, int li, int slot, int* s_slot,
+                                                  uint32_t (*s_mask)[18]) {
+    s_slot[li] = slot;
+    if (kFerro) {
+        const uint32_t t3 = __ldg(A.thresh + slot * 10 + 8), t4 = __ldg(A.thresh + slot * 10 + 9);
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+            s_mask[li][p] = 0u - ((t3 >> (31 - p)) & 1u);
+            s_mask[li][8 + p] = 0u - ((t4 >> (31 - p)) & 1u);
+        }
+        s_mask[li][16] = t3;
+        s_mask[li][17] = t4;
+    }
+}
+
 // Block b owns the contiguous lattices [lo, hi) and sweeps them together:
 // work items (lattice, word) are spread over all threads, __syncthreads
 // separates the colours, per-lattice (S, Bond) accumulate in shared memory.
-template <bool kFast, bool kFerro, int kThreads>
+// Slots live in shared memory for the whole launch: only the owner changes
+// them, after an exchange round.
+template <int kMode, bool kFerro, int kThreads>
 __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
     __shared__ int s_slot[kMaxLatPerBlock];
     __shared__ int s_S[kMaxLatPerBlock], s_B[kMaxLatPerBlock];
@@ -183,36 +223,26 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
     const int hi = (int)((int64_t)R * (blockIdx.x + 1) / gridDim.x);
     const int nl = hi - lo;
     const int items = nl * W;
+    const int items_pad = (items + 31) & ~31;  // whole warps iterate together (warp-reduced stats)
+    // (li, w) of this thread's first item and the per-iteration step
+    const int li_0 = (int)threadIdx.x / W, w_0 = (int)threadIdx.x - li_0 * W;
+    const int step_l = (int)blockDim.x / W, step_w = (int)blockDim.x - step_l * W;
     int buf = A.buf;
+    for (int i = threadIdx.x; i < nl; i += blockDim.x) {
+        resident_set_slot<kFerro>(A, i, A.r2s[buf][lo + i], s_slot, s_mask);
+        s_S[i] = 0;
+        s_B[i] = 0;
+    }
+    __syncthreads();
     for (int64_t t = A.first_sweep; t < A.first_sweep + A.n_sweeps; ++t) {
         const int64_t done = t + 1;
         const bool rec = A.record_every > 0 && done % A.record_every == 0;
         const bool exch = A.swap_every > 0 && done % A.swap_every == 0 && done < A.total_sweeps;
         const bool need_stats = rec || exch || t + 1 == A.first_sweep + A.n_sweeps;
-        for (int i = threadIdx.x; i < nl; i += blockDim.x) {
-            const int sl = A.r2s[buf][lo + i];
-            s_slot[i] = sl;
-            s_S[i] = 0;
-            s_B[i] = 0;
-            if (kFerro) {
-                const uint32_t t3 = __ldg(A.thresh + sl * 10 + 8), t4 = __ldg(A.thresh + sl * 10 + 9);
-                for (int p = 0; p < 8; ++p) {
-                    s_mask[i][p] = 0u - ((t3 >> (31 - p)) & 1u);
-                    s_mask[i][8 + p] = 0u - ((t4 >> (31 - p)) & 1u);
-                }
-                s_mask[i][16] = t3;
-                s_mask[i][17] = t4;
-            }
-        }
-        __syncthreads();
         for (int color = 0; color < 2; ++color) {
             const uint32_t ctr1 = (uint32_t)(2 * t + color);
             const bool st = color == 1 && need_stats;
-            // whole warps iterate together so the stats can be warp-reduced
-            const int items_pad = (items + 31) & ~31;
-            // (li, w) of item `it`, advanced incrementally (no division in the loop)
-            int li_c = (int)threadIdx.x / W, w_c = (int)threadIdx.x - li_c * W;
-            const int step_l = (int)blockDim.x / W, step_w = (int)blockDim.x - step_l * W;
+            int li_c = li_0, w_c = w_0;
             for (int it = threadIdx.x; it < items_pad; it += blockDim.x) {
                 const bool on = it < items;
                 const int li = on ? li_c : 0, w = on ? w_c : 0;
@@ -227,7 +257,7 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
                     uint32_t* c0 = A.packed + (int64_t)(lo + li) * 2 * W;
                     uint32_t* own = color ? c0 + W : c0;
                     const uint32_t* oth = color ? c0 : c0 + W;
-                    resident_word<kFast, kFerro>(A, own, oth, w, color, s_slot[li], ctr1, sS, sB, st,
+                    resident_word<kMode, kFerro>(A, own, oth, w, color, s_slot[li], ctr1, sS, sB, st,
                                                  kFerro ? s_mask[li] : nullptr, wr_shift);
                 }
                 if (st) {
@@ -249,32 +279,38 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
             }
             __syncthreads();
         }
-        if (need_stats) {
-            for (int i = threadIdx.x; i < nl; i += blockDim.x) {
-                const long long S = s_S[i], Bd = s_B[i];
-                A.stats[2 * (lo + i)] = S;
-                A.stats[2 * (lo + i) + 1] = Bd;
-                if (rec) {  // by slot, before the round (executor.py order)
-                    const int64_t col = done / A.record_every - 1;
-                    A.obs_e[(int64_t)s_slot[i] * A.ncols + col] =
-                        __dsub_rn(__dmul_rn(A.B, (double)S), __dmul_rn(A.J, (double)Bd));
-                    A.obs_m[(int64_t)s_slot[i] * A.ncols + col] = __ddiv_rn((double)S, (double)A.L * A.L);
-                }
+        if (!need_stats) continue;
+        // publish (S, Bond); zero the accumulators for the next stats sweep
+        // (the colour-0 barrier separates this from the next accumulation)
+        const int64_t round = exch ? done / A.swap_every - 1 : 0;
+        const int first = (int)(round % 2);
+        const int n_pairs = (R - first) / 2;
+        int64_t* pub = A.slot_stats + (round & 1) * 2 * (int64_t)R;
+        for (int i = threadIdx.x; i < nl; i += blockDim.x) {
+            const long long S = s_S[i], Bd = s_B[i];
+            s_S[i] = 0;
+            s_B[i] = 0;
+            A.stats[2 * (lo + i)] = S;
+            A.stats[2 * (lo + i) + 1] = Bd;
+            const int k = s_slot[i];
+            if (rec) {  // by slot, before the round (executor.py order)
+                const int64_t col = done / A.record_every - 1;
+                A.obs_e[(int64_t)k * A.ncols + col] = __dsub_rn(__dmul_rn(A.B, (double)S), __dmul_rn(A.J, (double)Bd));
+                A.obs_m[(int64_t)k * A.ncols + col] = __ddiv_rn((double)S, (double)A.L * A.L);
+            }
+            if (exch) {
+                // the exchange reads (S, Bond) by slot: one load per partner
+                pub[2 * k] = S;
+                pub[2 * k + 1] = Bd;
+                // the swap draw depends only on (round, pair): draw it before the barrier
+                s_u[i] = (k >= first && (k - first) / 2 < n_pairs)
+                             ? stream_uniform(A.seed, (uint64_t)(R + (k - first) / 2), (uint64_t)round)
+                             : 0.0;
             }
         }
         if (!exch) continue;
-        // the swap draw depends only on (round, pair): draw it before the barrier
-        const int64_t round = done / A.swap_every - 1;
-        const int first = (int)(round % 2);
-        const int n_pairs = (R - first) / 2;
-        for (int li = threadIdx.x; li < nl; li += blockDim.x) {
-            const int k = s_slot[li];
-            s_u[li] = (k >= first && (k - first) / 2 < n_pairs)
-                          ? stream_uniform(A.seed, (uint64_t)(R + (k - first) / 2), (uint64_t)round)
-                          : 0.0;
-        }
-        // every lattice's (S, Bond) is final.  (A point-to-point flag scheme
-        // without this barrier was measured slower: DESIGN.md 5.)
+        // every lattice's (S, Bond) is published.  (A point-to-point flag
+        // scheme without this barrier was measured slower: DESIGN.md 5.)
         cg::this_grid().sync();
         // ---- exchange round: the owner of lattice r decides the pair of its slot
         for (int li = threadIdx.x; li < nl; li += blockDim.x) {
@@ -284,11 +320,8 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
             if (k >= first && (k - first) / 2 < n_pairs) {
                 const int p = (k - first) / 2;
                 const int i = first + 2 * p, j = i + 1;
-                const int64_t ri = A.s2r[buf][i], rj = A.s2r[buf][j];
-                const double Ei = __dsub_rn(__dmul_rn(A.B, (double)A.stats[2 * ri]),
-                                            __dmul_rn(A.J, (double)A.stats[2 * ri + 1]));
-                const double Ej = __dsub_rn(__dmul_rn(A.B, (double)A.stats[2 * rj]),
-                                            __dmul_rn(A.J, (double)A.stats[2 * rj + 1]));
+                const double Ei = __dsub_rn(__dmul_rn(A.B, (double)pub[2 * i]), __dmul_rn(A.J, (double)pub[2 * i + 1]));
+                const double Ej = __dsub_rn(__dmul_rn(A.B, (double)pub[2 * j]), __dmul_rn(A.J, (double)pub[2 * j + 1]));
                 const double u = s_u[li];
                 const double x = __dmul_rn(__dsub_rn(A.betas[i], A.betas[j]), __dsub_rn(Ei, Ej));
                 double prob;
@@ -306,18 +339,20 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
                         atomicAdd((unsigned long long*)&A.counters[1], 1ull);
                 }
             }
+            // the permutation is an output only: nothing in the launch reads it back
             A.r2s[buf ^ 1][r] = nk;
             A.s2r[buf ^ 1][nk] = r;
+            if (nk != k) resident_set_slot<kFerro>(A, li, nk, s_slot, s_mask);
         }
         buf ^= 1;
-        __syncthreads();  // next sweep reads r2s[buf] of this block's lattices
+        __syncthreads();  // next sweep reads s_slot / s_mask
     }
 }
 
-template <bool kFast, bool kFerro, int kThreads>
+template <int kMode, bool kFerro, int kThreads>
 static int launch_resident_t(const ResidentArgs& a, int sms, cudaStream_t s) {
     int per_sm = 0;
-    PTMH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cb_resident_kernel<kFast, kFerro, kThreads>,
+    PTMH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cb_resident_kernel<kMode, kFerro, kThreads>,
                                                             kThreads, 0));
     // enough blocks to fill the GPU, few enough that no block owns more
     // lattices than its shared-memory tables hold
@@ -326,27 +361,59 @@ static int launch_resident_t(const ResidentArgs& a, int sms, cudaStream_t s) {
         set_error("resident kernel: too many lattices per block for this grid");
         return PTMH_ERR_ARG;
     }
+    // as few threads as keep the item loop's trip count: every thread then
+    // does the same number of words per colour (no tail warps at the barrier)
+    const int64_t items = (int64_t)((a.R + grid - 1) / grid) * a.W;
+    const int64_t trips = (items + kThreads - 1) / kThreads;
+    const int threads = (int)std::min<int64_t>(kThreads, (((items + trips - 1) / trips) + 31) & ~31);
     ResidentArgs args = a;
     void* kargs[] = {&args};
-    PTMH_CUDA(cudaLaunchCooperativeKernel((const void*)cb_resident_kernel<kFast, kFerro, kThreads>, grid,
-                                          kThreads, kargs, 0, s));
+    PTMH_CUDA(cudaLaunchCooperativeKernel((const void*)cb_resident_kernel<kMode, kFerro, kThreads>, grid,
+                                          threads, kargs, 0, s));
     return PTMH_OK;
 }
 
-template <bool kFast, bool kFerro>
+template <int kMode, bool kFerro>
 static int launch_resident_sized(const ResidentArgs& a, cudaStream_t s) {
     int dev = 0, sms = 0;
     PTMH_CUDA(cudaGetDevice(&dev));
     PTMH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    // fewer lattices than SMs and big lattices: one wide CTA per lattice
-    if (a.R < sms && a.W >= 1024) return launch_resident_t<kFast, kFerro, 1024>(a, sms, s);
-    return launch_resident_t<kFast, kFerro, 256>(a, sms, s);
+    // One 1024-thread CTA per SM: the per-round grid barrier then has the
+    // fewest participants (measured on B200: C5 +6%, C3 +12% over 256-thread
+    // CTAs).  Fall back to narrower CTAs only when a CTA would own more
+    // lattices than its shared tables hold.
+    if (const char* e = getenv("PTMH_RESIDENT_THREADS")) {  // tuning override
+        if (atoi(e) == 256) return launch_resident_t<kMode, kFerro, 256>(a, sms, s);
+    }
+    int per_sm = 0;
+    PTMH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cb_resident_kernel<kMode, kFerro, 1024>,
+                                                            1024, 0));
+    const int64_t grid = std::min<int64_t>(a.R, (int64_t)sms * std::max(1, per_sm));
+    if ((a.R + grid - 1) / grid <= kMaxLatPerBlock) return launch_resident_t<kMode, kFerro, 1024>(a, sms, s);
+    return launch_resident_t<kMode, kFerro, 256>(a, sms, s);
 }
 
-int launch_cb_resident(const ResidentArgs& a, bool fast, cudaStream_t s, int* grid_out) {
+int launch_cb_resident(const ResidentArgs& a_in, bool fast, cudaStream_t s, int* grid_out) {
     (void)grid_out;
-    if (fast) return a.ferro ? launch_resident_sized<true, true>(a, s) : launch_resident_sized<true, false>(a, s);
-    return a.ferro ? launch_resident_sized<false, true>(a, s) : launch_resident_sized<false, false>(a, s);
+    ResidentArgs a = a_in;
+    const bool segs = !fast && a.L >= 8 && 64 % a.L == 0;
+    if (segs) {
+        const int seg = a.L / 2;
+        a.seg_lo = 0;
+        a.seg_even = 0;
+        for (int b = 0; b < 32; b += seg) {
+            a.seg_lo |= 1u << b;
+            if (((b / seg) & 1) == 0) a.seg_even |= (seg == 32 ? 0xffffffffu : ((1u << seg) - 1u)) << b;
+        }
+    }
+    if (fast)
+        return a.ferro ? launch_resident_sized<kGatherRows, true>(a, s)
+                       : launch_resident_sized<kGatherRows, false>(a, s);
+    if (segs)
+        return a.ferro ? launch_resident_sized<kGatherSegments, true>(a, s)
+                       : launch_resident_sized<kGatherSegments, false>(a, s);
+    return a.ferro ? launch_resident_sized<kGatherGeneric, true>(a, s)
+                   : launch_resident_sized<kGatherGeneric, false>(a, s);
 }
 
 }  // namespace ptmh

@@ -244,14 +244,15 @@ class CheckerboardEngine(_Base):
         if getattr(self, "_s2r2", None) is None:
             self._s2r2 = torch.empty((2, self.R), dtype=torch.int64, device=self.dev)
             self._r2s2 = torch.empty((2, self.R), dtype=torch.int32, device=self.dev)
+            self._slot_stats = torch.empty((2, self.R, 2), dtype=torch.int64, device=self.dev)
         self._s2r2[0].copy_(self.slot_to_row)
         self._r2s2[0].copy_(self.row_to_slot)
         out = ctypes.c_int(0)
         ncols = obs_e.shape[1] if obs_e is not None else 0
         _lib.call("ptmh_cb_run_resident", _P(self.packed), self.R, self.L, _P(self._s2r2),
                   _P(self._r2s2), 0, _P(self.thr), self.always, self.seed, self.J, self.B,
-                  _P(self.betas), _P(self.stats), _P(self.counters), _P(obs_e), _P(obs_m), ncols,
-                  first_sweep, n_sweeps, total_sweeps, swap_every, record_every,
+                  _P(self.betas), _P(self.stats), _P(self._slot_stats), _P(self.counters), _P(obs_e),
+                  _P(obs_m), ncols, first_sweep, n_sweeps, total_sweeps, swap_every, record_every,
                   ctypes.byref(out), self._s())
         self.slot_to_row.copy_(self._s2r2[out.value])
         self.row_to_slot.copy_(self._r2s2[out.value])

@@ -171,7 +171,14 @@ def test_one_lattice_matches_oracle_at_1024(mods):
 @pytest.mark.parametrize("L,R,sweeps,every,seed,J,B,rec_every", [
     (64, 6, 20, 2, 42, 1.0, 0.0, 1),
     (64, 37, 15, 1, 8, 1.0, 0.0, 1),    # odd R, exchange every sweep
-    (32, 8, 30, 1, 3, 1.0, 0.0, 3),     # generic gather (L % 64 != 0)
+    (32, 8, 30, 1, 3, 1.0, 0.0, 3),     # segment gather (L = 32: two rows per word)
+    (16, 5, 40, 1, 12, 1.0, 0.0, 1),    # segment gather, 4 rows per word
+    (8, 9, 40, 2, 13, 1.0, 0.0, 2),     # segment gather, one word per colour
+    (16, 6, 20, 1, 14, 1.0, 0.3, 1),    # segment gather, field: class plan
+    (32, 4, 20, 1, 15, -1.0, 0.0, 1),   # segment gather, antiferromagnet
+    (12, 5, 20, 1, 16, 1.0, 0.0, 1),    # generic gather (64 % L != 0)
+    (64, 700, 6, 1, 17, 1.0, 0.0, 2),   # several lattices per CTA
+    (16, 2000, 5, 1, 18, 1.0, 0.0, 1),  # many lattices per CTA, segment gather
     (128, 5, 12, 5, 4, 1.0, 0.1, 2),    # field: class plan
     (256, 3, 6, 2, 9, -1.0, 0.0, 1),    # antiferromagnet
     (2, 7, 50, 3, 5, 1.0, 0.0, 1),
