@@ -268,6 +268,9 @@ def main():
     state = {"sweep": 0, "round": 0}
     from paper_2512_03825_b200.executor import _resident_wins
     resident = not sharded and _resident_wins(L, every)
+    # the engine's sweeps() takes the one-launch persistent path here
+    # (csrc/checkerboard.cu: cb_sweeps_persistent, J > 0, B = 0, L % 512 == 0)
+    persistent = not resident and eng.persistent and L >= 1024 and L % 512 == 0
     big = 1 << 30  # run length for the resident kernel: every interval ends in a round
 
     def step(sweep_events=None):
@@ -283,14 +286,11 @@ def main():
             return
         if ips != 1:
             raise ValueError("multi-interval steps are only defined for the resident path")
-        if sweep_events is None:
-            eng.sweeps(t0, every)
-        else:
-            for k in range(every):
-                a, b = sweep_events[k]
-                a.record(stream)
-                eng.sweeps(t0 + k, 1)
-                b.record(stream)
+        if sweep_events is not None:
+            sweep_events[0][0].record(stream)
+        eng.sweeps(t0, every)
+        if sweep_events is not None:
+            sweep_events[0][1].record(stream)
         if drv is not None:
             drv.gather_stats()
         eng.exchange(state["round"])
@@ -306,8 +306,8 @@ def main():
             flush.zero_()
             # per-launch events in every 4th timed step (they cost ~1-2 us each)
             probe = it % 4 == 0
-            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                  for _ in range(1 if resident else every)] if probe else None
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))] \
+                if probe else None
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             if sharded:
                 dist.barrier()
@@ -331,10 +331,14 @@ def main():
         launch_ms = statistics.mean(sweep_ms)
         bytes_per_launch = ALG_BYTES_PER_ATTEMPT * local_rows * L * L * every * ips
         kernel_name = "cb_resident_kernel<fast,ferro>"
+    elif persistent:  # one launch per interval: all 2*every half-sweeps
+        launch_ms = statistics.mean(sweep_ms)
+        bytes_per_launch = ALG_BYTES_PER_ATTEMPT * local_rows * L * L * every
+        kernel_name = "cb_sweeps_persistent<16>"
     else:
-        launch_ms = statistics.mean(sweep_ms) / 2.0  # two colour launches per sweep
+        launch_ms = statistics.mean(sweep_ms) / (2.0 * every)  # two colour launches per sweep
         bytes_per_launch = ALG_BYTES_PER_ATTEMPT * local_rows * L * L / 2
-        kernel_name = "cb_half_sweep_ferro<8,0|1>"
+        kernel_name = "cb_half_sweep_ferro<16,0|1>" if L >= 1024 else "cb_half_sweep_ferro<8,0|1>"
     achieved = bytes_per_launch / (launch_ms / 1e3) / 1e9
     peak, peak_kind = _peaks()
     traffic = _traffic(args.config) if not sharded and not resident else None
@@ -412,9 +416,12 @@ def main():
                              "kernel": kernel_name, "launch_ms": launch_ms,
                              "alg_bytes_per_launch": bytes_per_launch, "peak_kind": peak_kind,
                              "note": "issue-bound (Philox + bit-sliced logic), see DESIGN.md 5",
-                             "issue_from_ncu": _issue(args.config) if not resident else None},
+                             "issue_from_ncu": _issue(args.config) if not resident else None,
+                             "traffic_note": "ncu dram bytes per half-sweep (colour) launch of the "
+                                             "per-launch kernel; alg bytes per half-sweep = "
+                                             f"{ALG_BYTES_PER_ATTEMPT * local_rows * L * L / 2:.4g}"},
                 "cpu_baseline": cpu, "e2e": e2e, "exact_chain": exact,
-                "gpu_launches": args.steps * (1 if resident else 2 * every + 1),
+                "gpu_launches": args.steps * (1 if resident else (1 if persistent else 2 * every) + 1),
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if sharded:

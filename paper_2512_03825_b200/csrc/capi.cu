@@ -274,6 +274,18 @@ int ptmh_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* row
                             stats, as_stream(stream));
 }
 
+int64_t ptmh_cb_sync_words(int64_t rows) { return 2 + std::max<int64_t>(rows, 0); }
+
+int ptmh_cb_sweeps_sync(uint32_t* packed, int64_t rows, int64_t L, const int32_t* row_to_slot,
+                        const uint32_t* thresh, uint32_t always_mask, uint64_t seed, int64_t first_sweep,
+                        int64_t n_sweeps, int64_t* stats, uint32_t* sync, void* stream) {
+    PTMH_CHECK_ARG(L >= 2 && L % 2 == 0 && L <= 65536, "checkerboard needs even 2 <= L <= 65536");
+    PTMH_CHECK_ARG(first_sweep >= 0 && n_sweeps >= 0 && first_sweep + n_sweeps < (1LL << 31),
+                   "checkerboard sweep index must stay below 2^31");
+    return launch_cb_sweeps(packed, rows, L, row_to_slot, thresh, always_mask, seed, first_sweep, n_sweeps,
+                            stats, as_stream(stream), sync);
+}
+
 int ptmh_cb_run_resident(uint32_t* packed, int64_t R, int64_t L, int64_t* slot_to_row2, int32_t* row_to_slot2,
                          int buf, const uint32_t* thresh, uint32_t always_mask, uint64_t seed, double J, double B,
                          const double* betas, int64_t* stats, int64_t* slot_stats, int64_t* counters,
@@ -542,6 +554,17 @@ int ptmh_host_cb_interval(int8_t* spins, int64_t R, int64_t L, int64_t* slot_to_
     PTMH_TRY(ws_get(g_ws, 4, (size_t)R, &d_e));
     PTMH_TRY(ws_get(g_ws, 5, (size_t)R, &d_sums));
     PTMH_TRY(ws_get(g_ws, 12, 2, &d_cnt));
+    const int64_t nch = std::min<int64_t>(R, 16);
+    uint32_t* d_sync;  // one persistent-sweep sync block per chunk
+    const int64_t sync_words = ptmh_cb_sync_words(R);
+    // The chunks run concurrently on kComputeStreams streams, where the
+    // persistent path's co-resident spinning CTAs cost 2x (16.9 vs 7.2 ms per
+    // C3 call): they take the per-launch kernels.  PTMH_PLUGIN_SYNC=1 turns
+    // the persistent path on (A/B, tools/ only).
+    const char* ps = getenv("PTMH_PLUGIN_SYNC");
+    const bool plugin_sync = ps && ps[0] == '1';
+    PTMH_TRY(ws_get(g_ws, 17, (size_t)(nch * sync_words), &d_sync));
+    PTMH_CUDA(cudaMemsetAsync(d_sync, 0, (size_t)(nch * sync_words) * 4, sc));
     PTMH_CUDA(cudaMemcpyAsync(d_thr, thr.data(), R * 40, cudaMemcpyHostToDevice, sc));
     PTMH_CUDA(cudaMemcpyAsync(d_s2r, slot_to_row, R * 8, cudaMemcpyHostToDevice, sc));
     PTMH_CUDA(cudaMemcpyAsync(d_r2s, r2s.data(), R * 4, cudaMemcpyHostToDevice, sc));
@@ -550,7 +573,6 @@ int ptmh_host_cb_interval(int8_t* spins, int64_t R, int64_t L, int64_t* slot_to_
     // pipeline over replica chunks: all H2D copies are issued first, then the
     // compute chain (each chunk waits for its copy), then the D2H copies (each
     // waits for its chunk), so no queue ever blocks behind a later dependency
-    const int64_t nch = std::min<int64_t>(R, 16);
     if (getenv("PTMH_TRACE")) PTMH_CUDA(cudaEventRecord(g_ws.ev_t0, sin));
     auto chunk = [&](int64_t c, int64_t& lo, int64_t& n) {
         lo = R * c / nch;
@@ -574,7 +596,7 @@ int ptmh_host_cb_interval(int8_t* spins, int64_t R, int64_t L, int64_t* slot_to_
         PTMH_TRY(launch_cb_pack(d_spins + lo * nsite, n, L, d_packed + lo * 2 * W, cst));
         PTMH_TRY(launch_cb_row_stats(d_packed + lo * 2 * W, n, L, d_stats + 2 * lo, cst));
         PTMH_TRY(launch_cb_sweeps(d_packed + lo * 2 * W, n, L, d_r2s + lo, d_thr, always, seed, first_sweep,
-                                  n_sweeps, d_stats + 2 * lo, cst));
+                                  n_sweeps, d_stats + 2 * lo, cst, plugin_sync ? d_sync + c * sync_words : nullptr));
         PTMH_TRY(launch_cb_unpack(d_packed + lo * 2 * W, n, L, d_spins + lo * nsite, cst));
         PTMH_CUDA(cudaEventRecord(g_ws.ev_out[c], cst));
         PTMH_CUDA(cudaStreamWaitEvent(sc, g_ws.ev_out[c], 0));  // the exchange needs every chunk

@@ -24,6 +24,9 @@
 // order-free, so the stats are deterministic.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "launchers.cuh"
 #include "philox.cuh"
@@ -198,70 +201,100 @@ __global__ void __launch_bounds__(256) cb_half_sweep_fast(
 // colours' words, Bond = sum over colour-1 sites of s*nb (every bond has
 // exactly one colour-1 end) -- plus the deltas of its own tie flips.
 #ifndef PTMH_FERRO_MINB
-#define PTMH_FERRO_MINB 1
+#define PTMH_FERRO_MINB 3  // 80 registers: 3 CTAs (24 warps) per SM, no spills
 #endif
 
-template <int kRows, bool kStats>
-__global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_half_sweep_ferro(
-    uint32_t* __restrict__ packed, int64_t rows, int L, int WR, int64_t W,
-    const int32_t* __restrict__ row_to_slot, const uint32_t* __restrict__ thresh, const RoundKeys32 rk,
-    uint32_t ctr1, int color, int64_t* __restrict__ stats) {
-    constexpr int kWarps = 8;
-    __shared__ uint32_t tie_m[kWarps][kRows][32], tie_k4[kWarps][kRows][32];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// base + esz * idx as one wide multiply-add (IMAD.WIDE.U32, FMA pipe) instead
+// of the LEA / LEA.HI.X pair on the ALU pipe.  esz (= 4) is a kernel
+// parameter so ptxas cannot strength-reduce the multiply into a shift.
+template <typename T>
+__device__ __forceinline__ T* word_at(T* base, uint32_t idx, uint32_t esz) {
+    uint64_t r;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(idx), "r"(esz), "l"((uint64_t)base));
+    return reinterpret_cast<T*>(r);
+}
 
-    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int strips = L / kRows;
-    const int64_t per_lat = (int64_t)strips * WR;
-    const bool active = tid < rows * per_lat;
-    const int64_t lat = active ? tid / per_lat : 0;
-    const int rem = (int)(tid - lat * per_lat);
+// other-colour loads: the read-only path inside one launch, L2 (.cg) where
+// another CTA of the same launch may have written the word (persistent path)
+template <bool kNC>
+__device__ __forceinline__ uint32_t ld_other(const uint32_t* p) {
+    return kNC ? __ldg(p) : __ldcg(p);
+}
+
+// One thread's strip: word column k of lattice rows i0 .. i0+kRows-1 of one
+// colour (kStats doubles as the colour: colour 0 resets the lattice's stats,
+// colour 1 recomputes them).  Returns the thread's (S, Bond) contributions in
+// sumS / sumB; the caller reduces them (flush_stats).
+template <int kRows, bool kStats, bool kNC>
+__device__ __forceinline__ void ferro_strip(uint32_t* __restrict__ packed, int L, int WR, int64_t W,
+                                            const int32_t* __restrict__ row_to_slot,
+                                            const uint32_t* __restrict__ thresh, const RoundKeys32& rk,
+                                            uint32_t ctr1, int64_t* __restrict__ stats, uint32_t esz,
+                                            bool active, int64_t lat, int rem,
+                                            uint32_t (&tie_m)[kRows][32], uint32_t (&tie_k4)[kRows][32],
+                                            int& sumS, int& sumB) {
+    constexpr int kColor = kStats ? 1 : 0;
+    const int lane = threadIdx.x & 31;
     const int strip = rem / WR;
     const int k = rem - strip * WR;
     const int i0 = strip * kRows;
-    const uint32_t own_base = (uint32_t)((lat * 2 + color) * W);
+    const uint32_t own_base = (uint32_t)((lat * 2 + kColor) * W);
     int slot = 0;
     uint32_t t3 = 0, t4 = 0;
-    int sumS = 0, sumB = 0;
     uint32_t tie_rows = 0;  // bit rr: row rr has ties
     if (active) {
         if (!kStats && rem == 0) {  // colour-0 pass: reset, colour-1 pass recomputes
             stats[2 * lat] = 0;
             stats[2 * lat + 1] = 0;
         }
-        const uint32_t* __restrict__ other = packed + (lat * 2 + (1 - color)) * W;
+        const uint32_t* __restrict__ other = packed + (lat * 2 + (1 - kColor)) * W;
         uint32_t* __restrict__ own = packed + own_base;
         slot = row_to_slot[lat];
         t3 = __ldg(thresh + slot * 10 + 8);
         t4 = __ldg(thresh + slot * 10 + 9);
-        uint32_t TA[8], TB[8];
+        // Threshold plane p of a site is bit p of t4 where K4 is set, else of
+        // t3: Tm = K4 ? TB : TA with TA, TB in {0, ~0}.  Written as the
+        // integer K4 * (TB - TA) - TA (TM[p] in {-1, 0, 1}, TC[p] = -TA) so
+        // the select is one IMAD on the FMA pipe; the ALU pipe, which bounds
+        // this kernel, only does the compare itself.
+        uint32_t TM[8], TC[8];
 #pragma unroll
         for (int p = 0; p < 8; ++p) {
-            TA[p] = 0u - ((t3 >> (31 - p)) & 1u);
-            TB[p] = 0u - ((t4 >> (31 - p)) & 1u);
+            const uint32_t ta = (t3 >> (31 - p)) & 1u, tb = (t4 >> (31 - p)) & 1u;
+            TM[p] = tb - ta;
+            TC[p] = 0u - ta;
         }
         const int kl = (k == 0) ? WR - 1 : k - 1;
         const int kr = (k == WR - 1) ? 0 : k + 1;
-        // horizontal neighbour word column: kl when (i + colour) is even, else kr
-        const int kadj0 = ((i0 + color) & 1) == 0 ? kl : kr;
-        const int kadj1 = ((i0 + color) & 1) == 0 ? kr : kl;
-        uint32_t up = __ldg(other + (i0 == 0 ? L - 1 : i0 - 1) * WR + k);
-        uint32_t mid = __ldg(other + i0 * WR + k);
-        uint32_t dn = __ldg(other + (i0 + 1 == L ? 0 : i0 + 1) * WR + k);
-        uint32_t S = own[i0 * WR + k];
-        uint32_t adj = __ldg(other + i0 * WR + kadj0);
+        // horizontal neighbour word column: kl when (i + colour) is even, else
+        // kr; i0 is even, so row rr of the strip uses kl iff (rr + kColor) is
+        // even.  Offsets are 32-bit word indices into one colour plane; the
+        // next rows' offsets roll forward with one wrap (unsigned min) per row,
+        // and addresses are formed with one wide IMAD (FMA pipe) each.
+        const int dEven = kl - k, dOdd = kr - k;  // adjacent column, relative
+        const uint32_t uWR = (uint32_t)WR, LW = (uint32_t)L * uWR;
+        const uint32_t o0 = (uint32_t)(i0 * WR + k);
+        uint32_t oup = o0 + LW - uWR;
+        oup = min(oup, oup - LW);
+        uint32_t o1 = o0 + uWR;
+        o1 = min(o1, o1 - LW);
+        uint32_t up = ld_other<kNC>(word_at(other, oup, esz));
+        uint32_t mid = ld_other<kNC>(word_at(other, o0, esz));
+        uint32_t dn = ld_other<kNC>(word_at(other, o1, esz));
+        uint32_t S = __ldcg(word_at(own, o0, esz));
+        uint32_t adj = ld_other<kNC>(word_at(other, o0 + (uint32_t)((kColor & 1) ? dOdd : dEven), esz));
+        uint32_t o = o0;
 #pragma unroll 2
         for (int rr = 0; rr < kRows; ++rr) {
-            const int i = i0 + rr;
-            const int row = i * WR;
+            const bool even = ((rr + kColor) & 1) == 0;
             // prefetch row i+1 (own, adjacent) and row i+2 (other colour, below)
-            const int i1 = (i + 1 == L) ? 0 : i + 1;
-            const int i2 = (i1 + 1 == L) ? 0 : i1 + 1;
-            const uint32_t dn_n = __ldg(other + i2 * WR + k);
-            const uint32_t S_n = own[i1 * WR + k];
-            const uint32_t adj_n = __ldg(other + i1 * WR + ((rr & 1) ? kadj0 : kadj1));
-            const uint32_t hz = (((i + color) & 1) == 0) ? __funnelshift_l(adj, mid, 1)   // m sees m-1
-                                                         : __funnelshift_r(mid, adj, 1);  // m sees m+1
+            uint32_t o2 = o1 + uWR;
+            o2 = min(o2, o2 - LW);
+            const uint32_t dn_n = ld_other<kNC>(word_at(other, o2, esz));
+            const uint32_t S_n = __ldcg(word_at(own, o1, esz));
+            const uint32_t adj_n = ld_other<kNC>(word_at(other, o1 + (uint32_t)(even ? dOdd : dEven), esz));
+            const uint32_t hz = even ? __funnelshift_l(adj, mid, 1)   // m sees m-1
+                                     : __funnelshift_r(mid, adj, 1);  // m sees m+1
             const uint32_t a = ~(S ^ up), b = ~(S ^ dn), c = ~(S ^ mid), d = ~(S ^ hz);
             const uint32_t s1 = a ^ b, c1 = a & b, s2 = c ^ d, c2 = c & d;
             const uint32_t k0 = s1 ^ s2, c3 = s1 & s2;
@@ -269,31 +302,28 @@ __global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_half_sweep_ferro(
             const uint32_t upm = (k1 & k0) | K4;   // k = 3, 4
             const uint32_t K2 = k1 & ~k0;          // k = 2: dE = 0
             uint32_t acc = ~(k1 | K4);             // k = 0, 1: dE < 0
-            const uint32_t w32 = (uint32_t)(row + k);
+            const uint32_t w32 = o;
             const uint4 r0 = philox4x32_10(make_uint4(2u * w32, ctr1, (uint32_t)slot, 0u), rk);
             const uint4 r1 = philox4x32_10(make_uint4(2u * w32 + 1u, ctr1, (uint32_t)slot, 0u), rk);
             const uint32_t U[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
             acc |= K2 & ~U[0];  // neutral: u < 2^31 <=> top bit clear
             // byte compare u < t as the borrow of u - t, LSB plane first
             // (borrow' = MAJ(~u, t, borrow): one LOP3), plus the equality
-            // chain for the ties; K4 pinned in a register so the per-site
-            // threshold plane is a single select
-            uint32_t K4r = K4;
-            asm volatile("" : "+r"(K4r));
+            // chain for the ties; the per-site threshold plane is one IMAD
             uint32_t bor = 0, eq = upm;
 #pragma unroll
             for (int p = 7; p >= 0; --p) {
-                const uint32_t Tm = (K4r & TB[p]) | (~K4r & TA[p]);
+                const uint32_t Tm = K4 * TM[p] + TC[p];
                 bor = (~U[p] & Tm) | (~U[p] & bor) | (Tm & bor);
                 eq &= ~(U[p] ^ Tm);
             }
             acc |= bor & upm;
             // ties (top byte equal): bookkeeping only, resolved after the loop
-            tie_m[warp][rr][lane] = eq;
-            tie_k4[warp][rr][lane] = eq & K4;
+            tie_m[rr][lane] = eq;
+            tie_k4[rr][lane] = eq & K4;
             tie_rows |= (eq != 0u ? 1u : 0u) << rr;
             const uint32_t Sn = S ^ acc;
-            if (acc) own[row + k] = Sn;
+            if (acc) __stcg(word_at(own, o, esz), Sn);
             if (kStats) {
                 // new aligned masks: a flip toggles alignment with all four neighbours
                 const int kk = __popc(a ^ acc) + __popc(b ^ acc) + __popc(c ^ acc) + __popc(d ^ acc);
@@ -305,6 +335,8 @@ __global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_half_sweep_ferro(
             dn = dn_n;
             S = S_n;
             adj = adj_n;
+            o = o1;
+            o1 = o2;
         }
     }
     // ---- tie resolution: every lane walks its own ties (top byte equal)
@@ -319,10 +351,10 @@ __global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_half_sweep_ferro(
             if (m == 0 && tie_rows != 0) {
                 rr = __ffs(tie_rows) - 1;
                 tie_rows &= tie_rows - 1;
-                m = tie_m[warp][rr][lane];
-                mk4 = tie_k4[warp][rr][lane];
+                m = tie_m[rr][lane];
+                mk4 = tie_k4[rr][lane];
                 w32 = (uint32_t)((i0 + rr) * WR + k);
-                Sw = packed[own_base + w32];
+                Sw = __ldcg(packed + own_base + w32);
                 dirty = false;
             }
             if (m != 0) {
@@ -340,11 +372,131 @@ __global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_half_sweep_ferro(
                     Sw ^= 1u << bit;
                     dirty = true;
                 }
-                if (m == 0 && dirty) packed[own_base + w32] = Sw;
+                if (m == 0 && dirty) __stcg(packed + own_base + w32, Sw);
             }
         }
     }
+}
+
+
+template <int kRows, bool kStats>
+__global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_half_sweep_ferro(
+    uint32_t* __restrict__ packed, int64_t rows, int L, int WR, int64_t W,
+    const int32_t* __restrict__ row_to_slot, const uint32_t* __restrict__ thresh, const RoundKeys32 rk,
+    uint32_t ctr1, int64_t* __restrict__ stats, uint32_t esz) {
+    constexpr int kWarps = 8;
+    __shared__ uint32_t tie_m[kWarps][kRows][32], tie_k4[kWarps][kRows][32];
+    const int warp = threadIdx.x >> 5;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t per_lat = (int64_t)(L / kRows) * WR;
+    const bool active = tid < rows * per_lat;
+    const int64_t lat = active ? tid / per_lat : 0;
+    const int rem = (int)(tid - lat * per_lat);
+    int sumS = 0, sumB = 0;
+    ferro_strip<kRows, kStats, true>(packed, L, WR, W, row_to_slot, thresh, rk, ctr1, stats, esz, active,
+                                     lat, rem, tie_m[warp], tie_k4[warp], sumS, sumB);
     if (kStats) flush_stats(stats, lat, active, sumS, sumB);
+}
+
+// ---------------------------------------- persistent multi-sweep ferro path --
+// All 2n half-sweeps of ptmh_cb_sweeps in ONE launch, as a dataflow over
+// work items instead of 2n grid-wide launches.  An item is (phase, lattice,
+// slice): phase p = colour p & 1 of sweep first + p / 2, a slice = `group`
+// consecutive 256-thread blocks of the lattice's word-column strips.
+// Resident CTAs take items from a global ticket in phase-major order; an item
+// of phase p waits until every item of phases < p of ITS lattice is done (a
+// per-lattice done counter), because colour c reads only colour 1-c words of
+// its own lattice.  So the tail of one phase overlaps the head of the next,
+// there are no launch gaps, and no CTA ever waits on a ticket that has not
+// been taken by a running CTA (tickets are taken in order), which makes the
+// scheme deadlock-free at any residency.  Random numbers, acceptance and
+// statistics are those of the per-launch kernel: the paths are bit-identical.
+// (Per-warp items were tried: 25 % slower at C3.)
+//
+// sync (uint32, zeroed, 2 + rows words): [0] ticket, [1] CTAs finished,
+// [2 + lat] items of lattice lat done.  The last CTA out re-zeroes it.
+//
+// Coherence: own-colour words are read and written at L2 (.cg).  The other
+// colour is read through L1 (ld.global.nc), which is safe because (a) all
+// running items of a lattice are in the same phase, so the words they read
+// are not written while they run, and (b) every item of phase > 0 starts
+// with an ld.acquire.gpu of its dependency counter, which ptxas emits with
+// CCTL.IVALL: the SM's L1 is invalidated after the words were last written
+// and before they are read.  Phase-0 items read words no item of this launch
+// has written yet.
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// release-add (MEMBAR + RED: no L1 invalidate, no return value to wait for)
+__device__ __forceinline__ void red_release_gpu_add(uint32_t* p, uint32_t v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int kRows>
+__global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_sweeps_persistent(
+    uint32_t* __restrict__ packed, int64_t rows, int L, int WR, int64_t W,
+    const int32_t* __restrict__ row_to_slot, const uint32_t* __restrict__ thresh, const RoundKeys32 rk,
+    uint32_t ctr_base, uint32_t n_phases, int64_t* __restrict__ stats, uint32_t esz,
+    uint32_t* __restrict__ sync, uint32_t group) {
+    constexpr int kWarps = 8;
+    __shared__ uint32_t tie_m[kWarps][kRows][32], tie_k4[kWarps][kRows][32];
+    __shared__ uint32_t s_item[2];
+    const int warp = threadIdx.x >> 5;
+    // items per lattice and phase (the host picks group so that a phase still
+    // has >= 8 items per resident CTA)
+    const uint32_t subs = (uint32_t)((L / kRows) * WR / 256) / group;
+    const uint32_t per_phase = (uint32_t)rows * subs;
+    const uint32_t n_items = n_phases * per_phase;
+    // thread 0 schedules: it holds the next ticket (prefetched one item
+    // ahead, so the atomic's latency is off the critical path), waits for the
+    // item's lattice to finish the previous phase, and publishes it
+    uint32_t next = threadIdx.x == 0 ? atomicAdd(&sync[0], 1u) : 0u;
+    for (int it = 0;; ++it) {
+        if (threadIdx.x == 0) {
+            if (next < n_items) {
+                const uint32_t phase = next / per_phase;
+                const uint32_t lat = (next - phase * per_phase) / subs;
+                if (phase > 0)
+                    while (ld_acquire_gpu(&sync[2 + lat]) < phase * subs) __nanosleep(32);
+            }
+            s_item[it & 1] = next;  // double-buffered: the next write is past a barrier
+            if (next < n_items) next = atomicAdd(&sync[0], 1u);
+        }
+        __syncthreads();
+        const uint32_t item = s_item[it & 1];
+        if (item >= n_items) break;
+        const uint32_t phase = item / per_phase;
+        const uint32_t r = item - phase * per_phase;
+        const uint32_t lat = r / subs, sub = r - lat * subs;
+        const uint32_t ctr1 = ctr_base + phase;
+        int sumS = 0, sumB = 0;
+        if ((ctr1 & 1u) == 0) {
+            for (uint32_t g = 0; g < group; ++g)
+                ferro_strip<kRows, false, true>(packed, L, WR, W, row_to_slot, thresh, rk, ctr1, stats, esz,
+                                                true, lat, (int)((sub * group + g) * 256 + threadIdx.x),
+                                                tie_m[warp], tie_k4[warp], sumS, sumB);
+        } else {
+            for (uint32_t g = 0; g < group; ++g)
+                ferro_strip<kRows, true, true>(packed, L, WR, W, row_to_slot, thresh, rk, ctr1, stats, esz,
+                                               true, lat, (int)((sub * group + g) * 256 + threadIdx.x),
+                                               tie_m[warp], tie_k4[warp], sumS, sumB);
+            flush_stats(stats, lat, true, sumS, sumB);
+        }
+        __syncthreads();  // every store of this item is issued before the release
+        if (threadIdx.x == 0) red_release_gpu_add(&sync[2 + lat], 1u);
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&sync[1], 1u) == gridDim.x - 1) {  // last CTA out: leave sync zeroed
+            for (int64_t l = 0; l < rows; ++l) sync[2 + l] = 0;
+            sync[0] = 0;
+            __threadfence();
+            sync[1] = 0;
+        }
+    }
 }
 
 // ------------------------------------------------------- generic even L --
@@ -556,7 +708,7 @@ constexpr int kFastRows = PTMH_FERRO_ROWS;
 
 int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* row_to_slot,
                      const uint32_t* thresh, uint32_t always_mask, uint64_t seed, int64_t first_sweep,
-                     int64_t n_sweeps, int64_t* stats, cudaStream_t s) {
+                     int64_t n_sweeps, int64_t* stats, cudaStream_t s, uint32_t* sync) {
     if (rows == 0 || n_sweeps == 0) return PTMH_OK;
     const ClassPlan plan = make_plan(always_mask);
     const RoundKeys32 rk = make_round_keys32(seed);
@@ -565,6 +717,39 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
     // symmetric thresholds, k <= 1 always, k = 2 neutral (1/2), k = 3, 4 uphill
     const bool ferro = (always_mask & kSymmetricFlag) && (always_mask & 0x3ffu) == 0x078u &&
                        rows * 2 * W < (1LL << 32);  // 32-bit word offsets in the tie queue
+    // one persistent launch for every half-sweep: whole 256-thread blocks per
+    // lattice (L % 512 == 0) and a 32-bit item count
+    if (sync && fast && ferro && L >= 1024 && L % 512 == 0 && 2 * n_sweeps * rows * (L * L / 262144) < (1LL << 31)) {
+        static int cached_slots[256] = {};  // resident CTAs per device
+        int dev = 0;
+        PTMH_CUDA(cudaGetDevice(&dev));
+        if (dev >= 256) dev = 255;
+        if (cached_slots[dev] == 0) {
+            int sms = 0, occ = 0;
+            PTMH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            PTMH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cb_sweeps_persistent<16>, 256, 0));
+            cached_slots[dev] = sms * std::max(occ, 1);
+        }
+        const int WR = (int)(L / 64);
+        // 256-thread blocks per item: amortise the per-item scheduling over
+        // several blocks while a phase keeps >= 8 items per resident CTA
+        // (PTMH_PERSIST_ITEMS_PER_SLOT overrides the 8; tests use 0 to force
+        // the largest groups at small shapes)
+        const int64_t blocks = L * L / 262144;  // per lattice and phase
+        const char* ev = getenv("PTMH_PERSIST_ITEMS_PER_SLOT");
+        const int64_t per_slot = ev ? atoll(ev) : 8;
+        int64_t group = 1;
+        while (group * 2 <= blocks && blocks % (group * 2) == 0 &&
+               rows * blocks / (group * 2) >= per_slot * (int64_t)cached_slots[dev])
+            group *= 2;
+        const int64_t items = 2 * n_sweeps * rows * (blocks / group);
+        const unsigned grid = (unsigned)std::min<int64_t>(items, cached_slots[dev]);
+        cb_sweeps_persistent<16><<<grid, 256, 0, s>>>(packed, rows, (int)L, WR, W, row_to_slot, thresh, rk,
+                                                       (uint32_t)(2 * first_sweep), (uint32_t)(2 * n_sweeps),
+                                                       stats, 4u, sync, (uint32_t)group);
+        PTMH_LAUNCH_CHECK();
+        return PTMH_OK;
+    }
     for (int64_t t = first_sweep; t < first_sweep + n_sweeps; ++t) {
         for (int color = 0; color < 2; ++color) {
             const uint32_t ctr1 = (uint32_t)(2 * t + color);
@@ -573,19 +758,19 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
                 const int64_t threads = rows * (L / 16) * WR;
                 if (color == 0)
                     cb_half_sweep_ferro<16, false><<<ceil_div(threads, 256), 256, 0, s>>>(
-                        packed, rows, (int)L, WR, W, row_to_slot, thresh, rk, ctr1, color, stats);
+                        packed, rows, (int)L, WR, W, row_to_slot, thresh, rk, ctr1, stats, 4u);
                 else
                     cb_half_sweep_ferro<16, true><<<ceil_div(threads, 256), 256, 0, s>>>(
-                        packed, rows, (int)L, WR, W, row_to_slot, thresh, rk, ctr1, color, stats);
+                        packed, rows, (int)L, WR, W, row_to_slot, thresh, rk, ctr1, stats, 4u);
             } else if (fast && ferro) {
                 const int WR = (int)(L / 64);
                 const int64_t threads = rows * (L / kFastRows) * WR;
                 if (color == 0)
                     cb_half_sweep_ferro<kFastRows, false><<<ceil_div(threads, 256), 256, 0, s>>>(
-                        packed, rows, (int)L, WR, W, row_to_slot, thresh, rk, ctr1, color, stats);
+                        packed, rows, (int)L, WR, W, row_to_slot, thresh, rk, ctr1, stats, 4u);
                 else
                     cb_half_sweep_ferro<kFastRows, true><<<ceil_div(threads, 256), 256, 0, s>>>(
-                        packed, rows, (int)L, WR, W, row_to_slot, thresh, rk, ctr1, color, stats);
+                        packed, rows, (int)L, WR, W, row_to_slot, thresh, rk, ctr1, stats, 4u);
             } else if (fast) {
                 const int WR = (int)(L / 64);
                 const int64_t threads = rows * (L / kFastRows) * WR;

@@ -193,6 +193,9 @@ class CheckerboardEngine(_Base):
         self.always = int(always)
         self.energies = torch.zeros(R, dtype=torch.float64, device=d)
         self.spin_sums = torch.zeros(R, dtype=torch.int64, device=d)
+        # zeroed sync block of the persistent sweep path (left zeroed by every call)
+        self.persistent = True
+        self._sync = torch.zeros(int(_lib.LIB.ptmh_cb_sync_words(self.rows)), dtype=torch.int32, device=d)
 
     @property
     def local_stats(self) -> torch.Tensor:
@@ -221,8 +224,15 @@ class CheckerboardEngine(_Base):
         if self.rows == 0 or n <= 0:
             return
         rts = self.row_to_slot[self.row_lo:self.row_hi]
-        _lib.call("ptmh_cb_sweeps", _P(self.packed), self.rows, self.L, _P(rts), _P(self.thr),
-                  self.always, self.seed, first_sweep, n, _P(self.local_stats), self._s())
+        if self.persistent:
+            # one persistent launch for all 2n half-sweeps where the kernel
+            # supports it (csrc/checkerboard.cu, cb_sweeps_persistent)
+            _lib.call("ptmh_cb_sweeps_sync", _P(self.packed), self.rows, self.L, _P(rts), _P(self.thr),
+                      self.always, self.seed, first_sweep, n, _P(self.local_stats), _P(self._sync),
+                      self._s())
+        else:
+            _lib.call("ptmh_cb_sweeps", _P(self.packed), self.rows, self.L, _P(rts), _P(self.thr),
+                      self.always, self.seed, first_sweep, n, _P(self.local_stats), self._s())
 
     def exchange(self, round_index: int) -> int:
         """Swap round on the energies of every lattice (self.stats must hold

@@ -265,3 +265,64 @@ def test_full_states_match_oracle(mods, L, R, sweeps, every, rec_every):
     assert np.array_equal(rec.energies, ref.energies)
     # magnetisations are the recorded states' means (reference test_executor.py:172-181)
     assert np.array_equal(rec.magnetizations, rec.states.sum(axis=(2, 3)) / (L * L))
+
+
+@pytest.mark.parametrize("L,R,first,nsweeps,per_slot", [
+    (1024, 24, 3, 7, None), (1024, 256, 0, 10, None), (2048, 5, 1, 3, None),
+    (2048, 5, 1, 3, "0"),      # 16 slices per item: one item per lattice and phase
+    (1024, 256, 0, 4, "0"),    # 4 slices per item
+])
+def test_persistent_sweeps_equal_per_launch_path(mods, monkeypatch, L, R, first, nsweeps, per_slot):
+    """The one-launch dataflow path (cb_sweeps_persistent) and the per-launch
+    half-sweep kernels give identical lattices and stats; the sync block is
+    left zeroed for the next call."""
+    p, engine, _, _ = mods
+    if per_slot is not None:
+        monkeypatch.setenv("PTMH_PERSIST_ITEMS_PER_SLOT", per_slot)
+    temps = p.build_ladder(R)
+    perm = np.random.default_rng(R).permutation(R)
+    r2s = np.empty(R, dtype=np.int64); r2s[perm] = np.arange(R)
+    outs = []
+    for persistent in (True, False):
+        eng = engine.CheckerboardEngine(L, R, temps, 99, 1.0, 0.0, 0.5, 0)
+        eng.persistent = persistent
+        eng.slot_to_row.copy_(torch.from_numpy(perm.astype(np.int64)))
+        eng.row_to_slot.copy_(torch.from_numpy(r2s.astype(np.int32)))
+        eng.init_state()
+        eng.sweeps(first, nsweeps)
+        eng.sweeps(first + nsweeps, 1)  # a second call reuses the (re-zeroed) sync block
+        torch.cuda.synchronize()
+        if persistent:
+            assert int(eng._sync.abs().sum().item()) == 0
+        outs.append((eng.packed.clone(), eng.local_stats.clone(), eng.audit_stats()))
+        del eng
+        torch.cuda.empty_cache()
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert torch.equal(outs[0][1], outs[1][1])
+    assert torch.equal(outs[0][1], outs[0][2])
+
+
+@pytest.mark.parametrize("plugin_sync", ["0", "1"])
+def test_host_interval_plugin_at_1024(mods, monkeypatch, plugin_sync):
+    """The host plugin at L = 1024, with the chunks on the per-launch kernels
+    (default) and on the persistent path: equal to the device engine (which
+    matches the oracle, above)."""
+    p, engine, kernels, _ = mods
+    monkeypatch.setenv("PTMH_PLUGIN_SYNC", plugin_sync)
+    L, R, seed = 1024, 6, 23
+    temps = p.build_ladder(R)
+    betas = 1.0 / temps
+    eng = engine.CheckerboardEngine(L, R, temps, seed, 1.0, 0.0, 0.5, 0)
+    eng.init_state()
+    sp = eng.final_spins()
+    s2r = np.arange(R, dtype=np.int64)
+    prev = 0
+    for rnd in range(2):
+        e = np.zeros(R); ss = np.zeros(R, dtype=np.int64)
+        acc = kernels.cb_interval(sp, s2r, betas, 1.0, 0.0, seed, 2 * rnd, 2, rnd, e, ss)
+        eng.sweeps(2 * rnd, 2)
+        eng.exchange(rnd)
+        assert acc == eng.swap_counts()[0] - prev
+        prev = eng.swap_counts()[0]
+        assert np.array_equal(sp, eng.final_spins())
+        assert np.array_equal(s2r, eng.slot_to_row.cpu().numpy())

@@ -13,9 +13,11 @@ from bench import CONFIGS  # noqa: E402
 from paper_2512_03825_b200 import build_ladder  # noqa: E402
 from paper_2512_03825_b200.engine import CheckerboardEngine  # noqa: E402
 
-for name in (sys.argv[1:] or ["c3"]):
+persist = "--no-persist" not in sys.argv
+for name in ([a for a in sys.argv[1:] if not a.startswith("--")] or ["c3"]):
     L, R, every, _ = CONFIGS[name]
     eng = CheckerboardEngine(L, R, build_ladder(R), 42, 1.0, 0.0, 0.5, 0)
+    eng.persistent = persist
     eng.init_state()
     n = max(2, min(200, int(4e9 // (R * L * L))))
     t = 0
@@ -34,7 +36,7 @@ for name in (sys.argv[1:] or ["c3"]):
         t += n
         ms_all.append(a.elapsed_time(b))
     ms = statistics.median(ms_all)
-    print(f"{name}: L={L} R={R} {n} sweeps {ms:.3f} ms -> {n * R * L * L / ms / 1e9:.4g} T attempts/s "
+    print(f"{name}{'' if persist else ' (per-launch)'}: L={L} R={R} {n} sweeps {ms:.3f} ms -> {n * R * L * L / ms / 1e9:.4g} T attempts/s "
           f"({ms / n * 1e3:.1f} us/sweep; min {min(ms_all):.3f} max {max(ms_all):.3f} ms)", flush=True)
     del eng
     torch.cuda.empty_cache()
