@@ -417,9 +417,10 @@ def main():
                              "alg_bytes_per_launch": bytes_per_launch, "peak_kind": peak_kind,
                              "note": "issue-bound (Philox + bit-sliced logic), see DESIGN.md 5",
                              "issue_from_ncu": _issue(args.config) if not resident else None,
-                             "traffic_note": "ncu dram bytes per half-sweep (colour) launch of the "
-                                             "per-launch kernel; alg bytes per half-sweep = "
-                                             f"{ALG_BYTES_PER_ATTEMPT * local_rows * L * L / 2:.4g}"},
+                             "traffic_note": "ncu dram read+write bytes per launch of the same kernel "
+                                             "(profiles/ncu_sweep_summary.json); below the algorithmic "
+                                             "bytes when the packed state stays in L2 across the "
+                                             "launch's sweeps"},
                 "cpu_baseline": cpu, "e2e": e2e, "exact_chain": exact,
                 "gpu_launches": args.steps * (1 if resident else (1 if persistent else 2 * every) + 1),
                 "clocks": clk.summary()}
