@@ -554,15 +554,18 @@ int ptmh_host_cb_interval(int8_t* spins, int64_t R, int64_t L, int64_t* slot_to_
     PTMH_TRY(ws_get(g_ws, 4, (size_t)R, &d_e));
     PTMH_TRY(ws_get(g_ws, 5, (size_t)R, &d_sums));
     PTMH_TRY(ws_get(g_ws, 12, 2, &d_cnt));
-    const int64_t nch = std::min<int64_t>(R, 16);
+    const char* pc = getenv("PTMH_PLUGIN_CHUNKS");  // A/B, tools/ only
+    const int64_t nch = std::min<int64_t>(R, pc ? std::max(1, std::min(64, atoi(pc))) : 8);  // <= 64 (events); 8: 6.6 ms per C3 call, 4: 7.0, 16: 6.7, 32: 8.3
     uint32_t* d_sync;  // one persistent-sweep sync block per chunk
     const int64_t sync_words = ptmh_cb_sync_words(R);
-    // The chunks run concurrently on kComputeStreams streams, where the
-    // persistent path's co-resident spinning CTAs cost 2x (16.9 vs 7.2 ms per
-    // C3 call): they take the per-launch kernels.  PTMH_PLUGIN_SYNC=1 turns
-    // the persistent path on (A/B, tools/ only).
+    // Chunk compute: where the persistent path applies, every chunk runs on
+    // ONE stream as one persistent launch (it fills the GPU by itself; two
+    // of them side by side cost 2x, 16.9 vs 7.2 ms per C3 call); otherwise
+    // the per-launch kernels of a chunk do not fill the GPU and the chunks run
+    // on kComputeStreams concurrent streams.  PTMH_PLUGIN_SYNC=0 forces the
+    // latter (A/B, tools/ only).
     const char* ps = getenv("PTMH_PLUGIN_SYNC");
-    const bool plugin_sync = ps && ps[0] == '1';
+    const bool plugin_sync = !(ps && ps[0] == '0') && cb_sweeps_persistent_applies(L, always, n_sweeps);
     PTMH_TRY(ws_get(g_ws, 17, (size_t)(nch * sync_words), &d_sync));
     PTMH_CUDA(cudaMemsetAsync(d_sync, 0, (size_t)(nch * sync_words) * 4, sc));
     PTMH_CUDA(cudaMemcpyAsync(d_thr, thr.data(), R * 40, cudaMemcpyHostToDevice, sc));
@@ -590,7 +593,7 @@ int ptmh_host_cb_interval(int8_t* spins, int64_t R, int64_t L, int64_t* slot_to_
     for (int64_t c = 0; c < nch; ++c) {
         int64_t lo, n;
         chunk(c, lo, n);
-        cudaStream_t cst = g_ws.cs[c % kComputeStreams];  // a chunk alone does not fill the GPU
+        cudaStream_t cst = plugin_sync ? g_ws.cs[0] : g_ws.cs[c % kComputeStreams];
         PTMH_CUDA(cudaStreamWaitEvent(cst, g_ws.ev_tab, 0));
         PTMH_CUDA(cudaStreamWaitEvent(cst, g_ws.ev_in[c], 0));
         PTMH_TRY(launch_cb_pack(d_spins + lo * nsite, n, L, d_packed + lo * 2 * W, cst));

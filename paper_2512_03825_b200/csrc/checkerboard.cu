@@ -648,6 +648,113 @@ __global__ void cb_row_stats_kernel(const uint32_t* __restrict__ packed, int64_t
     }
 }
 
+// ------------------------------------ layout conversion, L % 64 == 0 fast path --
+// One thread per (lattice, row i, 64-site column block k): the 64 int8 sites
+// j = 64k .. 64k+63 of row i are one 16-byte-vector read (or write), and the
+// even / odd j of the block are exactly word k of row i of colour i & 1 /
+// 1 - (i & 1) (half-lattice index h = i*L/2 + j/2).
+__device__ __forceinline__ void bytes_to_bits(uint32_t w, int s, uint32_t& ev, uint32_t& od) {
+    // 4 int8 sites s .. s+3 (s even): bit = (site > 0)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        const uint32_t pos = (int8_t)(w >> (8 * b)) > 0 ? 1u : 0u;
+        if (((s + b) & 1) == 0) ev |= pos << ((s + b) >> 1);
+        else od |= pos << ((s + b) >> 1);
+    }
+}
+
+__global__ void cb_pack_fast_kernel(const int8_t* __restrict__ spins, int64_t rows, int L, int WR, int64_t W,
+                                    uint32_t* __restrict__ packed) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t per_lat = (int64_t)L * WR;
+    if (tid >= rows * per_lat) return;
+    const int64_t lat = tid / per_lat;
+    const int rem = (int)(tid - lat * per_lat);
+    const int i = rem / WR;
+    const uint4* src = reinterpret_cast<const uint4*>(spins + lat * (int64_t)L * L) + (int64_t)rem * 4;
+    uint32_t ev = 0, od = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint4 v = __ldcs(src + q);  // streamed once
+        bytes_to_bits(v.x, 16 * q, ev, od);
+        bytes_to_bits(v.y, 16 * q + 4, ev, od);
+        bytes_to_bits(v.z, 16 * q + 8, ev, od);
+        bytes_to_bits(v.w, 16 * q + 12, ev, od);
+    }
+    const int ce = i & 1;  // colour of the even-j sites of row i
+    packed[(lat * 2 + ce) * W + rem] = ev;
+    packed[(lat * 2 + (1 - ce)) * W + rem] = od;
+}
+
+__device__ __forceinline__ uint32_t bits_to_bytes(uint32_t ev, uint32_t od, int s) {
+    // sites s .. s+3 (s even) as int8 +1 / -1
+    uint32_t w = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        const uint32_t bit = (((s + b) & 1) == 0 ? (ev >> ((s + b) >> 1)) : (od >> ((s + b) >> 1))) & 1u;
+        w |= (bit ? 0x01u : 0xffu) << (8 * b);
+    }
+    return w;
+}
+
+// out row block (lat_out, i, k) <- packed lattice lat_in (slot order when
+// s2r is given: lat_in = s2r[lat_out])
+__global__ void cb_unpack_fast_kernel(const uint32_t* __restrict__ packed, const int64_t* __restrict__ s2r,
+                                      int64_t rows, int L, int WR, int64_t W, int8_t* __restrict__ spins) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t per_lat = (int64_t)L * WR;
+    if (tid >= rows * per_lat) return;
+    const int64_t lat = tid / per_lat;
+    const int rem = (int)(tid - lat * per_lat);
+    const int i = rem / WR;
+    const int64_t src = s2r ? s2r[lat] : lat;
+    const int ce = i & 1;
+    const uint32_t ev = packed[(src * 2 + ce) * W + rem];
+    const uint32_t od = packed[(src * 2 + (1 - ce)) * W + rem];
+    uint4* dst = reinterpret_cast<uint4*>(spins + lat * (int64_t)L * L) + (int64_t)rem * 4;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        __stcs(dst + q, make_uint4(bits_to_bytes(ev, od, 16 * q), bits_to_bytes(ev, od, 16 * q + 4),
+                                   bits_to_bytes(ev, od, 16 * q + 8), bits_to_bytes(ev, od, 16 * q + 12)));
+}
+
+// (S, Bond) per lattice from the packed state, word-parallel: Bond as the sum
+// over colour-0 sites of s*nb = 2k - 4 (k aligned neighbours, the sweep
+// kernel's neighbour logic), S from both colours' popcounts.
+__global__ void cb_row_stats_fast_kernel(const uint32_t* __restrict__ packed, int64_t rows, int L, int WR,
+                                         int64_t W, int64_t* __restrict__ stats) {
+    const int64_t lat = blockIdx.x;
+    const uint32_t* c0 = packed + lat * 2 * W;
+    const uint32_t* c1 = c0 + W;
+    long long S = 0, Bd = 0;
+    for (int w = threadIdx.x; w < L * WR; w += blockDim.x) {
+        const int i = w / WR, k = w - i * WR;
+        const int iu = i == 0 ? L - 1 : i - 1, id = i == L - 1 ? 0 : i + 1;
+        const uint32_t s = c0[w], mid = c1[w];
+        const uint32_t up = c1[iu * WR + k], dn = c1[id * WR + k];
+        uint32_t hz;
+        if ((i & 1) == 0) hz = __funnelshift_l(c1[i * WR + (k == 0 ? WR - 1 : k - 1)], mid, 1);  // m sees m-1
+        else hz = __funnelshift_r(mid, c1[i * WR + (k == WR - 1 ? 0 : k + 1)], 1);              // m sees m+1
+        const int ka = __popc(~(s ^ up)) + __popc(~(s ^ dn)) + __popc(~(s ^ mid)) + __popc(~(s ^ hz));
+        Bd += 2 * ka - 128;
+        S += 2 * (__popc(s) + __popc(mid)) - 64;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        S += __shfl_down_sync(kFullMask, S, o);
+        Bd += __shfl_down_sync(kFullMask, Bd, o);
+    }
+    __shared__ long long sS[32], sB[32];
+    const int wid = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) { sS[wid] = S; sB[wid] = Bd; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long a = 0, b = 0;
+        for (int q = 0; q < (int)(blockDim.x >> 5); ++q) { a += sS[q]; b += sB[q]; }
+        stats[2 * lat] = a;
+        stats[2 * lat + 1] = b;
+    }
+}
+
 // energies / observables by slot from per-lattice stats (lattice.py:61-65)
 __global__ void cb_slot_energy_kernel(const int64_t* __restrict__ stats, const int64_t* __restrict__ s2r,
                                       int64_t R, double J, double B, double* __restrict__ energies,
@@ -706,6 +813,13 @@ void fill_class_plan(uint32_t always_mask, int* n_up, int* k, int* sf, int* cls,
 #endif
 constexpr int kFastRows = PTMH_FERRO_ROWS;
 
+// one persistent launch for every half-sweep: the ferro kernel with whole
+// 256-thread blocks per lattice (L % 512 == 0)
+bool cb_sweeps_persistent_applies(int64_t L, uint32_t always_mask, int64_t n_sweeps) {
+    const bool ferro = (always_mask & kSymmetricFlag) && (always_mask & 0x3ffu) == 0x078u;
+    return ferro && n_sweeps > 0 && L >= 1024 && L % 512 == 0;
+}
+
 int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* row_to_slot,
                      const uint32_t* thresh, uint32_t always_mask, uint64_t seed, int64_t first_sweep,
                      int64_t n_sweeps, int64_t* stats, cudaStream_t s, uint32_t* sync) {
@@ -717,9 +831,8 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
     // symmetric thresholds, k <= 1 always, k = 2 neutral (1/2), k = 3, 4 uphill
     const bool ferro = (always_mask & kSymmetricFlag) && (always_mask & 0x3ffu) == 0x078u &&
                        rows * 2 * W < (1LL << 32);  // 32-bit word offsets in the tie queue
-    // one persistent launch for every half-sweep: whole 256-thread blocks per
-    // lattice (L % 512 == 0) and a 32-bit item count
-    if (sync && fast && ferro && L >= 1024 && L % 512 == 0 && 2 * n_sweeps * rows * (L * L / 262144) < (1LL << 31)) {
+    if (sync && ferro && cb_sweeps_persistent_applies(L, always_mask, n_sweeps) &&
+        2 * n_sweeps * rows * (L * L / 262144) < (1LL << 31)) {
         static int cached_slots[256] = {};  // resident CTAs per device
         int dev = 0;
         PTMH_CUDA(cudaGetDevice(&dev));
@@ -788,10 +901,18 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
     return PTMH_OK;
 }
 
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
 int launch_cb_pack(const int8_t* spins, int64_t rows, int64_t L, uint32_t* packed, cudaStream_t s) {
     const int64_t W = cb_words(L), n = rows * 2 * W;
     if (n == 0) return PTMH_OK;
-    cb_pack_kernel<<<ceil_div(n, 256), 256, 0, s>>>(spins, rows, (int)L, W, packed);
+    if (L % 64 == 0 && aligned16(spins)) {
+        const int64_t threads = rows * L * (L / 64);
+        cb_pack_fast_kernel<<<ceil_div(threads, 256), 256, 0, s>>>(spins, rows, (int)L, (int)(L / 64), W,
+                                                                   packed);
+    } else {
+        cb_pack_kernel<<<ceil_div(n, 256), 256, 0, s>>>(spins, rows, (int)L, W, packed);
+    }
     PTMH_LAUNCH_CHECK();
     return PTMH_OK;
 }
@@ -799,7 +920,13 @@ int launch_cb_pack(const int8_t* spins, int64_t rows, int64_t L, uint32_t* packe
 int launch_cb_unpack(const uint32_t* packed, int64_t rows, int64_t L, int8_t* spins, cudaStream_t s) {
     const int64_t W = cb_words(L), n = rows * L * L;
     if (n == 0) return PTMH_OK;
-    cb_unpack_kernel<<<ceil_div(n, 256), 256, 0, s>>>(packed, rows, (int)L, W, spins);
+    if (L % 64 == 0 && aligned16(spins)) {
+        const int64_t threads = rows * L * (L / 64);
+        cb_unpack_fast_kernel<<<ceil_div(threads, 256), 256, 0, s>>>(packed, nullptr, rows, (int)L,
+                                                                     (int)(L / 64), W, spins);
+    } else {
+        cb_unpack_kernel<<<ceil_div(n, 256), 256, 0, s>>>(packed, rows, (int)L, W, spins);
+    }
     PTMH_LAUNCH_CHECK();
     return PTMH_OK;
 }
@@ -808,14 +935,24 @@ int launch_cb_unpack_slots(const uint32_t* packed, const int64_t* s2r, int64_t R
                            cudaStream_t s) {
     const int64_t n = R * L * L;
     if (n == 0) return PTMH_OK;
-    cb_unpack_slots_kernel<<<ceil_div(n, 256), 256, 0, s>>>(packed, s2r, R, (int)L, cb_words(L), out);
+    if (L % 64 == 0 && aligned16(out)) {
+        const int64_t threads = R * L * (L / 64);
+        cb_unpack_fast_kernel<<<ceil_div(threads, 256), 256, 0, s>>>(packed, s2r, R, (int)L, (int)(L / 64),
+                                                                     cb_words(L), out);
+    } else {
+        cb_unpack_slots_kernel<<<ceil_div(n, 256), 256, 0, s>>>(packed, s2r, R, (int)L, cb_words(L), out);
+    }
     PTMH_LAUNCH_CHECK();
     return PTMH_OK;
 }
 
 int launch_cb_row_stats(const uint32_t* packed, int64_t rows, int64_t L, int64_t* stats, cudaStream_t s) {
     if (rows == 0) return PTMH_OK;
-    cb_row_stats_kernel<<<(unsigned)rows, 256, 0, s>>>(packed, rows, (int)L, cb_words(L), stats);
+    if (L % 64 == 0)
+        cb_row_stats_fast_kernel<<<(unsigned)rows, 512, 0, s>>>(packed, rows, (int)L, (int)(L / 64), cb_words(L),
+                                                               stats);
+    else
+        cb_row_stats_kernel<<<(unsigned)rows, 256, 0, s>>>(packed, rows, (int)L, cb_words(L), stats);
     PTMH_LAUNCH_CHECK();
     return PTMH_OK;
 }

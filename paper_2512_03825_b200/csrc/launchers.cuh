@@ -54,6 +54,7 @@ int64_t cb_words(int64_t L);
 int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* row_to_slot,
                      const uint32_t* thresh, uint32_t always_mask, uint64_t seed, int64_t first_sweep,
                      int64_t n_sweeps, int64_t* stats, cudaStream_t s, uint32_t* sync = nullptr);
+bool cb_sweeps_persistent_applies(int64_t L, uint32_t always_mask, int64_t n_sweeps);
 int launch_cb_pack(const int8_t* spins, int64_t rows, int64_t L, uint32_t* packed, cudaStream_t s);
 int launch_cb_unpack(const uint32_t* packed, int64_t rows, int64_t L, int8_t* spins, cudaStream_t s);
 int launch_cb_row_stats(const uint32_t* packed, int64_t rows, int64_t L, int64_t* stats, cudaStream_t s);
