@@ -22,12 +22,19 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
 
 #include "common.cuh"
 #include "launchers.cuh"
 #include "philox.cuh"
 
 namespace ptmh {
+
+#define PTMH_TRY_RC(expr)               \
+    do {                                \
+        int rc_ = (expr);               \
+        if (rc_ != PTMH_OK) return rc_; \
+    } while (0)
 
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -522,9 +529,47 @@ static int64_t advance_stride(int64_t nslots, int64_t nsteps) {
     return std::min(advance_chunk(nslots), (nsteps + kSW - 1) / kSW * kSW);
 }
 
+// Two record buffers: the draws of chunk k+1 (issue-bound, fills the GPU) run
+// on a side stream while chunk k commits (latency-bound, one warp per slot).
 int64_t advance_ws_bytes(int64_t nslots, int64_t nsteps) {
     const int64_t stride = advance_stride(nslots, nsteps);
-    return nslots * stride * 12 + nslots * (stride / kSW) * 4;
+    const int64_t one = nslots * stride * 12 + nslots * (stride / kSW) * 4;
+    return (nsteps > stride ? 2 : 1) * one;
+}
+
+// side stream + events for the draw/commit overlap, one set per device
+struct DrawStream {
+    std::mutex mu;  // held while a call enqueues (the events are shared)
+    cudaStream_t s = nullptr;   // draws (default priority)
+    cudaStream_t sc = nullptr;  // commits, highest priority: their few CTAs are
+                                // placed as soon as draw CTAs retire
+    cudaEvent_t drawn[2], committed[2], start;
+};
+
+static int draw_stream(DrawStream** out) {
+    static std::mutex mu;
+    static DrawStream per_dev[64];
+    int dev = 0;
+    PTMH_CUDA(cudaGetDevice(&dev));
+    if (dev >= 64) {
+        set_error("advance: device index >= 64");
+        return PTMH_ERR_ARG;
+    }
+    std::lock_guard<std::mutex> lk(mu);
+    DrawStream& d = per_dev[dev];
+    if (!d.s) {
+        PTMH_CUDA(cudaStreamCreateWithFlags(&d.s, cudaStreamNonBlocking));
+        int lo_pri = 0, hi_pri = 0;
+        PTMH_CUDA(cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri));
+        PTMH_CUDA(cudaStreamCreateWithPriority(&d.sc, cudaStreamNonBlocking, hi_pri));
+        for (int b = 0; b < 2; ++b) {
+            PTMH_CUDA(cudaEventCreateWithFlags(&d.drawn[b], cudaEventDisableTiming));
+            PTMH_CUDA(cudaEventCreateWithFlags(&d.committed[b], cudaEventDisableTiming));
+        }
+        PTMH_CUDA(cudaEventCreateWithFlags(&d.start, cudaEventDisableTiming));
+    }
+    *out = &d;
+    return PTMH_OK;
 }
 
 int launch_advance_2phase(const AdvanceArgs& a, void* ws, int64_t ws_bytes, cudaStream_t s) {
@@ -535,23 +580,45 @@ int launch_advance_2phase(const AdvanceArgs& a, void* ws, int64_t ws_bytes, cuda
         set_error("advance workspace too small");
         return PTMH_ERR_ARG;
     }
-    int32_t* rs = static_cast<int32_t*>(ws);
-    uint32_t* ra = reinterpret_cast<uint32_t*>(rs + nslots * stride);
-    uint32_t* rc = ra + nslots * stride;
-    uint32_t* rind = rc + nslots * stride;
-    for (int64_t a0 = 0; a0 < a.nsteps; a0 += stride) {
+    const int nbuf = a.nsteps > stride ? 2 : 1;
+    const int64_t one = nslots * stride * 12 + nslots * (stride / kSW) * 4;
+    DrawStream* ds = nullptr;
+    std::unique_lock<std::mutex> lk;
+    if (nbuf == 2) {
+        PTMH_TRY_RC(draw_stream(&ds));
+        lk = std::unique_lock<std::mutex>(ds->mu);
+        PTMH_CUDA(cudaEventRecord(ds->start, s));  // the draws read positions / tables written on s
+        PTMH_CUDA(cudaStreamWaitEvent(ds->s, ds->start, 0));
+        PTMH_CUDA(cudaStreamWaitEvent(ds->sc, ds->start, 0));
+    }
+    cudaStream_t sc = nbuf == 2 ? ds->sc : s;
+    int k = 0;
+    for (int64_t a0 = 0; a0 < a.nsteps; a0 += stride, ++k) {
+        const int b = k % nbuf;
+        int32_t* rs = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + b * one);
+        uint32_t* ra = reinterpret_cast<uint32_t*>(rs + nslots * stride);
+        uint32_t* rc = ra + nslots * stride;
+        uint32_t* rind = rc + nslots * stride;
         const int64_t n = std::min(stride, a.nsteps - a0);
         DrawArgs D{a.lo, nslots, a.L, a.tbl, a.dcls, a.seed, a.positions, a0, n, stride, rs, ra, rc, rind};
         const int64_t npad = (n + kSW - 1) / kSW * kSW;
-        draw_kernel<<<ceil_div(nslots * npad, 256), 256, 0, s>>>(D);
+        cudaStream_t sd = nbuf == 2 ? ds->s : s;
+        if (nbuf == 2 && k >= 2) PTMH_CUDA(cudaStreamWaitEvent(sd, ds->committed[b], 0));  // buffer free
+        draw_kernel<<<ceil_div(nslots * npad, 256), 256, 0, sd>>>(D);
         PTMH_LAUNCH_CHECK();
+        if (nbuf == 2) {
+            PTMH_CUDA(cudaEventRecord(ds->drawn[b], sd));
+            PTMH_CUDA(cudaStreamWaitEvent(sc, ds->drawn[b], 0));
+        }
         CommitArgs C{a, a0, n, stride, rs, ra, rc, rind, a0 + n >= a.nsteps};
         if (a.bits)
-            commit_kernel<true><<<ceil_div(nslots, 4), 128, 0, s>>>(C);
+            commit_kernel<true><<<ceil_div(nslots, 4), 128, 0, sc>>>(C);
         else
-            commit_kernel<false><<<ceil_div(nslots, 4), 128, 0, s>>>(C);
+            commit_kernel<false><<<ceil_div(nslots, 4), 128, 0, sc>>>(C);
         PTMH_LAUNCH_CHECK();
+        if (nbuf == 2) PTMH_CUDA(cudaEventRecord(ds->committed[b], sc));
     }
+    if (nbuf == 2) PTMH_CUDA(cudaStreamWaitEvent(s, ds->committed[(k - 1) % 2], 0));  // join
     return PTMH_OK;
 }
 
