@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -518,6 +519,246 @@ __global__ void __launch_bounds__(128) commit_kernel(CommitArgs C) {
     }
 }
 
+// ---------------------------------------- 1024-attempt windows (L >= 512) --
+// For integer J, B and no per-attempt recording (the energy sum is then
+// order-free) and lattices large enough that attempts rarely touch, a slot's
+// attempts are committed 1024 at a time by a whole CTA:
+//   * "free" attempts -- no EARLIER attempt of the window writes a site they
+//     read (their site or a neighbour) -- are pairwise independent and go in
+//     one parallel pass, 4 per thread;
+//   * the few "dependent" ones (~2.6 per window at L = 1024) follow in
+//     attempt order, 32 at a time, in dependency levels.
+// This is the reference order: a free attempt that touches a dependent one is
+// always the earlier of the two (otherwise it would not be free).
+// draw_w_kernel marks dependents (bit 31 of the acceptance mask) with a
+// shared-memory hash of the window's sites -> earliest attempt.
+constexpr int kWin = 1024;
+constexpr int kWinHash = 2048;
+
+__device__ __forceinline__ int win_hash(int site) { return (int)(((uint32_t)site * 0x9E3779B1u) >> (32 - 11)); }
+
+// The window path's commit needs no 32-window conflict masks (rec_conf is
+// not written).  Per attempt: the two draws, the site (a shift for
+// power-of-two L, which equals the reference's int(u * L*L) exactly), the
+// uphill-class acceptance bits against the slot's table held in shared
+// memory, and the dependent flag.
+#ifndef PTMH_DRAW_MINB
+#define PTMH_DRAW_MINB 3  // 80 registers, no spills (4: 64 + spills, 2% slower)
+#endif
+__global__ void __launch_bounds__(256, PTMH_DRAW_MINB) draw_w_kernel(DrawArgs D) {
+    __shared__ int h_key[kWinHash], h_val[kWinHash];
+    __shared__ double s_tbl[10];
+    __shared__ int s_up[10];
+    const int64_t nwin = (D.n + kWin - 1) / kWin;
+    const int64_t s = blockIdx.x / nwin;  // grid = nslots * nwin
+    const int64_t w0 = (blockIdx.x - s * nwin) * kWin;
+    const int64_t slot = D.lo + s;
+    for (int k = threadIdx.x; k < kWinHash; k += blockDim.x) {
+        h_key[k] = -1;
+        h_val[k] = 0x7fffffff;
+    }
+    if (threadIdx.x < 10) {
+        s_tbl[threadIdx.x] = D.tbl[slot * 10 + threadIdx.x];
+        s_up[threadIdx.x] = D.dcls[threadIdx.x] > 0.0;
+    }
+    __syncthreads();
+    const int Li = (int)D.L;
+    const float invL = 1.0f / (float)Li;
+    const int lg = __ffs(Li) - 1;
+    const bool pow2 = (Li & (Li - 1)) == 0;
+    const uint64_t pos0 = D.positions[slot] + 2 * (uint64_t)(D.a0 + w0);
+    int site[4];
+    uint32_t accm[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int li = q * 256 + threadIdx.x;
+        const uint64_t p = pos0 + 2 * (uint64_t)li;
+        const uint64_t w_site = philox4x64_word0(D.seed, (uint64_t)slot, p);
+        const double u_acc = uniform53(philox4x64_word0(D.seed, (uint64_t)slot, p + 1));
+        if (pow2)  // int(u * 2^(2 lg)) with u = (w >> 11) 2^-53: the top 2 lg bits of w
+            site[q] = lg == 0 ? 0 : (int)(w_site >> (64 - 2 * lg));
+        else
+            site[q] = (int)__dmul_rn(uniform53(w_site), (double)((int64_t)Li * Li));
+        uint32_t am = 0;
+#pragma unroll
+        for (int cl = 0; cl < 10; ++cl)
+            if (s_up[cl] && u_acc < s_tbl[cl]) am |= 1u << cl;
+        accm[q] = am;
+        if (w0 + li < D.n) {  // site -> earliest attempt of the window
+            int h = win_hash(site[q]);
+            while (true) {
+                const int old = atomicCAS(&h_key[h], -1, site[q]);
+                if (old == -1 || old == site[q]) {
+                    atomicMin(&h_val[h], li);
+                    break;
+                }
+                h = (h + 1) & (kWinHash - 1);
+            }
+        }
+    }
+    __syncthreads();
+    auto earliest = [&](int x) -> int {
+        int h = win_hash(x);
+        while (true) {
+            const int k = h_key[h];
+            if (k == x) return h_val[h];
+            if (k == -1) return 0x7fffffff;
+            h = (h + 1) & (kWinHash - 1);
+        }
+    };
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int li = q * 256 + threadIdx.x;
+        if (w0 + li >= D.n) continue;
+        const int x = site[q];
+        const int r = pow2 ? x >> lg : site_row(x, Li, invL), c = x - r * Li;
+        const int rp = (r + 1 == Li) ? 0 : r + 1, cp = (c + 1 == Li) ? 0 : c + 1;
+        const bool dep = (earliest(x) < li) | (earliest(rp * Li + c) < li) |
+                         (earliest((r == 0 ? Li - 1 : r - 1) * Li + c) < li) | (earliest(r * Li + cp) < li) |
+                         (earliest(r * Li + (c == 0 ? Li - 1 : c - 1)) < li);
+        const int64_t o = s * D.stride + w0 + li;
+        D.rec_site[o] = site[q];
+        D.rec_acc[o] = accm[q] | (dep ? 0x80000000u : 0u);
+    }
+}
+
+__global__ void __launch_bounds__(256) commit_w_kernel(CommitArgs C) {
+    __shared__ uint32_t dep_bits[kWin / 32];
+    __shared__ int dep_list[kWin];
+    __shared__ double red_d[8];
+    __shared__ long long red_s[8];
+    const AdvanceArgs& A = C.A;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t s = blockIdx.x;
+    const int64_t slot = A.lo + s;
+    const int Li = (int)A.L;
+    const float invL = 1.0f / (float)Li;
+    const int64_t nwords = ((int64_t)Li * Li + 31) >> 5;
+    uint32_t* latw = A.bits + A.slot_to_row[slot] * nwords;
+    auto spin = [&](int x) -> int { return 2 * (int)((latw[x >> 5] >> (x & 31)) & 1u) - 1; };
+    auto nbrs = [&](int x, int& up, int& dn, int& rt, int& lf) {
+        const int r = site_row(x, Li, invL), c = x - r * Li;
+        up = (r + 1 == Li ? 0 : r + 1) * Li + c;
+        dn = (r == 0 ? Li - 1 : r - 1) * Li + c;
+        rt = r * Li + (c + 1 == Li ? 0 : c + 1);
+        lf = r * Li + (c == 0 ? Li - 1 : c - 1);
+    };
+    double acc_d = -0.0;  // IEEE identity (see commit_kernel)
+    long long acc_ds = 0;
+    const int32_t* rs = C.rec_site + s * C.stride;
+    const uint32_t* ra = C.rec_acc + s * C.stride;
+    for (int64_t w0 = 0; w0 < C.n; w0 += kWin) {
+        if (threadIdx.x < kWin / 32) dep_bits[threadIdx.x] = 0;
+        __syncthreads();
+        // ---- free attempts: one parallel pass
+        int st[4];
+        uint32_t am[4];
+        bool on[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int64_t a = w0 + q * 256 + threadIdx.x;
+            on[q] = a < C.n;
+            st[q] = on[q] ? rs[a] : 0;
+            am[q] = on[q] ? ra[a] : 0u;
+        }
+        int sp[4], nb[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            int up, dn, rt, lf;
+            nbrs(st[q], up, dn, rt, lf);
+            sp[q] = spin(st[q]);
+            nb[q] = spin(up) + spin(dn) + spin(rt) + spin(lf);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (!on[q]) continue;
+            if (am[q] >> 31) {
+                const int li = q * 256 + threadIdx.x;
+                atomicOr(&dep_bits[li >> 5], 1u << (li & 31));
+                continue;
+            }
+            const int cls = (sp[q] > 0 ? 5 : 0) + (nb[q] + 4) / 2;
+            const double d = A.dcls[cls];
+            if ((d <= 0.0) || ((am[q] >> cls) & 1u)) {
+                atomicXor(&latw[st[q] >> 5], 1u << (st[q] & 31));
+                acc_d = __dadd_rn(acc_d, d);
+                acc_ds += -2 * sp[q];
+            }
+        }
+        __syncthreads();
+        // ---- dependents: warp 0, attempt order, 32 at a time in levels
+        if (warp == 0) {
+            const uint32_t m = dep_bits[lane];
+            int pre = __popc(m);
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(kFull, pre, o);
+                if (lane >= o) pre += v;
+            }
+            const int total = __shfl_sync(kFull, pre, 31);
+            int pos = pre - __popc(m);
+            for (uint32_t mm = m; mm; mm &= mm - 1) dep_list[pos++] = lane * 32 + __ffs(mm) - 1;
+            __syncwarp();
+            for (int b0 = 0; b0 < total; b0 += 32) {
+                const bool valid = b0 + lane < total;
+                const int64_t a = w0 + (valid ? dep_list[b0 + lane] : 0);
+                const int x = valid ? rs[a] : -1;
+                const uint32_t amk = valid ? ra[a] : 0u;
+                int up = 0, dn = 0, rt = 0, lf = 0;
+                if (valid) nbrs(x, up, dn, rt, lf);
+                unsigned conf = 0;
+                for (int k = 0; k < 32; ++k) {
+                    const int s2 = __shfl_sync(kFull, x, k);
+                    const bool hit = (s2 == x) | (s2 == up) | (s2 == dn) | (s2 == rt) | (s2 == lf);
+                    conf |= (hit && k < lane && s2 >= 0) ? (1u << k) : 0u;
+                }
+                unsigned pending = __ballot_sync(kFull, valid);
+                while (pending) {
+                    const bool ready = ((pending >> lane) & 1u) && ((conf & pending) == 0u);
+                    if (ready) {
+                        const int spx = spin(x);
+                        const int nbx = spin(up) + spin(dn) + spin(rt) + spin(lf);
+                        const int cls = (spx > 0 ? 5 : 0) + (nbx + 4) / 2;
+                        const double d = A.dcls[cls];
+                        if ((d <= 0.0) || ((amk >> cls) & 1u)) {
+                            atomicXor(&latw[x >> 5], 1u << (x & 31));
+                            acc_d = __dadd_rn(acc_d, d);
+                            acc_ds += -2 * spx;
+                        }
+                    }
+                    __syncwarp();
+                    pending &= ~__ballot_sync(kFull, ready);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // order-free sums (integer-valued d): warp shuffles, then the CTA
+    for (int o = 16; o > 0; o >>= 1) {
+        acc_d = __dadd_rn(acc_d, __shfl_down_sync(kFull, acc_d, o));
+        acc_ds += __shfl_down_sync(kFull, acc_ds, o);
+    }
+    if (lane == 0) {
+        red_d[warp] = acc_d;
+        red_s[warp] = acc_ds;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double td = -0.0;
+        long long ts = 0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+            td = __dadd_rn(td, red_d[k]);
+            ts += red_s[k];
+        }
+        A.energies[slot] = __dadd_rn(A.energies[slot], td);
+        A.spin_sums[slot] += ts;
+        if (C.last) {
+            A.positions[slot] += 2 * (uint64_t)(C.a0 + C.n);
+            A.iters_done[slot] = A.start_iter + C.a0 + C.n;
+        }
+    }
+}
+
 int64_t advance_chunk(int64_t nslots) {
     // attempts per slot per phase-1/phase-2 pass: ~16M records (~200 MiB)
     int64_t c = (int64_t(1) << 24) / std::max<int64_t>(1, nslots);
@@ -581,6 +822,13 @@ int launch_advance_2phase(const AdvanceArgs& a, void* ws, int64_t ws_bytes, cuda
         return PTMH_ERR_ARG;
     }
     const int nbuf = a.nsteps > stride ? 2 : 1;
+    // 1024-attempt CTA windows: bit lattices, order-free energy sums, and
+    // L >= 512 so that a window holds few dependent attempts
+    // (PTMH_EXACT_WINDOWS=0 forces the warp path, =2 the window path at any
+    // L: A/B in tools/, dependent-heavy windows in tests)
+    const char* ew = getenv("PTMH_EXACT_WINDOWS");
+    const bool windows = a.bits && a.int_energy && a.record == 0 && a.L <= 4096 &&
+                         (ew && ew[0] == '2' ? a.L >= 3 : a.L >= 512) && !(ew && ew[0] == '0');
     const int64_t one = nslots * stride * 12 + nslots * (stride / kSW) * 4;
     DrawStream* ds = nullptr;
     std::unique_lock<std::mutex> lk;
@@ -604,14 +852,20 @@ int launch_advance_2phase(const AdvanceArgs& a, void* ws, int64_t ws_bytes, cuda
         const int64_t npad = (n + kSW - 1) / kSW * kSW;
         cudaStream_t sd = nbuf == 2 ? ds->s : s;
         if (nbuf == 2 && k >= 2) PTMH_CUDA(cudaStreamWaitEvent(sd, ds->committed[b], 0));  // buffer free
-        draw_kernel<<<ceil_div(nslots * npad, 256), 256, 0, sd>>>(D);
+        const int64_t nwin = (n + kWin - 1) / kWin;
+        if (windows)
+            draw_w_kernel<<<(unsigned)(nslots * nwin), 256, 0, sd>>>(D);
+        else
+            draw_kernel<<<ceil_div(nslots * npad, 256), 256, 0, sd>>>(D);
         PTMH_LAUNCH_CHECK();
         if (nbuf == 2) {
             PTMH_CUDA(cudaEventRecord(ds->drawn[b], sd));
             PTMH_CUDA(cudaStreamWaitEvent(sc, ds->drawn[b], 0));
         }
         CommitArgs C{a, a0, n, stride, rs, ra, rc, rind, a0 + n >= a.nsteps};
-        if (a.bits)
+        if (windows)
+            commit_w_kernel<<<(unsigned)nslots, 256, 0, sc>>>(C);
+        else if (a.bits)
             commit_kernel<true><<<ceil_div(nslots, 4), 128, 0, sc>>>(C);
         else
             commit_kernel<false><<<ceil_div(nslots, 4), 128, 0, sc>>>(C);
