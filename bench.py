@@ -96,18 +96,23 @@ class ClockSampler:
         self.samples = []
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
-
-    def _run(self):
-        nv = None
-        try:  # NVML: ~1 ms per query, so short timed regions still get samples
+        # NVML is initialised here, before the timed region (nvmlInit can take
+        # longer than a whole C3 run); each query then costs ~1 ms
+        self._nv = None
+        try:
             import pynvml as nv
             nv.nvmlInit()
-            h = nv.nvmlDeviceGetHandleByIndex(self.index)
-            bits = (nv.nvmlClocksThrottleReasonHwSlowdown, nv.nvmlClocksThrottleReasonHwThermalSlowdown,
-                    nv.nvmlClocksThrottleReasonSwThermalSlowdown, nv.nvmlClocksThrottleReasonSwPowerCap)
-            smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            self._h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self._bits = (nv.nvmlClocksThrottleReasonHwSlowdown, nv.nvmlClocksThrottleReasonHwThermalSlowdown,
+                          nv.nvmlClocksThrottleReasonSwThermalSlowdown, nv.nvmlClocksThrottleReasonSwPowerCap)
+            self._smax = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+            self._nv = nv
         except Exception:  # noqa: BLE001
-            nv = None
+            self._nv = None
+
+    def _run(self):
+        nv, h, bits = self._nv, getattr(self, "_h", None), getattr(self, "_bits", ())
+        smax = getattr(self, "_smax", None)
         while not self._stop.is_set():
             try:
                 if nv is not None:
@@ -122,7 +127,7 @@ class ClockSampler:
                         self.samples.append([x.strip() for x in out.split(",")])
             except Exception:  # noqa: BLE001
                 pass
-            self._stop.wait(0.01)
+            self._stop.wait(0.002)
 
     def __enter__(self):
         self._t.start()
@@ -249,6 +254,7 @@ def main():
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    clk = ClockSampler(local_rank)
     sharded = world > 1 or args.sharded
     if sharded:
         dist.init_process_group("nccl", device_id=dev)
@@ -298,7 +304,7 @@ def main():
         state["round"] += 1
 
     step_ms, sweep_ms = [], []
-    with ClockSampler(local_rank) as clk:
+    with clk:
         for _ in range(args.warmup):
             step()
         torch.cuda.synchronize()
