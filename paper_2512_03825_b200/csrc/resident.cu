@@ -107,12 +107,12 @@ __device__ __forceinline__ void resident_word(const ResidentArgs& A, uint32_t* o
         const uint4 r1 = philox4x32_10(make_uint4(2u * (uint32_t)w + 1u, ctr1, (uint32_t)slot, 0u), A.rk);
         const uint32_t U[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
         acc |= K2 & ~U[0];
-        uint32_t K4r = K4;
-        asm volatile("" : "+r"(K4r));
         uint32_t bor = 0, eq = upm;  // borrow of u - t (LSB first) + ties
 #pragma unroll
         for (int p = 7; p >= 0; --p) {
-            const uint32_t Tm = (K4r & masks[8 + p]) | (~K4r & masks[p]);
+            // threshold plane: t4's bit where K4, else t3's, as one IMAD
+            // (checkerboard.cu, ferro_strip)
+            const uint32_t Tm = K4 * masks[p] + masks[8 + p];
             bor = (~U[p] & Tm) | (~U[p] & bor) | (Tm & bor);
             eq &= ~(U[p] ^ Tm);
         }
@@ -189,7 +189,7 @@ __device__ __forceinline__ void resident_word(const ResidentArgs& A, uint32_t* o
 constexpr int kMaxLatPerBlock = 64;
 
 // lattice li of this block now holds `slot`: cache its slot and (ferro) the
-// threshold bit-plane masks in shared memory
+// threshold-plane select coefficients in shared memory
 template <bool kFerro>
 __device__ __forceinline__ void resident_set_slot(const ResidentArgs& A, int li, int slot, int* s_slot,
                                                   uint32_t (*s_mask)[18]) {
@@ -198,8 +198,9 @@ __device__ __forceinline__ void resident_set_slot(const ResidentArgs& A, int li,
         const uint32_t t3 = __ldg(A.thresh + slot * 10 + 8), t4 = __ldg(A.thresh + slot * 10 + 9);
 #pragma unroll
         for (int p = 0; p < 8; ++p) {
-            s_mask[li][p] = 0u - ((t3 >> (31 - p)) & 1u);
-            s_mask[li][8 + p] = 0u - ((t4 >> (31 - p)) & 1u);
+            const uint32_t ta = (t3 >> (31 - p)) & 1u, tb = (t4 >> (31 - p)) & 1u;
+            s_mask[li][p] = tb - ta;     // TM: Tm = K4 * TM + TC
+            s_mask[li][8 + p] = 0u - ta;  // TC
         }
         s_mask[li][16] = t3;
         s_mask[li][17] = t4;
@@ -216,7 +217,7 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
     __shared__ int s_slot[kMaxLatPerBlock];
     __shared__ int s_S[kMaxLatPerBlock], s_B[kMaxLatPerBlock];
     __shared__ double s_u[kMaxLatPerBlock];
-    __shared__ uint32_t s_mask[kFerro ? kMaxLatPerBlock : 1][18];  // TA[8], TB[8], t3, t4
+    __shared__ uint32_t s_mask[kFerro ? kMaxLatPerBlock : 1][18];  // TM[8], TC[8], t3, t4
     const int wr_shift = (A.WR > 0 && (A.WR & (A.WR - 1)) == 0) ? __ffs(A.WR) - 1 : -1;
     const int R = A.R, W = A.W;
     const int lo = (int)((int64_t)R * blockIdx.x / gridDim.x);
