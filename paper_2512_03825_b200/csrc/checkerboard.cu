@@ -832,7 +832,7 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
     const bool ferro = (always_mask & kSymmetricFlag) && (always_mask & 0x3ffu) == 0x078u &&
                        rows * 2 * W < (1LL << 32);  // 32-bit word offsets in the tie queue
     if (sync && ferro && cb_sweeps_persistent_applies(L, always_mask, n_sweeps) &&
-        2 * n_sweeps * rows * (L * L / 262144) < (1LL << 31)) {
+        2 * n_sweeps * rows * (L * L / 65536) < (1LL << 31)) {
         static int cached_slots[256] = {};  // resident CTAs per device
         int dev = 0;
         PTMH_CUDA(cudaGetDevice(&dev));
@@ -843,23 +843,53 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
             PTMH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cb_sweeps_persistent<16>, 256, 0));
             cached_slots[dev] = sms * std::max(occ, 1);
         }
+        const int64_t slots = cached_slots[dev];
         const int WR = (int)(L / 64);
+        // Rows per thread: 16 amortises the per-strip setup best, but one
+        // lattice's phases are sequential, so the interval's critical path is
+        // 2n items.  With few lattices (a rank's shard of C3 on 8 GPUs: 32)
+        // the phase has too few items to fill the GPU and that path binds:
+        // take the largest kRows whose phase still has >= 1 item per CTA
+        // slot (else 4).  Measured on one B200 (attempts/s at L = 1024):
+        // R = 256: 16 rows 3.23e12 (8: 2.93e12); R = 64: 8 rows 2.55e12
+        // (16: 2.01e12, 4: 2.38e12); R = 32: 4 rows 2.00e12 (16: 1.18e12).
+        // (PTMH_PERSIST_ROWS pins it: A/B and tests.)
+        const char* er = getenv("PTMH_PERSIST_ROWS");
+        int krows = 4;
+        if (er) {
+            krows = atoi(er);
+        } else {
+            for (int k : {16, 8}) {
+                if (rows * (L * L / (256LL * 64 * k)) >= slots) {
+                    krows = k;
+                    break;
+                }
+            }
+        }
+        if (krows != 4 && krows != 8 && krows != 16) krows = 16;
         // 256-thread blocks per item: amortise the per-item scheduling over
         // several blocks while a phase keeps >= 8 items per resident CTA
         // (PTMH_PERSIST_ITEMS_PER_SLOT overrides the 8; tests use 0 to force
         // the largest groups at small shapes)
-        const int64_t blocks = L * L / 262144;  // per lattice and phase
+        const int64_t blocks = L * L / (256LL * 64 * krows);  // per lattice and phase
         const char* ev = getenv("PTMH_PERSIST_ITEMS_PER_SLOT");
         const int64_t per_slot = ev ? atoll(ev) : 8;
         int64_t group = 1;
         while (group * 2 <= blocks && blocks % (group * 2) == 0 &&
-               rows * blocks / (group * 2) >= per_slot * (int64_t)cached_slots[dev])
+               rows * blocks / (group * 2) >= per_slot * slots)
             group *= 2;
         const int64_t items = 2 * n_sweeps * rows * (blocks / group);
-        const unsigned grid = (unsigned)std::min<int64_t>(items, cached_slots[dev]);
-        cb_sweeps_persistent<16><<<grid, 256, 0, s>>>(packed, rows, (int)L, WR, W, row_to_slot, thresh, rk,
-                                                       (uint32_t)(2 * first_sweep), (uint32_t)(2 * n_sweeps),
-                                                       stats, 4u, sync, (uint32_t)group);
+        const unsigned grid = (unsigned)std::min<int64_t>(items, slots);
+        const uint32_t c0 = (uint32_t)(2 * first_sweep), np = (uint32_t)(2 * n_sweeps);
+        if (krows == 16)
+            cb_sweeps_persistent<16><<<grid, 256, 0, s>>>(packed, rows, (int)L, WR, W, row_to_slot, thresh, rk,
+                                                           c0, np, stats, 4u, sync, (uint32_t)group);
+        else if (krows == 8)
+            cb_sweeps_persistent<8><<<grid, 256, 0, s>>>(packed, rows, (int)L, WR, W, row_to_slot, thresh, rk,
+                                                          c0, np, stats, 4u, sync, (uint32_t)group);
+        else
+            cb_sweeps_persistent<4><<<grid, 256, 0, s>>>(packed, rows, (int)L, WR, W, row_to_slot, thresh, rk,
+                                                          c0, np, stats, 4u, sync, (uint32_t)group);
         PTMH_LAUNCH_CHECK();
         return PTMH_OK;
     }

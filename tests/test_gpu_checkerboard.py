@@ -267,18 +267,23 @@ def test_full_states_match_oracle(mods, L, R, sweeps, every, rec_every):
     assert np.array_equal(rec.magnetizations, rec.states.sum(axis=(2, 3)) / (L * L))
 
 
-@pytest.mark.parametrize("L,R,first,nsweeps,per_slot", [
-    (1024, 24, 3, 7, None), (1024, 256, 0, 10, None), (2048, 5, 1, 3, None),
-    (2048, 5, 1, 3, "0"),      # 16 slices per item: one item per lattice and phase
-    (1024, 256, 0, 4, "0"),    # 4 slices per item
+@pytest.mark.parametrize("L,R,first,nsweeps,per_slot,rows", [
+    (1024, 24, 3, 7, None, None), (1024, 256, 0, 10, None, None), (2048, 5, 1, 3, None, None),
+    (2048, 5, 1, 3, "0", "16"),    # 16 blocks per item: one item per lattice and phase
+    (1024, 256, 0, 4, "0", "16"),  # 4 blocks per item
+    (1024, 32, 2, 5, None, "8"),   # 8 rows per thread
+    (1024, 32, 2, 5, None, "4"),   # 4 rows per thread (a rank's C3 shard at 8 GPUs)
+    (512, 9, 0, 6, "0", "4"),      # L = 512, grouped 4-row items
 ])
-def test_persistent_sweeps_equal_per_launch_path(mods, monkeypatch, L, R, first, nsweeps, per_slot):
+def test_persistent_sweeps_equal_per_launch_path(mods, monkeypatch, L, R, first, nsweeps, per_slot, rows):
     """The one-launch dataflow path (cb_sweeps_persistent) and the per-launch
     half-sweep kernels give identical lattices and stats; the sync block is
     left zeroed for the next call."""
     p, engine, _, _ = mods
     if per_slot is not None:
         monkeypatch.setenv("PTMH_PERSIST_ITEMS_PER_SLOT", per_slot)
+    if rows is not None:
+        monkeypatch.setenv("PTMH_PERSIST_ROWS", rows)
     temps = p.build_ladder(R)
     perm = np.random.default_rng(R).permutation(R)
     r2s = np.empty(R, dtype=np.int64); r2s[perm] = np.arange(R)

@@ -15,7 +15,10 @@ from paper_2512_03825_b200.engine import CheckerboardEngine  # noqa: E402
 
 persist = "--no-persist" not in sys.argv
 for name in ([a for a in sys.argv[1:] if not a.startswith("--")] or ["c3"]):
-    L, R, every, _ = CONFIGS[name]
+    if name in CONFIGS:
+        L, R, every, _ = CONFIGS[name]
+    else:  # "L,R": e.g. 1024,32 = one rank's shard of C3 at 8 GPUs
+        L, R = (int(x) for x in name.split(","))
     eng = CheckerboardEngine(L, R, build_ladder(R), 42, 1.0, 0.0, 0.5, 0)
     eng.persistent = persist
     eng.init_state()
