@@ -212,21 +212,38 @@ __device__ __forceinline__ void resident_set_slot(const ResidentArgs& A, int li,
 // separates the colours, per-lattice (S, Bond) accumulate in shared memory.
 // Slots live in shared memory for the whole launch: only the owner changes
 // them, after an exchange round.
-template <int kMode, bool kFerro, int kThreads>
+//
+// kCl: a thread-block CLUSTER owns the lattices instead (when there are fewer
+// lattices than SMs, e.g. C2's 64 lattices of 256^2): its CTAs split the
+// (lattice, word) items, the cluster barrier separates the colours, and the
+// per-lattice (S, Bond) partial sums go to rank 0's shared memory through
+// DSMEM atomics.  Every CTA keeps its own copy of the slots and masks and
+// decides the exchange for its cluster's lattices redundantly (same inputs,
+// same rule); rank 0 alone writes the outputs.
+template <int kMode, bool kFerro, int kThreads, bool kCl>
 __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
     __shared__ int s_slot[kMaxLatPerBlock];
     __shared__ int s_S[kMaxLatPerBlock], s_B[kMaxLatPerBlock];
     __shared__ double s_u[kMaxLatPerBlock];
     __shared__ uint32_t s_mask[kFerro ? kMaxLatPerBlock : 1][18];  // TM[8], TC[8], t3, t4
+    cg::cluster_group cluster = cg::this_cluster();
+    const int cs = kCl ? (int)cluster.num_blocks() : 1;
+    const int crank = kCl ? (int)cluster.block_rank() : 0;
+    const int cid = (int)blockIdx.x / cs, ncl = (int)gridDim.x / cs;
+    int* s_S0 = kCl ? cluster.map_shared_rank(s_S, 0) : s_S;  // rank 0 accumulates
+    int* s_B0 = kCl ? cluster.map_shared_rank(s_B, 0) : s_B;
+    const bool owner = crank == 0;
     const int wr_shift = (A.WR > 0 && (A.WR & (A.WR - 1)) == 0) ? __ffs(A.WR) - 1 : -1;
     const int R = A.R, W = A.W;
-    const int lo = (int)((int64_t)R * blockIdx.x / gridDim.x);
-    const int hi = (int)((int64_t)R * (blockIdx.x + 1) / gridDim.x);
+    const int lo = (int)((int64_t)R * cid / ncl);
+    const int hi = (int)((int64_t)R * (cid + 1) / ncl);
     const int nl = hi - lo;
-    const int items = nl * W;
+    // this CTA's slice [ib, ib + items) of the cluster's (lattice, word) items
+    const int ib = (int)((int64_t)nl * W * crank / cs);
+    const int items = (int)((int64_t)nl * W * (crank + 1) / cs) - ib;
     const int items_pad = (items + 31) & ~31;  // whole warps iterate together (warp-reduced stats)
     // (li, w) of this thread's first item and the per-iteration step
-    const int li_0 = (int)threadIdx.x / W, w_0 = (int)threadIdx.x - li_0 * W;
+    const int li_0 = (ib + (int)threadIdx.x) / W, w_0 = ib + (int)threadIdx.x - li_0 * W;
     const int step_l = (int)blockDim.x / W, step_w = (int)blockDim.x - step_l * W;
     int buf = A.buf;
     for (int i = threadIdx.x; i < nl; i += blockDim.x) {
@@ -234,7 +251,10 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
         s_S[i] = 0;
         s_B[i] = 0;
     }
-    __syncthreads();
+    if (kCl)
+        cluster.sync();
+    else
+        __syncthreads();
     for (int64_t t = A.first_sweep; t < A.first_sweep + A.n_sweeps; ++t) {
         const int64_t done = t + 1;
         const bool rec = A.record_every > 0 && done % A.record_every == 0;
@@ -269,16 +289,19 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
                             sB += __shfl_down_sync(0xffffffffu, sB, o);
                         }
                         if ((threadIdx.x & 31) == 0) {
-                            atomicAdd(&s_S[li0], sS);
-                            atomicAdd(&s_B[li0], sB);
+                            atomicAdd(&s_S0[li0], sS);
+                            atomicAdd(&s_B0[li0], sB);
                         }
                     } else if (on) {
-                        atomicAdd(&s_S[li], sS);
-                        atomicAdd(&s_B[li], sB);
+                        atomicAdd(&s_S0[li], sS);
+                        atomicAdd(&s_B0[li], sB);
                     }
                 }
             }
-            __syncthreads();
+            if (kCl)
+                cluster.sync();
+            else
+                __syncthreads();
         }
         if (!need_stats) continue;
         // publish (S, Bond); zero the accumulators for the next stats sweep
@@ -288,12 +311,17 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
         const int n_pairs = (R - first) / 2;
         int64_t* pub = A.slot_stats + (round & 1) * 2 * (int64_t)R;
         for (int i = threadIdx.x; i < nl; i += blockDim.x) {
+            const int k = s_slot[i];
+            if (exch)  // the swap draw depends only on (round, pair): draw it before the barrier
+                s_u[i] = (k >= first && (k - first) / 2 < n_pairs)
+                             ? stream_uniform(A.seed, (uint64_t)(R + (k - first) / 2), (uint64_t)round)
+                             : 0.0;
+            if (!owner) continue;
             const long long S = s_S[i], Bd = s_B[i];
             s_S[i] = 0;
             s_B[i] = 0;
             A.stats[2 * (lo + i)] = S;
             A.stats[2 * (lo + i) + 1] = Bd;
-            const int k = s_slot[i];
             if (rec) {  // by slot, before the round (executor.py order)
                 const int64_t col = done / A.record_every - 1;
                 A.obs_e[(int64_t)k * A.ncols + col] = __dsub_rn(__dmul_rn(A.B, (double)S), __dmul_rn(A.J, (double)Bd));
@@ -303,10 +331,6 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
                 // the exchange reads (S, Bond) by slot: one load per partner
                 pub[2 * k] = S;
                 pub[2 * k + 1] = Bd;
-                // the swap draw depends only on (round, pair): draw it before the barrier
-                s_u[i] = (k >= first && (k - first) / 2 < n_pairs)
-                             ? stream_uniform(A.seed, (uint64_t)(R + (k - first) / 2), (uint64_t)round)
-                             : 0.0;
             }
         }
         if (!exch) continue;
@@ -334,15 +358,17 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
                 }
                 const bool acc = u < prob;
                 if (acc) nk = (k == i) ? j : i;
-                if (k == i) {
+                if (k == i && owner) {
                     if (acc) atomicAdd((unsigned long long*)&A.counters[0], 1ull);
                     if (fabs(u - prob) <= 4.0 * 2.220446049250313e-16 * fmax(prob, 2.2250738585072014e-308))
                         atomicAdd((unsigned long long*)&A.counters[1], 1ull);
                 }
             }
             // the permutation is an output only: nothing in the launch reads it back
-            A.r2s[buf ^ 1][r] = nk;
-            A.s2r[buf ^ 1][nk] = r;
+            if (owner) {
+                A.r2s[buf ^ 1][r] = nk;
+                A.s2r[buf ^ 1][nk] = r;
+            }
             if (nk != k) resident_set_slot<kFerro>(A, li, nk, s_slot, s_mask);
         }
         buf ^= 1;
@@ -353,24 +379,52 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
 template <int kMode, bool kFerro, int kThreads>
 static int launch_resident_t(const ResidentArgs& a, int sms, cudaStream_t s) {
     int per_sm = 0;
-    PTMH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cb_resident_kernel<kMode, kFerro, kThreads>,
-                                                            kThreads, 0));
+    PTMH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, cb_resident_kernel<kMode, kFerro, kThreads, false>, kThreads, 0));
+    const int slots = sms * std::max(1, per_sm);
+    // Fewer lattices than CTA slots and enough words per lattice: a cluster
+    // of cs CTAs owns each lattice (C2: 64 lattices of 2048 words per colour
+    // on 128 SMs instead of 64).  PTMH_RESIDENT_CLUSTER=1 turns it off.
+    int cs = 1;
+    const char* ec = getenv("PTMH_RESIDENT_CLUSTER");  // "1": off; "2", "4", "8": that size
+    if (ec && atoi(ec) > 1) {
+        cs = atoi(ec);
+    } else if (!(ec && ec[0] == '1') && kThreads == 1024) {
+        while (cs < 8 && (int64_t)a.R * cs * 2 <= slots && a.W / (cs * 2) >= 512) cs *= 2;
+    }
     // enough blocks to fill the GPU, few enough that no block owns more
     // lattices than its shared-memory tables hold
-    const int grid = std::min(a.R, sms * std::max(1, per_sm));
-    if ((a.R + grid - 1) / grid > kMaxLatPerBlock) {
+    const int grid = cs > 1 ? a.R * cs : std::min(a.R, slots);
+    if (cs == 1 && (a.R + grid - 1) / grid > kMaxLatPerBlock) {
         set_error("resident kernel: too many lattices per block for this grid");
         return PTMH_ERR_ARG;
     }
     // as few threads as keep the item loop's trip count: every thread then
     // does the same number of words per colour (no tail warps at the barrier)
-    const int64_t items = (int64_t)((a.R + grid - 1) / grid) * a.W;
+    const int64_t items = (int64_t)((a.R * cs + grid - 1) / grid) * a.W / cs;
     const int64_t trips = (items + kThreads - 1) / kThreads;
     const int threads = (int)std::min<int64_t>(kThreads, (((items + trips - 1) / trips) + 31) & ~31);
     ResidentArgs args = a;
     void* kargs[] = {&args};
-    PTMH_CUDA(cudaLaunchCooperativeKernel((const void*)cb_resident_kernel<kMode, kFerro, kThreads>, grid,
-                                          threads, kargs, 0, s));
+    if (cs == 1) {
+        PTMH_CUDA(cudaLaunchCooperativeKernel((const void*)cb_resident_kernel<kMode, kFerro, kThreads, false>, grid,
+                                              threads, kargs, 0, s));
+        return PTMH_OK;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)threads);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeCooperative;
+    attr[1].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    PTMH_CUDA(cudaLaunchKernelExC(&cfg, (const void*)cb_resident_kernel<kMode, kFerro, kThreads, true>, kargs));
     return PTMH_OK;
 }
 
@@ -387,8 +441,8 @@ static int launch_resident_sized(const ResidentArgs& a, cudaStream_t s) {
         if (atoi(e) == 256) return launch_resident_t<kMode, kFerro, 256>(a, sms, s);
     }
     int per_sm = 0;
-    PTMH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cb_resident_kernel<kMode, kFerro, 1024>,
-                                                            1024, 0));
+    PTMH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, cb_resident_kernel<kMode, kFerro, 1024, false>, 1024, 0));
     const int64_t grid = std::min<int64_t>(a.R, (int64_t)sms * std::max(1, per_sm));
     if ((a.R + grid - 1) / grid <= kMaxLatPerBlock) return launch_resident_t<kMode, kFerro, 1024>(a, sms, s);
     return launch_resident_t<kMode, kFerro, 256>(a, sms, s);

@@ -180,7 +180,9 @@ def test_one_lattice_matches_oracle_at_1024(mods):
     (64, 700, 6, 1, 17, 1.0, 0.0, 2),   # several lattices per CTA
     (16, 2000, 5, 1, 18, 1.0, 0.0, 1),  # many lattices per CTA, segment gather
     (128, 5, 12, 5, 4, 1.0, 0.1, 2),    # field: class plan
-    (256, 3, 6, 2, 9, -1.0, 0.0, 1),    # antiferromagnet
+    (256, 3, 6, 2, 9, -1.0, 0.0, 1),    # antiferromagnet (cluster of 2 CTAs per lattice)
+    (256, 5, 12, 1, 19, 1.0, 0.0, 2),   # ferro, cluster of 2 CTAs per lattice
+    (512, 3, 6, 1, 20, 1.0, 0.0, 1),    # cluster of 8 CTAs per lattice
     (2, 7, 50, 3, 5, 1.0, 0.0, 1),
     (6, 4, 25, 0, 6, 0.5, -0.5, 5),     # no exchanges
 ])
