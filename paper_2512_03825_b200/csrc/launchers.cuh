@@ -89,6 +89,7 @@ struct ResidentArgs {
     int n_up, up_k[10], up_sf[10], up_cls[10];
     int ferro;
     uint32_t seg_lo, seg_even;  // L in {8, 16, 32}: bit 0 of each row segment, even-row segments
+    int warp_lat;               // launcher-set: each warp owns whole lattices (no CTA barrier per colour)
 };
 int launch_cb_resident(const ResidentArgs& a, bool fast, cudaStream_t s, int* grid_out);
 void fill_class_plan(uint32_t always_mask, int* n_up, int* k, int* sf, int* cls, int* ferro);

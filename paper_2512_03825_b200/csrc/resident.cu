@@ -260,6 +260,38 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
         const bool rec = A.record_every > 0 && done % A.record_every == 0;
         const bool exch = A.swap_every > 0 && done % A.swap_every == 0 && done < A.total_sweeps;
         const bool need_stats = rec || exch || t + 1 == A.first_sweep + A.n_sweeps;
+        if (!kCl && A.warp_lat) {
+            // warp-owned lattices: warp q sweeps lattices q, q + nwarps, ...
+            // whole (both colours, lanes striding over the words), so the
+            // colours only need __syncwarp and the warps never wait for each
+            // other between exchange rounds
+            const int lane = threadIdx.x & 31, nwarps = (int)blockDim.x >> 5;
+            for (int color = 0; color < 2; ++color) {
+                const uint32_t ctr1 = (uint32_t)(2 * t + color);
+                const bool st = color == 1 && need_stats;
+                for (int li = (int)threadIdx.x >> 5; li < nl; li += nwarps) {
+                    uint32_t* c0 = A.packed + (int64_t)(lo + li) * 2 * W;
+                    uint32_t* own = color ? c0 + W : c0;
+                    const uint32_t* oth = color ? c0 : c0 + W;
+                    int sS = 0, sB = 0;
+                    for (int w = lane; w < W; w += 32)
+                        resident_word<kMode, kFerro>(A, own, oth, w, color, s_slot[li], ctr1, sS, sB, st,
+                                                     kFerro ? s_mask[li] : nullptr, wr_shift);
+                    if (st) {
+                        for (int o = 16; o > 0; o >>= 1) {
+                            sS += __shfl_down_sync(0xffffffffu, sS, o);
+                            sB += __shfl_down_sync(0xffffffffu, sB, o);
+                        }
+                        if (lane == 0) {
+                            s_S[li] += sS;
+                            s_B[li] += sB;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+            if (need_stats) __syncthreads();  // every lattice's stats before the publish
+        } else
         for (int color = 0; color < 2; ++color) {
             const uint32_t ctr1 = (uint32_t)(2 * t + color);
             const bool st = color == 1 && need_stats;
@@ -333,7 +365,10 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
                 pub[2 * k + 1] = Bd;
             }
         }
-        if (!exch) continue;
+        if (!exch) {
+            if (!kCl && A.warp_lat) __syncthreads();  // the publish zeroed s_S before the next accumulation
+            continue;
+        }
         // every lattice's (S, Bond) is published.  (A point-to-point flag
         // scheme without this barrier was measured slower: DESIGN.md 5.)
         cg::this_grid().sync();
@@ -403,8 +438,15 @@ static int launch_resident_t(const ResidentArgs& a, int sms, cudaStream_t s) {
     // does the same number of words per colour (no tail warps at the barrier)
     const int64_t items = (int64_t)((a.R * cs + grid - 1) / grid) * a.W / cs;
     const int64_t trips = (items + kThreads - 1) / kThreads;
-    const int threads = (int)std::min<int64_t>(kThreads, (((items + trips - 1) / trips) + 31) & ~31);
+    int threads = (int)std::min<int64_t>(kThreads, (((items + trips - 1) / trips) + 31) & ~31);
     ResidentArgs args = a;
+    // warp-owned lattices when a lattice is at most 2 words per lane per
+    // colour and the CTA's lattices fit its warps (C5: 28 lattices of 64
+    // words per CTA); PTMH_RESIDENT_WARPLAT=0 turns it off (A/B)
+    const char* ew = getenv("PTMH_RESIDENT_WARPLAT");
+    const int nl_max = (a.R + grid - 1) / grid;
+    args.warp_lat = cs == 1 && !(ew && ew[0] == '0') && a.W <= 64 && nl_max <= kThreads / 32;
+    if (args.warp_lat) threads = 32 * nl_max;
     void* kargs[] = {&args};
     if (cs == 1) {
         PTMH_CUDA(cudaLaunchCooperativeKernel((const void*)cb_resident_kernel<kMode, kFerro, kThreads, false>, grid,
