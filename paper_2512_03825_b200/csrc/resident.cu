@@ -225,6 +225,8 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
     __shared__ int s_slot[kMaxLatPerBlock];
     __shared__ int s_S[kMaxLatPerBlock], s_B[kMaxLatPerBlock];
     __shared__ double s_u[kMaxLatPerBlock];
+    __shared__ double s_bd[kMaxLatPerBlock];       // beta_i - beta_j of the slot's pair (this round)
+    __shared__ uint32_t s_pt[kMaxLatPerBlock][2];  // thresholds t3, t4 of the partner slot (ferro)
     __shared__ uint32_t s_mask[kFerro ? kMaxLatPerBlock : 1][18];  // TM[8], TC[8], t3, t4
     cg::cluster_group cluster = cg::this_cluster();
     const int cs = kCl ? (int)cluster.num_blocks() : 1;
@@ -344,10 +346,23 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
         int64_t* pub = A.slot_stats + (round & 1) * 2 * (int64_t)R;
         for (int i = threadIdx.x; i < nl; i += blockDim.x) {
             const int k = s_slot[i];
-            if (exch)  // the swap draw depends only on (round, pair): draw it before the barrier
-                s_u[i] = (k >= first && (k - first) / 2 < n_pairs)
-                             ? stream_uniform(A.seed, (uint64_t)(R + (k - first) / 2), (uint64_t)round)
-                             : 0.0;
+            if (exch && k >= first && (k - first) / 2 < n_pairs) {
+                // everything of the round that does not need the partner's
+                // energy, before the barrier: the swap draw (stream R+p,
+                // position = round), the pair's beta difference and the
+                // partner slot's thresholds (their loads overlap the draw)
+                const int pi = (k - first) / 2, si = first + 2 * pi, sj = si + 1;
+                const double bi = A.betas[si], bj = A.betas[sj];
+                const int other = (k == si) ? sj : si;
+                const uint32_t t3 = kFerro ? __ldg(A.thresh + other * 10 + 8) : 0u;
+                const uint32_t t4 = kFerro ? __ldg(A.thresh + other * 10 + 9) : 0u;
+                s_u[i] = stream_uniform(A.seed, (uint64_t)(R + pi), (uint64_t)round);
+                s_bd[i] = __dsub_rn(bi, bj);
+                s_pt[i][0] = t3;
+                s_pt[i][1] = t4;
+            } else if (exch) {
+                s_u[i] = 0.0;
+            }
             if (!owner) continue;
             const long long S = s_S[i], Bd = s_B[i];
             s_S[i] = 0;
@@ -383,7 +398,7 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
                 const double Ei = __dsub_rn(__dmul_rn(A.B, (double)pub[2 * i]), __dmul_rn(A.J, (double)pub[2 * i + 1]));
                 const double Ej = __dsub_rn(__dmul_rn(A.B, (double)pub[2 * j]), __dmul_rn(A.J, (double)pub[2 * j + 1]));
                 const double u = s_u[li];
-                const double x = __dmul_rn(__dsub_rn(A.betas[i], A.betas[j]), __dsub_rn(Ei, Ej));
+                const double x = __dmul_rn(s_bd[li], __dsub_rn(Ei, Ej));
                 double prob;
                 if (x >= 0.0) {
                     prob = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-x)));
@@ -404,7 +419,20 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
                 A.r2s[buf ^ 1][r] = nk;
                 A.s2r[buf ^ 1][nk] = r;
             }
-            if (nk != k) resident_set_slot<kFerro>(A, li, nk, s_slot, s_mask);
+            if (nk != k) {
+                s_slot[li] = nk;
+                if (kFerro) {  // resident_set_slot with the prefetched thresholds
+                    const uint32_t t3 = s_pt[li][0], t4 = s_pt[li][1];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const uint32_t ta = (t3 >> (31 - q)) & 1u, tb = (t4 >> (31 - q)) & 1u;
+                        s_mask[li][q] = tb - ta;
+                        s_mask[li][8 + q] = 0u - ta;
+                    }
+                    s_mask[li][16] = t3;
+                    s_mask[li][17] = t4;
+                }
+            }
         }
         buf ^= 1;
         __syncthreads();  // next sweep reads s_slot / s_mask
