@@ -545,8 +545,19 @@ __device__ __forceinline__ int win_hash(int site) { return (int)(((uint32_t)site
 #ifndef PTMH_DRAW_MINB
 #define PTMH_DRAW_MINB 3  // 80 registers, no spills (4: 64 + spills, 2% slower)
 #endif
+// A 64 Kbit filter in front of the hash: most of the 5 lookups per attempt
+// (the site and its neighbours) find no attempt of the window there, and the
+// filter answers those without a probe loop -- warp-wide, a probe loop runs as
+// long as its longest lane (~10 iterations at load 1/2).
+constexpr int kWinFilterWords = 2048;
+
+__device__ __forceinline__ uint32_t win_filter_bit(int site) {
+    return ((uint32_t)site * 0x85EBCA6Bu) >> 16;  // 16-bit index
+}
+
 __global__ void __launch_bounds__(256, PTMH_DRAW_MINB) draw_w_kernel(DrawArgs D) {
     __shared__ int h_key[kWinHash], h_val[kWinHash];
+    __shared__ uint32_t s_filter[kWinFilterWords];
     __shared__ double s_tbl[10];
     __shared__ int s_up[10];
     const int64_t nwin = (D.n + kWin - 1) / kWin;
@@ -557,6 +568,7 @@ __global__ void __launch_bounds__(256, PTMH_DRAW_MINB) draw_w_kernel(DrawArgs D)
         h_key[k] = -1;
         h_val[k] = 0x7fffffff;
     }
+    for (int k = threadIdx.x; k < kWinFilterWords; k += blockDim.x) s_filter[k] = 0u;
     if (threadIdx.x < 10) {
         s_tbl[threadIdx.x] = D.tbl[slot * 10 + threadIdx.x];
         s_up[threadIdx.x] = D.dcls[threadIdx.x] > 0.0;
@@ -585,6 +597,8 @@ __global__ void __launch_bounds__(256, PTMH_DRAW_MINB) draw_w_kernel(DrawArgs D)
             if (s_up[cl] && u_acc < s_tbl[cl]) am |= 1u << cl;
         accm[q] = am;
         if (w0 + li < D.n) {  // site -> earliest attempt of the window
+            const uint32_t fb = win_filter_bit(site[q]);
+            atomicOr(&s_filter[fb >> 5], 1u << (fb & 31));
             int h = win_hash(site[q]);
             while (true) {
                 const int old = atomicCAS(&h_key[h], -1, site[q]);
@@ -598,6 +612,8 @@ __global__ void __launch_bounds__(256, PTMH_DRAW_MINB) draw_w_kernel(DrawArgs D)
     }
     __syncthreads();
     auto earliest = [&](int x) -> int {
+        const uint32_t fb = win_filter_bit(x);
+        if (!((s_filter[fb >> 5] >> (fb & 31)) & 1u)) return 0x7fffffff;  // no attempt at x
         int h = win_hash(x);
         while (true) {
             const int k = h_key[h];
