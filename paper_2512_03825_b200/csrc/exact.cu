@@ -533,9 +533,9 @@ __global__ void __launch_bounds__(128) commit_kernel(CommitArgs C) {
 // draw_w_kernel marks dependents (bit 31 of the acceptance mask) with a
 // shared-memory hash of the window's sites -> earliest attempt.
 constexpr int kWin = 1024;
-constexpr int kWinHash = 2048;
+constexpr int kWinHash = 4096;  // load 1/4: short warp-wide probe loops (2048: -18 %)
 
-__device__ __forceinline__ int win_hash(int site) { return (int)(((uint32_t)site * 0x9E3779B1u) >> (32 - 11)); }
+__device__ __forceinline__ int win_hash(int site) { return (int)(((uint32_t)site * 0x9E3779B1u) >> (32 - 12)); }
 
 // The window path's commit needs no 32-window conflict masks (rec_conf is
 // not written).  Per attempt: the two draws, the site (a shift for
