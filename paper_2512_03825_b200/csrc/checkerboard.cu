@@ -850,23 +850,24 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
         // 2n items.  With few lattices (a rank's shard of C3 on 8 GPUs: 32)
         // the phase has too few items to fill the GPU and that path binds:
         // take the largest kRows whose phase still has >= 1 item per CTA
-        // slot (else 4).  Measured on one B200 (attempts/s at L = 1024):
+        // slot (else 2).  Measured on one B200 (attempts/s at L = 1024):
         // R = 256: 16 rows 3.23e12 (8: 2.93e12); R = 64: 8 rows 2.55e12
-        // (16: 2.01e12, 4: 2.38e12); R = 32: 4 rows 2.00e12 (16: 1.18e12).
+        // (16: 2.01e12, 4: 2.38e12); R = 32: 4 rows 2.00e12 (16: 1.18e12,
+        // 2: 1.77e12); R = 16: 2 rows 1.32e12 (4: 1.16e12).
         // (PTMH_PERSIST_ROWS pins it: A/B and tests.)
         const char* er = getenv("PTMH_PERSIST_ROWS");
-        int krows = 4;
+        int krows = 2;
         if (er) {
             krows = atoi(er);
         } else {
-            for (int k : {16, 8}) {
+            for (int k : {16, 8, 4}) {
                 if (rows * (L * L / (256LL * 64 * k)) >= slots) {
                     krows = k;
                     break;
                 }
             }
         }
-        if (krows != 4 && krows != 8 && krows != 16) krows = 16;
+        if (krows != 2 && krows != 4 && krows != 8 && krows != 16) krows = 16;
         // 256-thread blocks per item: amortise the per-item scheduling over
         // several blocks while a phase keeps >= 8 items per resident CTA
         // (PTMH_PERSIST_ITEMS_PER_SLOT overrides the 8; tests use 0 to force
@@ -887,8 +888,11 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
         else if (krows == 8)
             cb_sweeps_persistent<8><<<grid, 256, 0, s>>>(packed, rows, (int)L, WR, W, row_to_slot, thresh, rk,
                                                           c0, np, stats, 4u, sync, (uint32_t)group);
-        else
+        else if (krows == 4)
             cb_sweeps_persistent<4><<<grid, 256, 0, s>>>(packed, rows, (int)L, WR, W, row_to_slot, thresh, rk,
+                                                          c0, np, stats, 4u, sync, (uint32_t)group);
+        else
+            cb_sweeps_persistent<2><<<grid, 256, 0, s>>>(packed, rows, (int)L, WR, W, row_to_slot, thresh, rk,
                                                           c0, np, stats, 4u, sync, (uint32_t)group);
         PTMH_LAUNCH_CHECK();
         return PTMH_OK;
