@@ -386,7 +386,10 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
         }
         // every lattice's (S, Bond) is published.  (A point-to-point flag
         // scheme without this barrier was measured slower: DESIGN.md 5.)
-        cg::this_grid().sync();
+        if (gridDim.x == 1)
+            __syncthreads();  // one CTA owns every lattice: the round needs no grid barrier
+        else
+            cg::this_grid().sync();
         // ---- exchange round: the owner of lattice r decides the pair of its slot
         for (int li = threadIdx.x; li < nl; li += blockDim.x) {
             const int r = lo + li;
@@ -457,7 +460,10 @@ static int launch_resident_t(const ResidentArgs& a, int sms, cudaStream_t s) {
     }
     // enough blocks to fill the GPU, few enough that no block owns more
     // lattices than its shared-memory tables hold
-    const int grid = cs > 1 ? a.R * cs : std::min(a.R, slots);
+    // Tiny runs (C1: 8 lattices of 16 words per colour) go to ONE CTA: its
+    // exchange rounds then need a CTA barrier instead of a grid barrier.
+    const bool one_cta = cs == 1 && (int64_t)a.R * a.W <= 4 * kThreads && a.R <= kMaxLatPerBlock;
+    const int grid = cs > 1 ? a.R * cs : (one_cta ? 1 : std::min(a.R, slots));
     if (cs == 1 && (a.R + grid - 1) / grid > kMaxLatPerBlock) {
         set_error("resident kernel: too many lattices per block for this grid");
         return PTMH_ERR_ARG;
