@@ -237,6 +237,38 @@ int ptmh_cb_run_resident(uint32_t *packed, int64_t R, int64_t L,
                          int64_t total_sweeps, int64_t swap_every,
                          int64_t record_every, int *buf_out, void *stream);
 
+/* ptmh_cb_run_resident over `world` GPUs (one process each): this rank owns
+ * the `rows` lattices of global rows row_lo .. row_lo + rows - 1; slots,
+ * betas, thresholds, observables and slot_to_row2 (2, R_total) range over
+ * R_total.  Each round's (S, Bond) by slot is stored into every rank's
+ * slot_stats (pub_peers[g], peer pointers from ptmh_ipc_open; [rank] =
+ * slot_stats) and signalled through flag_peers[g][rank] (uint32, world
+ * entries per rank, zeroed once per run); no collective library call.  On
+ * return this rank's row_to_slot2 / stats are current; counters, the
+ * observables and slot_to_row2 hold only this rank's part (the caller
+ * combines them).  max_ctas caps the grid (0: fill the GPU). */
+int ptmh_cb_run_resident_sharded(uint32_t *packed, int64_t rows, int64_t L,
+                                 int64_t *slot_to_row2, int32_t *row_to_slot2,
+                                 int buf, const uint32_t *thresh,
+                                 uint32_t always_mask, uint64_t seed, double J,
+                                 double B, const double *betas, int64_t *stats,
+                                 int64_t *slot_stats, int64_t *counters,
+                                 double *obs_e, double *obs_m, int64_t ncols,
+                                 int64_t first_sweep, int64_t n_sweeps,
+                                 int64_t total_sweeps, int64_t swap_every,
+                                 int64_t record_every, int *buf_out,
+                                 int64_t R_total, int rank, int world,
+                                 int64_t row_lo, int64_t *const *pub_peers,
+                                 uint32_t *const *flag_peers, int max_ctas,
+                                 void *stream);
+
+/* CUDA IPC for the peer buffers above: handle_out receives
+ * ptmh_ipc_handle_bytes() bytes. */
+int64_t ptmh_ipc_handle_bytes(void);
+int ptmh_ipc_handle(void *dev_ptr, void *handle_out);
+int ptmh_ipc_open(const void *handle, void **dev_ptr_out);
+int ptmh_ipc_close(void *dev_ptr);
+
 /* Per-lattice (S, Bond) recomputed from the packed state (audit of the
  * incremental stats; L % 64 == 0 or any even L). */
 int ptmh_cb_row_stats(const uint32_t *packed, int64_t rows, int64_t L,

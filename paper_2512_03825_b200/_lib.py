@@ -65,6 +65,13 @@ def _load():
         "ptmh_cb_unpack_slots": ([P, P, i64, i64, P, P], i32),
         "ptmh_cb_run_resident": ([P, i64, i64, P, P, i32, P, u32, u64, f64, f64, P, P, P, P, P,
                                   P, i64, i64, i64, i64, i64, i64, P, P], i32),
+        "ptmh_cb_run_resident_sharded": ([P, i64, i64, P, P, i32, P, u32, u64, f64, f64, P, P, P, P, P,
+                                          P, i64, i64, i64, i64, i64, i64, P, i64, i32, i32, i64, P, P,
+                                          i32, P], i32),
+        "ptmh_ipc_handle_bytes": ([], i64),
+        "ptmh_ipc_handle": ([P, P], i32),
+        "ptmh_ipc_open": ([P, P], i32),
+        "ptmh_ipc_close": ([P], i32),
         "ptmh_cb_slot_energies": ([P, P, i64, f64, f64, P, P, P], i32),
         "ptmh_cb_observe": ([P, P, i64, i64, f64, f64, P, P, i64, i64, P], i32),
     }

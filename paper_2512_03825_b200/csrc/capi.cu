@@ -286,12 +286,14 @@ int ptmh_cb_sweeps_sync(uint32_t* packed, int64_t rows, int64_t L, const int32_t
                             stats, as_stream(stream), sync);
 }
 
-int ptmh_cb_run_resident(uint32_t* packed, int64_t R, int64_t L, int64_t* slot_to_row2, int32_t* row_to_slot2,
-                         int buf, const uint32_t* thresh, uint32_t always_mask, uint64_t seed, double J, double B,
-                         const double* betas, int64_t* stats, int64_t* slot_stats, int64_t* counters,
-                         double* obs_e, double* obs_m, int64_t ncols, int64_t first_sweep, int64_t n_sweeps,
-                         int64_t total_sweeps,
-                         int64_t swap_every, int64_t record_every, int* buf_out, void* stream) {
+static int run_resident_impl(uint32_t* packed, int64_t R, int64_t L, int64_t* slot_to_row2,
+                             int32_t* row_to_slot2, int buf, const uint32_t* thresh, uint32_t always_mask,
+                             uint64_t seed, double J, double B, const double* betas, int64_t* stats,
+                             int64_t* slot_stats, int64_t* counters, double* obs_e, double* obs_m, int64_t ncols,
+                             int64_t first_sweep, int64_t n_sweeps, int64_t total_sweeps, int64_t swap_every,
+                             int64_t record_every, int* buf_out, void* stream, int64_t R_total, int rank,
+                             int world, int64_t row_lo, int64_t* const* pub_peers, uint32_t* const* flag_peers,
+                             int max_ctas) {
     PTMH_CHECK_ARG(L >= 2 && L % 2 == 0 && L <= 65536 && R >= 1 && R < (1LL << 26), "resident shape");
     PTMH_CHECK_ARG(buf == 0 || buf == 1, "resident buffer index");
     PTMH_CHECK_ARG(slot_stats != nullptr || swap_every == 0, "resident slot_stats scratch");
@@ -299,6 +301,8 @@ int ptmh_cb_run_resident(uint32_t* packed, int64_t R, int64_t L, int64_t* slot_t
                        total_sweeps < (1LL << 31), "resident sweep range");
     PTMH_CHECK_ARG(record_every == 0 || (obs_e && obs_m && total_sweeps / record_every <= ncols),
                    "resident observables");
+    PTMH_CHECK_ARG(world >= 1 && world <= 8 && rank >= 0 && rank < world && R_total >= R && row_lo >= 0 &&
+                       row_lo + R <= R_total, "resident sharding");
     ResidentArgs a{};
     a.packed = packed;
     a.R = (int)R;
@@ -312,7 +316,7 @@ int ptmh_cb_run_resident(uint32_t* packed, int64_t R, int64_t L, int64_t* slot_t
     a.B = B;
     a.betas = betas;
     a.s2r[0] = slot_to_row2;
-    a.s2r[1] = slot_to_row2 + R;
+    a.s2r[1] = slot_to_row2 + R_total;
     a.r2s[0] = row_to_slot2;
     a.r2s[1] = row_to_slot2 + R;
     a.stats = stats;
@@ -327,6 +331,16 @@ int ptmh_cb_run_resident(uint32_t* packed, int64_t R, int64_t L, int64_t* slot_t
     a.swap_every = swap_every;
     a.record_every = record_every;
     a.buf = buf;
+    a.world = world;
+    a.rank = rank;
+    a.R_total = (int)R_total;
+    a.row_lo = row_lo;
+    a.max_ctas = max_ctas;
+    for (int g = 0; g < world && world > 1; ++g) {
+        PTMH_CHECK_ARG(pub_peers && flag_peers && pub_peers[g] && flag_peers[g], "resident peer buffers");
+        a.pub_peer[g] = pub_peers[g];
+        a.flag_peer[g] = flag_peers[g];
+    }
     fill_class_plan(always_mask, &a.n_up, a.up_k, a.up_sf, a.up_cls, &a.ferro);
     int rounds = 0;
     for (int64_t d = first_sweep + 1; d <= first_sweep + n_sweeps; ++d)
@@ -335,6 +349,57 @@ int ptmh_cb_run_resident(uint32_t* packed, int64_t R, int64_t L, int64_t* slot_t
     if (n_sweeps == 0) return PTMH_OK;
     return launch_cb_resident(a, a.WR > 0, as_stream(stream), nullptr);
 }
+
+int ptmh_cb_run_resident(uint32_t* packed, int64_t R, int64_t L, int64_t* slot_to_row2, int32_t* row_to_slot2,
+                         int buf, const uint32_t* thresh, uint32_t always_mask, uint64_t seed, double J, double B,
+                         const double* betas, int64_t* stats, int64_t* slot_stats, int64_t* counters,
+                         double* obs_e, double* obs_m, int64_t ncols, int64_t first_sweep, int64_t n_sweeps,
+                         int64_t total_sweeps,
+                         int64_t swap_every, int64_t record_every, int* buf_out, void* stream) {
+    return run_resident_impl(packed, R, L, slot_to_row2, row_to_slot2, buf, thresh, always_mask, seed, J, B, betas,
+                             stats, slot_stats, counters, obs_e, obs_m, ncols, first_sweep, n_sweeps, total_sweeps,
+                             swap_every, record_every, buf_out, stream, R, 0, 1, 0, nullptr, nullptr, 0);
+}
+
+int ptmh_cb_run_resident_sharded(uint32_t* packed, int64_t rows, int64_t L, int64_t* slot_to_row2,
+                                 int32_t* row_to_slot2, int buf, const uint32_t* thresh, uint32_t always_mask,
+                                 uint64_t seed, double J, double B, const double* betas, int64_t* stats,
+                                 int64_t* slot_stats, int64_t* counters, double* obs_e, double* obs_m,
+                                 int64_t ncols, int64_t first_sweep, int64_t n_sweeps, int64_t total_sweeps,
+                                 int64_t swap_every, int64_t record_every, int* buf_out, int64_t R_total,
+                                 int rank, int world, int64_t row_lo, int64_t* const* pub_peers,
+                                 uint32_t* const* flag_peers, int max_ctas, void* stream) {
+    return run_resident_impl(packed, rows, L, slot_to_row2, row_to_slot2, buf, thresh, always_mask, seed, J, B,
+                             betas, stats, slot_stats, counters, obs_e, obs_m, ncols, first_sweep, n_sweeps,
+                             total_sweeps, swap_every, record_every, buf_out, stream, R_total, rank, world, row_lo,
+                             pub_peers, flag_peers, max_ctas);
+}
+
+// CUDA IPC (one process per GPU): a device allocation's handle, opened as a
+// peer pointer by the other ranks (NVLink peer memory for the resident
+// kernel's round exchange).
+int ptmh_ipc_handle(void* dev_ptr, void* handle_out) {
+    PTMH_CHECK_ARG(dev_ptr && handle_out, "ipc handle");
+    cudaIpcMemHandle_t h;
+    PTMH_CUDA(cudaIpcGetMemHandle(&h, dev_ptr));
+    std::memcpy(handle_out, &h, sizeof(h));
+    return PTMH_OK;
+}
+
+int ptmh_ipc_open(const void* handle, void** dev_ptr_out) {
+    PTMH_CHECK_ARG(handle && dev_ptr_out, "ipc open");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    PTMH_CUDA(cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+    return PTMH_OK;
+}
+
+int ptmh_ipc_close(void* dev_ptr) {
+    PTMH_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+    return PTMH_OK;
+}
+
+int64_t ptmh_ipc_handle_bytes(void) { return (int64_t)sizeof(cudaIpcMemHandle_t); }
 
 int ptmh_cb_unpack_slots(const uint32_t* packed, const int64_t* slot_to_row, int64_t R, int64_t L,
                          int8_t* out, void* stream) {

@@ -90,6 +90,16 @@ struct ResidentArgs {
     int ferro;
     uint32_t seg_lo, seg_even;  // L in {8, 16, 32}: bit 0 of each row segment, even-row segments
     int warp_lat;               // launcher-set: each warp owns whole lattices (no CTA barrier per colour)
+    // Sharded across GPUs (world > 1): R above counts this rank's lattices
+    // (global rows row_lo ..), slots and pairs range over R_total.  Each
+    // round's (S, Bond) by slot goes to every rank's pub buffer (peer memory
+    // over NVLink), then one flag per (source rank) in every rank's flags
+    // array; a rank proceeds when all flags reached round + 1.
+    int world, rank, R_total;
+    int64_t row_lo;
+    int64_t* pub_peer[8];    // slot_stats (2, R_total, 2) of every rank (peer pointers), [rank] = own
+    uint32_t* flag_peer[8];  // flags (world) of every rank, [rank] = own
+    int max_ctas;            // 0 = fill the GPU (tests cap it to co-run virtual ranks on one GPU)
 };
 int launch_cb_resident(const ResidentArgs& a, bool fast, cudaStream_t s, int* grid_out);
 void fill_class_plan(uint32_t always_mask, int* n_up, int* k, int* sf, int* cls, int* ferro);

@@ -236,9 +236,10 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
     int* s_B0 = kCl ? cluster.map_shared_rank(s_B, 0) : s_B;
     const bool owner = crank == 0;
     const int wr_shift = (A.WR > 0 && (A.WR & (A.WR - 1)) == 0) ? __ffs(A.WR) - 1 : -1;
-    const int R = A.R, W = A.W;
-    const int lo = (int)((int64_t)R * cid / ncl);
-    const int hi = (int)((int64_t)R * (cid + 1) / ncl);
+    const int W = A.W;
+    const int R = A.world > 1 ? A.R_total : A.R;  // slots (pairs, swap streams, pub indices)
+    const int lo = (int)((int64_t)A.R * cid / ncl);  // this CTA's (local) lattices
+    const int hi = (int)((int64_t)A.R * (cid + 1) / ncl);
     const int nl = hi - lo;
     // this CTA's slice [ib, ib + items) of the cluster's (lattice, word) items
     const int ib = (int)((int64_t)nl * W * crank / cs);
@@ -378,6 +379,12 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
                 // the exchange reads (S, Bond) by slot: one load per partner
                 pub[2 * k] = S;
                 pub[2 * k + 1] = Bd;
+                for (int g = 0; g < A.world; ++g) {  // sharded: every other rank's copy (NVLink peer stores)
+                    if (g == A.rank) continue;
+                    int64_t* pg = A.pub_peer[g] + (round & 1) * 2 * (int64_t)R;
+                    pg[2 * k] = S;
+                    pg[2 * k + 1] = Bd;
+                }
             }
         }
         if (!exch) {
@@ -386,10 +393,32 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
         }
         // every lattice's (S, Bond) is published.  (A point-to-point flag
         // scheme without this barrier was measured slower: DESIGN.md 5.)
-        if (gridDim.x == 1)
-            __syncthreads();  // one CTA owns every lattice: the round needs no grid barrier
-        else
+        if (A.world > 1) {
+            // every rank's (S, Bond) is published here when all ranks' flags
+            // for this round arrived: publishers fence at system scope, the
+            // grid barrier collects them, one thread signals every rank and
+            // waits for every rank, a second grid barrier releases the CTAs
+            __threadfence_system();
             cg::this_grid().sync();
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                const uint32_t want = (uint32_t)(round + 1);
+                for (int g = 0; g < A.world; ++g)
+                    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(A.flag_peer[g] + A.rank), "r"(want)
+                                 : "memory");
+                for (int g = 0; g < A.world; ++g) {
+                    uint32_t v;
+                    do {
+                        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(A.flag_peer[A.rank] + g)
+                                     : "memory");
+                    } while ((int32_t)(v - want) < 0);
+                }
+            }
+            cg::this_grid().sync();
+        } else if (gridDim.x == 1) {
+            __syncthreads();  // one CTA owns every lattice: the round needs no grid barrier
+        } else {
+            cg::this_grid().sync();
+        }
         // ---- exchange round: the owner of lattice r decides the pair of its slot
         for (int li = threadIdx.x; li < nl; li += blockDim.x) {
             const int r = lo + li;
@@ -420,7 +449,7 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
             // the permutation is an output only: nothing in the launch reads it back
             if (owner) {
                 A.r2s[buf ^ 1][r] = nk;
-                A.s2r[buf ^ 1][nk] = r;
+                A.s2r[buf ^ 1][nk] = A.row_lo + r;  // sharded: only the slots held here
             }
             if (nk != k) {
                 s_slot[li] = nk;
@@ -447,7 +476,7 @@ static int launch_resident_t(const ResidentArgs& a, int sms, cudaStream_t s) {
     int per_sm = 0;
     PTMH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
         &per_sm, cb_resident_kernel<kMode, kFerro, kThreads, false>, kThreads, 0));
-    const int slots = sms * std::max(1, per_sm);
+    const int slots = a.max_ctas > 0 ? std::min(a.max_ctas, sms * std::max(1, per_sm)) : sms * std::max(1, per_sm);
     // Fewer lattices than CTA slots and enough words per lattice: a cluster
     // of cs CTAs owns each lattice (C2: 64 lattices of 2048 words per colour
     // on 128 SMs instead of 64).  PTMH_RESIDENT_CLUSTER=1 turns it off.

@@ -267,6 +267,36 @@ class CheckerboardEngine(_Base):
         self.slot_to_row.copy_(self._s2r2[out.value])
         self.row_to_slot.copy_(self._r2s2[out.value])
 
+    def run_resident_sharded(self, first_sweep: int, n_sweeps: int, total_sweeps: int, swap_every: int,
+                             rank: int, world: int, pub_peers, flag_peers, slot_stats: torch.Tensor,
+                             record_every: int = 0, obs_e=None, obs_m=None, max_ctas: int = 0) -> None:
+        """One rank's part of a resident run over `world` GPUs (the local rows
+        only); rounds exchange (S, Bond) through peer memory and flags
+        (csrc/resident.cu).  pub_peers / flag_peers: device pointers (ints) of
+        every rank's slot_stats (2, R, 2) int64 and flags (world,) uint32,
+        [rank] = this rank's own.  Afterwards the local rows' slots are in
+        row_to_slot[row_lo:row_hi]; counters, observables and slot_to_row hold
+        this rank's part (ShardedCheckerboard combines them)."""
+        if getattr(self, "_r2s2_loc", None) is None:
+            self._s2r2_g = torch.empty((2, self.R), dtype=torch.int64, device=self.dev)
+            self._r2s2_loc = torch.empty((2, max(1, self.rows)), dtype=torch.int32, device=self.dev)
+        self._s2r2_g[0].copy_(self.slot_to_row)
+        self._r2s2_loc[0, :self.rows].copy_(self.row_to_slot[self.row_lo:self.row_hi])
+        out = ctypes.c_int(0)
+        ncols = obs_e.shape[1] if obs_e is not None else 0
+        pubs = (ctypes.c_void_p * world)(*[int(x) for x in pub_peers])
+        flags = (ctypes.c_void_p * world)(*[int(x) for x in flag_peers])
+        # (everything runs on the current stream: co-running ranks on one GPU
+        # in the tests each use their own)
+        _lib.call("ptmh_cb_run_resident_sharded", _P(self.packed), self.rows, self.L, _P(self._s2r2_g),
+                  _P(self._r2s2_loc), 0, _P(self.thr), self.always, self.seed, self.J, self.B,
+                  _P(self.betas), _P(self.local_stats), _P(slot_stats), _P(self.counters), _P(obs_e),
+                  _P(obs_m), ncols, first_sweep, n_sweeps, total_sweeps, swap_every, record_every,
+                  ctypes.byref(out), self.R, rank, world, self.row_lo, ctypes.cast(pubs, ctypes.c_void_p),
+                  ctypes.cast(flags, ctypes.c_void_p), max_ctas, self._s())
+        self.row_to_slot[self.row_lo:self.row_hi].copy_(self._r2s2_loc[out.value, :self.rows])
+        self.slot_to_row.copy_(self._s2r2_g[out.value])
+
     def observe(self, obs_e: torch.Tensor, obs_m: torch.Tensor, col: int) -> None:
         _lib.call("ptmh_cb_observe", _P(self.stats), _P(self.slot_to_row), self.R, self.L,
                   self.J, self.B, _P(obs_e), _P(obs_m), obs_e.shape[1], col, self._s())

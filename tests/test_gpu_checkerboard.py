@@ -334,3 +334,46 @@ def test_host_interval_plugin_at_1024(mods, monkeypatch, plugin_sync):
         prev = eng.swap_counts()[0]
         assert np.array_equal(sp, eng.final_spins())
         assert np.array_equal(s2r, eng.slot_to_row.cpu().numpy())
+
+
+@pytest.mark.parametrize("L,R,G,total,every,rec", [(64, 24, 2, 30, 1, 1), (64, 37, 3, 20, 2, 2),
+                                                   (16, 40, 4, 25, 1, 5)])
+def test_resident_sharded_virtual_ranks(mods, L, R, G, total, every, rec):
+    """The multi-GPU resident kernel (rounds exchanged through peer memory
+    and flags, no collective) with G ranks co-running on ONE GPU, each on its
+    own stream and a share of the SMs: after combining the ranks' parts it is
+    the single-GPU resident run, bit for bit."""
+    p, engine, _, _ = mods
+    from paper_2512_03825_b200.executor import assign_replicas
+    temps, seed = p.build_ladder(R), 31
+    ncols = total // rec
+    ref = engine.CheckerboardEngine(L, R, temps, seed, 1.0, 0.0, 0.5, 0)
+    ref.init_state()
+    roe = torch.zeros((R, ncols), dtype=torch.float64, device="cuda")
+    rom = torch.zeros_like(roe)
+    ref.run_resident(0, total, total, every, record_every=rec, obs_e=roe, obs_m=rom)
+    bounds = assign_replicas(R, G)
+    engs = [engine.CheckerboardEngine(L, R, temps, seed, 1.0, 0.0, 0.5, 0, row_range=b) for b in bounds]
+    for e in engs:
+        e.init_state()
+    pubs = [torch.zeros((2, R, 2), dtype=torch.int64, device="cuda") for _ in range(G)]
+    flags = [torch.zeros(G, dtype=torch.int32, device="cuda") for _ in range(G)]
+    oes = [torch.zeros((R, ncols), dtype=torch.float64, device="cuda") for _ in range(G)]
+    oms = [torch.zeros_like(o) for o in oes]
+    streams = [torch.cuda.Stream() for _ in range(G)]
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    torch.cuda.synchronize()
+    for g, e in enumerate(engs):
+        with torch.cuda.stream(streams[g]):
+            e.run_resident_sharded(0, total, total, every, g, G, [t.data_ptr() for t in pubs],
+                                   [f.data_ptr() for f in flags], pubs[g], record_every=rec, obs_e=oes[g],
+                                   obs_m=oms[g], max_ctas=sms // G - 2)
+    torch.cuda.synchronize()
+    r2s = np.concatenate([e.row_to_slot[e.row_lo:e.row_hi].cpu().numpy() for e in engs])
+    assert np.array_equal(r2s, ref.row_to_slot.cpu().numpy())
+    spins = np.concatenate([e.final_spins() for e in engs])
+    assert np.array_equal(spins, ref.final_spins())
+    stats = np.concatenate([e.local_stats.cpu().numpy() for e in engs])
+    assert np.array_equal(stats, ref.local_stats.cpu().numpy())
+    assert sum(e.swap_counts()[0] for e in engs) == ref.swap_counts()[0]
+    assert torch.equal(sum(oes), roe) and torch.equal(sum(oms), rom)
