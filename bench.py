@@ -257,6 +257,13 @@ def main():
     clk = ClockSampler(local_rank)
     sharded = world > 1 or args.sharded
     if sharded:
+        if "RANK" not in os.environ:  # --sharded without torchrun: a world of one
+            import socket
+            with socket.socket() as so:
+                so.bind(("127.0.0.1", 0))
+                port = so.getsockname()[1]
+            os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
+                              MASTER_PORT=str(port))
         dist.init_process_group("nccl", device_id=dev)
     temps = geometric_ladder(R) if args.config == "c1" else build_ladder(R)
     if sharded:
@@ -273,7 +280,15 @@ def main():
 
     state = {"sweep": 0, "round": 0}
     from paper_2512_03825_b200.executor import _resident_wins
-    resident = not sharded and _resident_wins(L, every)
+    # small lattices, exchange every sweep: one persistent launch per step;
+    # across GPUs the rounds go through peer memory (distributed.PeerBuffers)
+    resident = _resident_wins(L, every)
+    peers = None
+    if sharded and resident:
+        from paper_2512_03825_b200.distributed import PeerBuffers, resident_sharded
+        peers = PeerBuffers(R, dev)
+        config["parallelism"] = (f"rows sharded over {world} GPU(s), exchange rounds through peer "
+                                 f"memory (CUDA IPC, no collective)")
     # the engine's sweeps() takes the one-launch persistent path here
     # (csrc/checkerboard.cu: cb_sweeps_persistent, J > 0, B = 0, L % 512 == 0)
     persistent = not resident and eng.persistent and L >= 1024 and L % 512 == 0
@@ -284,7 +299,10 @@ def main():
         if resident:  # one persistent launch = `ips` intervals, sweeps + exchange rounds
             if sweep_events is not None:
                 sweep_events[0][0].record(stream)
-            eng.run_resident(t0, every * ips, big, every)
+            if peers is not None:
+                resident_sharded(drv, peers, t0, every * ips, big, every)
+            else:
+                eng.run_resident(t0, every * ips, big, every)
             if sweep_events is not None:
                 sweep_events[0][1].record(stream)
             state["sweep"] += every * ips

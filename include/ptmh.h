@@ -268,6 +268,10 @@ int64_t ptmh_ipc_handle_bytes(void);
 int ptmh_ipc_handle(void *dev_ptr, void *handle_out);
 int ptmh_ipc_open(const void *handle, void **dev_ptr_out);
 int ptmh_ipc_close(void *dev_ptr);
+/* zeroed cudaMalloc allocation for IPC-shared buffers (a handle names a whole
+ * allocation, not a sub-block of a caching allocator's segment) */
+int ptmh_peer_alloc(int64_t bytes, void **dev_ptr_out);
+int ptmh_peer_free(void *dev_ptr);
 
 /* Per-lattice (S, Bond) recomputed from the packed state (audit of the
  * incremental stats; L % 64 == 0 or any even L). */

@@ -72,6 +72,8 @@ def _load():
         "ptmh_ipc_handle": ([P, P], i32),
         "ptmh_ipc_open": ([P, P], i32),
         "ptmh_ipc_close": ([P], i32),
+        "ptmh_peer_alloc": ([i64, P], i32),
+        "ptmh_peer_free": ([P], i32),
         "ptmh_cb_slot_energies": ([P, P, i64, f64, f64, P, P, P], i32),
         "ptmh_cb_observe": ([P, P, i64, i64, f64, f64, P, P, i64, i64, P], i32),
     }

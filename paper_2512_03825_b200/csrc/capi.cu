@@ -401,6 +401,21 @@ int ptmh_ipc_close(void* dev_ptr) {
 
 int64_t ptmh_ipc_handle_bytes(void) { return (int64_t)sizeof(cudaIpcMemHandle_t); }
 
+// A dedicated, zeroed device allocation for buffers shared over IPC: a handle
+// names a whole cudaMalloc allocation, so a sub-block of a caching allocator's
+// segment (a torch tensor) would be opened at the segment's base.
+int ptmh_peer_alloc(int64_t bytes, void** dev_ptr_out) {
+    PTMH_CHECK_ARG(bytes > 0 && dev_ptr_out, "peer alloc");
+    PTMH_CUDA(cudaMalloc(dev_ptr_out, (size_t)bytes));
+    PTMH_CUDA(cudaMemset(*dev_ptr_out, 0, (size_t)bytes));
+    return PTMH_OK;
+}
+
+int ptmh_peer_free(void* dev_ptr) {
+    PTMH_CUDA(cudaFree(dev_ptr));
+    return PTMH_OK;
+}
+
 int ptmh_cb_unpack_slots(const uint32_t* packed, const int64_t* slot_to_row, int64_t R, int64_t L,
                          int8_t* out, void* stream) {
     PTMH_CHECK_ARG(L >= 2 && L % 2 == 0 && R >= 0, "cb_unpack_slots shape");

@@ -14,6 +14,8 @@ the permutation stays identical everywhere without a second collective.
 
 from __future__ import annotations
 
+import ctypes
+
 import torch
 import torch.distributed as dist
 
@@ -68,3 +70,93 @@ class ShardedCheckerboard:
             return 0
         self.gather_stats()
         return self.eng.exchange(round_index)
+
+
+class PeerBuffers:
+    """Every rank's round buffers, reachable from every other rank: each rank
+    allocates its slot_stats (2, R, 2) int64 and flags (world,) uint32, shares
+    CUDA IPC handles over the process group (one all_gather_object at setup)
+    and opens the peers' buffers -- NVLink peer memory between the GPUs of a
+    node.  Used by the multi-GPU resident kernel (csrc/resident.cu)."""
+
+    def __init__(self, R: int, device, group=None):
+        from . import _lib
+
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        # own cudaMalloc allocations (an IPC handle names a whole allocation)
+        self._own = []
+        for nbytes in (2 * R * 2 * 8, 4 * self.world):
+            p = ctypes.c_void_p()
+            with torch.cuda.device(device):
+                _lib.call("ptmh_peer_alloc", nbytes, ctypes.byref(p))
+            self._own.append(p.value)
+        self.slot_stats, self.flags = self._own  # device pointers
+        nb = int(_lib.LIB.ptmh_ipc_handle_bytes())
+        mine = []
+        for ptr in self._own:
+            h = (ctypes.c_char * nb)()
+            _lib.call("ptmh_ipc_handle", ptr, h)
+            mine.append(bytes(h))
+        allh = [None] * self.world
+        dist.all_gather_object(allh, mine, group=group)
+        self._opened = []
+        self.pub_peers, self.flag_peers = [], []
+        for g in range(self.world):
+            if g == self.rank:
+                self.pub_peers.append(self.slot_stats)
+                self.flag_peers.append(self.flags)
+                continue
+            ptrs = []
+            for hb in allh[g]:
+                p = ctypes.c_void_p()
+                _lib.call("ptmh_ipc_open", ctypes.create_string_buffer(hb, nb), ctypes.byref(p))
+                ptrs.append(p.value)
+                self._opened.append(p.value)
+            self.pub_peers.append(ptrs[0])
+            self.flag_peers.append(ptrs[1])
+
+    def close(self) -> None:
+        from . import _lib
+
+        for p in self._opened:
+            _lib.call("ptmh_ipc_close", p)
+        self._opened = []
+        for p in self._own:
+            _lib.call("ptmh_peer_free", p)
+        self._own = []
+
+
+def resident_sharded(drv: "ShardedCheckerboard", peers: PeerBuffers, first_sweep: int, n_sweeps: int,
+                     total_sweeps: int, swap_every: int, record_every: int = 0, obs_e=None,
+                     obs_m=None) -> None:
+    """A resident run segment over the ranks of drv.group: one launch per
+    rank, rounds through peer memory; then the ranks' parts are combined
+    (all_gather of the local rows' slots, all_reduce of the swap counters and
+    of the observables, which each rank wrote for the slots it held)."""
+    eng = drv.eng
+    lo, hi = drv.bounds[drv.rank]
+    before = eng.counters.clone()
+    eng.run_resident_sharded(first_sweep, n_sweeps, total_sweeps, swap_every, drv.rank, drv.world,
+                             peers.pub_peers, peers.flag_peers, peers.slot_stats,
+                             record_every=record_every, obs_e=obs_e, obs_m=obs_m)
+    loc = torch.zeros(drv.maxc, dtype=torch.int32, device=eng.stats.device)
+    loc[: hi - lo].copy_(eng.row_to_slot[lo:hi])
+    allr = torch.empty(drv.world * drv.maxc, dtype=torch.int32, device=loc.device)
+    dist.all_gather_into_tensor(allr, loc, group=drv.group)
+    for g, (l, h) in enumerate(drv.bounds):
+        eng.row_to_slot[l:h].copy_(allr[g * drv.maxc: g * drv.maxc + (h - l)])
+    eng.slot_to_row[eng.row_to_slot.long()] = torch.arange(eng.R, dtype=torch.int64, device=loc.device)
+    delta = eng.counters - before  # this segment's counts on this rank
+    dist.all_reduce(delta, group=drv.group)
+    eng.counters.copy_(before + delta)
+    if obs_e is not None and record_every > 0:
+        # the columns recorded in this segment; each slot's entry was
+        # written by the rank holding it, the others hold zeros
+        c0, c1 = first_sweep // record_every, (first_sweep + n_sweeps) // record_every
+        if c1 > c0:
+            for o in (obs_e, obs_m):
+                part = o[:, c0:c1].contiguous()
+                dist.all_reduce(part, group=drv.group)
+                o[:, c0:c1].copy_(part)

@@ -268,7 +268,7 @@ class CheckerboardEngine(_Base):
         self.row_to_slot.copy_(self._r2s2[out.value])
 
     def run_resident_sharded(self, first_sweep: int, n_sweeps: int, total_sweeps: int, swap_every: int,
-                             rank: int, world: int, pub_peers, flag_peers, slot_stats: torch.Tensor,
+                             rank: int, world: int, pub_peers, flag_peers, slot_stats,
                              record_every: int = 0, obs_e=None, obs_m=None, max_ctas: int = 0) -> None:
         """One rank's part of a resident run over `world` GPUs (the local rows
         only); rounds exchange (S, Bond) through peer memory and flags
@@ -290,7 +290,8 @@ class CheckerboardEngine(_Base):
         # in the tests each use their own)
         _lib.call("ptmh_cb_run_resident_sharded", _P(self.packed), self.rows, self.L, _P(self._s2r2_g),
                   _P(self._r2s2_loc), 0, _P(self.thr), self.always, self.seed, self.J, self.B,
-                  _P(self.betas), _P(self.local_stats), _P(slot_stats), _P(self.counters), _P(obs_e),
+                  _P(self.betas), _P(self.local_stats),
+                  slot_stats if isinstance(slot_stats, int) else _P(slot_stats), _P(self.counters), _P(obs_e),
                   _P(obs_m), ncols, first_sweep, n_sweeps, total_sweeps, swap_every, record_every,
                   ctypes.byref(out), self.R, rank, world, self.row_lo, ctypes.cast(pubs, ctypes.c_void_p),
                   ctypes.cast(flags, ctypes.c_void_p), max_ctas, self._s())

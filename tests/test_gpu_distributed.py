@@ -42,3 +42,50 @@ def test_sharded_coordinator_over_nccl_world1():
         assert drv.eng.swap_counts()[0] == ref.swaps_accepted
     finally:
         dist.destroy_process_group()
+
+
+def _ipc_worker(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)  # both ranks on the one GPU: CUDA IPC across processes
+    from cuda.bindings import runtime as rt
+    from paper_2512_03825_b200.distributed import PeerBuffers
+    peers = PeerBuffers(5, torch.device("cuda", 0))
+    # every rank writes (rank + 1) * 100 + g into flag slot [rank] of rank g's
+    # buffer, and its rank into row `rank` of every peer's slot_stats[0]
+    src = torch.empty(1, dtype=torch.int32, device="cuda")
+    row = torch.full((2,), rank + 7, dtype=torch.int64, device="cuda")
+    for g in range(world):
+        src.fill_((rank + 1) * 100 + g)
+        torch.cuda.synchronize()
+        err, = rt.cudaMemcpy(peers.flag_peers[g] + 4 * rank, src.data_ptr(), 4,
+                             rt.cudaMemcpyKind.cudaMemcpyDeviceToDevice)
+        assert err == rt.cudaError_t.cudaSuccess, err
+        err, = rt.cudaMemcpy(peers.pub_peers[g] + 16 * rank, row.data_ptr(), 16,
+                             rt.cudaMemcpyKind.cudaMemcpyDeviceToDevice)
+        assert err == rt.cudaError_t.cudaSuccess, err
+    torch.cuda.synchronize()
+    dist.barrier()
+    flags = torch.empty(world, dtype=torch.int32, device="cuda")
+    stats = torch.empty((world, 2), dtype=torch.int64, device="cuda")
+    for dst, ptr, n in ((flags, peers.flags, 4 * world), (stats, peers.slot_stats, 16 * world)):
+        err, = rt.cudaMemcpy(dst.data_ptr(), ptr, n, rt.cudaMemcpyKind.cudaMemcpyDeviceToDevice)
+        assert err == rt.cudaError_t.cudaSuccess, err
+    np.savez(os.path.join(out_dir, f"ipc{rank}.npz"), flags=flags.cpu().numpy(), stats=stats.cpu().numpy())
+    dist.barrier()
+    peers.close()
+    dist.destroy_process_group()
+
+
+def test_peer_buffers_ipc_two_processes(tmp_path):
+    """PeerBuffers: CUDA IPC handles shared over the process group and opened
+    as peer pointers (two processes on the one GPU): every rank's writes land
+    in every other rank's round buffers."""
+    import torch.multiprocessing as mp
+    world = 2
+    mp.spawn(_ipc_worker, args=(world, _port(), str(tmp_path)), nprocs=world, join=True)
+    for g in range(world):
+        d = np.load(tmp_path / f"ipc{g}.npz")
+        assert d["flags"].tolist() == [(r + 1) * 100 + g for r in range(world)]
+        for r in range(world):
+            assert d["stats"][r].tolist() == [r + 7, r + 7]
