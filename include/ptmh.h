@@ -273,6 +273,24 @@ int ptmh_ipc_close(void *dev_ptr);
 int ptmh_peer_alloc(int64_t bytes, void **dev_ptr_out);
 int ptmh_peer_free(void *dev_ptr);
 
+/* The exact chain for iterations start_iter .. start_iter+nsteps-1 of a run
+ * of total_iters, WITH its swap rounds (every swap_every iterations,
+ * executor.py:111-125): draws on the whole GPU, then one CTA per chunk
+ * commits every slot (R <= 32, bit lattices in shared memory) and runs the
+ * rounds in between (csrc/exact.cu, exact_resident_kernel).  slot_to_row,
+ * energies, spin_sums are updated in place; counters += (accepted, near
+ * ties).  Workspace: ptmh_advance_workspace_bytes(R, nsteps).  Bit-exact with
+ * the reference's executor loop. */
+int ptmh_exact_run_resident(uint32_t *bits, int64_t L, int64_t *slot_to_row,
+                            int64_t R, const double *tbl, const double *dcls,
+                            int int_energy, double *energies, int64_t *spin_sums,
+                            uint64_t *positions, int64_t *iters_done,
+                            uint64_t seed, int64_t start_iter, int64_t nsteps,
+                            int64_t swap_every, int64_t total_iters,
+                            const double *betas, int64_t *counters,
+                            double *obs_e, double *obs_m, int64_t ncols,
+                            void *workspace, int64_t ws_bytes, void *stream);
+
 /* Per-lattice (S, Bond) recomputed from the packed state (audit of the
  * incremental stats; L % 64 == 0 or any even L). */
 int ptmh_cb_row_stats(const uint32_t *packed, int64_t rows, int64_t L,

@@ -49,6 +49,8 @@ def _load():
         "ptmh_advance_workspace_bytes": ([i64, i64], i64),
         "ptmh_advance_block_ws": ([P, i64, P, i64, i64, P, P, i32, P, P, P, P, u64, i64, i64,
                                    P, P, i64, P, i64, P], i32),
+        "ptmh_exact_run_resident": ([P, i64, P, i64, P, P, i32, P, P, P, P, u64, i64, i64, i64, i64, P, P,
+                                     P, P, i64, P, i64, P], i32),
         "ptmh_bits_pack": ([P, i64, i64, P, P], i32),
         "ptmh_bits_unpack": ([P, i64, i64, P, P], i32),
         "ptmh_advance_block_bits": ([P, i64, P, i64, i64, P, P, i32, P, P, P, P, u64, i64, i64,

@@ -219,6 +219,23 @@ int ptmh_bits_unpack(const uint32_t* bits, int64_t rows, int64_t L, int8_t* spin
     return launch_bits_unpack(bits, rows, L, spins, as_stream(stream));
 }
 
+int ptmh_exact_run_resident(uint32_t* bits, int64_t L, int64_t* slot_to_row, int64_t R, const double* tbl,
+                            const double* dcls, int int_energy, double* energies, int64_t* spin_sums,
+                            uint64_t* positions, int64_t* iters_done, uint64_t seed, int64_t start_iter,
+                            int64_t nsteps, int64_t swap_every, int64_t total_iters, const double* betas,
+                            int64_t* counters, double* obs_e, double* obs_m, int64_t ncols, void* workspace,
+                            int64_t ws_bytes, void* stream) {
+    PTMH_CHECK_ARG(L >= 2 && L <= 4096 && R >= 1 && R <= 32, "resident exact run: 1 <= R <= 32 slots");
+    PTMH_CHECK_ARG(nsteps >= 0 && start_iter >= 1 && swap_every >= 0 && start_iter + nsteps <= total_iters,
+                   "resident exact run: iteration range");
+    PTMH_CHECK_ARG(obs_e == nullptr || start_iter + nsteps <= ncols, "resident exact run: obs columns");
+    AdvanceArgs a{nullptr, L, slot_to_row, 0, R, tbl, dcls, int_energy, energies, spin_sums,
+                  positions, iters_done, seed, start_iter, nsteps, obs_e, obs_m, ncols,
+                  obs_e ? 1 : 0, nullptr, bits};
+    ExactRounds x{swap_every, total_iters, betas, counters};
+    return launch_advance_2phase(a, workspace, ws_bytes, as_stream(stream), &x);
+}
+
 int ptmh_advance_block_bits(uint32_t* bits, int64_t L, const int64_t* slot_to_row, int64_t lo, int64_t hi,
                             const double* tbl, const double* dcls, int int_energy, double* energies,
                             int64_t* spin_sums, uint64_t* positions, int64_t* iters_done, uint64_t seed,

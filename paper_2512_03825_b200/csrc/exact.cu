@@ -775,6 +775,228 @@ __global__ void __launch_bounds__(256) commit_w_kernel(CommitArgs C) {
     }
 }
 
+// ----------------------------------------- resident exact run, few slots --
+// The reference's C1 shape (8 slots of 32^2, a round every sweep) is bound by
+// per-interval launches and by the commit's L2 round trips, not by work.  For
+// up to 32 slots whose bit lattices fit in shared memory, ONE CTA commits a
+// whole chunk of precomputed draws (draw_kernel records) for every slot --
+// warp w = slot w, lattices in shared memory -- and runs the swap rounds that
+// fall inside the chunk itself (reference rule, kernels.py:116-148), so a
+// chunk of ~64 intervals is one launch.  Windows of 32 attempts are committed
+// in dependency levels with energies summed in attempt order, exactly as
+// commit_kernel; a round boundary may cut a window (its two parts are
+// committed on either side of the round).
+
+__global__ void __launch_bounds__(1024, 1) exact_resident_kernel(CommitArgs C, ExactRounds X) {
+    extern __shared__ uint32_t s_lat[];  // every lattice, by row, ceil(L*L/32) words each
+    __shared__ int s_s2r[32];
+    __shared__ double s_e[32];
+    __shared__ long long s_ss[32];
+    const AdvanceArgs& A = C.A;
+    const int R = (int)A.hi;  // lo == 0: every slot
+    const int lane = threadIdx.x & 31, slot = threadIdx.x >> 5;
+    const int Li = (int)A.L;
+    const float invL = 1.0f / (float)Li;
+    const int nwords = (Li * Li + 31) >> 5;
+    for (int k = threadIdx.x; k < R * nwords; k += blockDim.x) s_lat[k] = A.bits[k];
+    if ((int)threadIdx.x < R) {
+        s_s2r[threadIdx.x] = (int)A.slot_to_row[threadIdx.x];
+        s_e[threadIdx.x] = A.energies[threadIdx.x];
+        s_ss[threadIdx.x] = A.spin_sums[threadIdx.x];
+    }
+    __syncthreads();
+    const int64_t it0 = A.start_iter + C.a0;  // iteration of chunk attempt 0
+    const int64_t I = X.swap_every;
+    const double nsd = (double)(Li * Li);
+    const int32_t* rs = C.rec_site + (int64_t)slot * C.stride;
+    const uint32_t* ra = C.rec_acc + (int64_t)slot * C.stride;
+    const uint32_t* rc = C.rec_conf + (int64_t)slot * C.stride;
+    uint32_t* latw = s_lat + (int64_t)s_s2r[slot < R ? slot : 0] * nwords;
+    double e = slot < R ? s_e[slot] : 0.0;
+    long long ssum = slot < R ? s_ss[slot] : 0;
+    // next round: after chunk attempt bnd - 1 (completed = it0 + bnd), if any
+    auto next_boundary = [&](int64_t from, int64_t& round) -> int64_t {
+        round = -1;
+        if (I <= 0) return INT64_MAX;
+        const int64_t nb = ((it0 + from) / I + 1) * I;
+        if (nb < X.total_iters) round = nb / I - 1;
+        return round >= 0 ? nb - it0 : INT64_MAX;
+    };
+    int64_t round = -1;
+    int64_t bnd = next_boundary(0, round);
+    auto commit = [&](int64_t w0, int64_t lo, int64_t hi, int site, uint32_t accm, unsigned conf) {
+        // attempts [lo, hi) of the window at w0 (32-window dependency levels,
+        // energies in attempt order: commit_kernel's ordered path)
+        const int64_t a = w0 + lane;
+        const bool valid = slot < R && a >= lo && a < hi;
+        const int last = (int)(hi - w0) - 1;
+        auto spin = [&](int x) -> int { return 2 * (int)((latw[x >> 5] >> (x & 31)) & 1u) - 1; };
+        const int r = site_row(site, Li, invL), c = site - r * Li;
+        const int up = (r + 1 == Li ? 0 : r + 1) * Li + c, dn = (r == 0 ? Li - 1 : r - 1) * Li + c;
+        const int rt = r * Li + (c + 1 == Li ? 0 : c + 1), lf = r * Li + (c == 0 ? Li - 1 : c - 1);
+        unsigned pending = __ballot_sync(kFull, valid);
+        double my_d = -0.0;
+        int my_ds = 0;
+        bool my_acc = false;
+        while (pending) {
+            const bool ready = ((pending >> lane) & 1u) && ((conf & pending) == 0u);
+            if (ready) {
+                const int sp = spin(site);
+                const int nbs = spin(up) + spin(dn) + spin(rt) + spin(lf);
+                const int cls = (sp > 0 ? 5 : 0) + (nbs + 4) / 2;
+                const double d = A.dcls[cls];
+                if ((d <= 0.0) || ((accm >> cls) & 1u)) {
+                    atomicXor(&latw[site >> 5], 1u << (site & 31));
+                    my_d = d;
+                    my_ds = -2 * sp;
+                    my_acc = true;
+                }
+            }
+            __syncwarp();
+            pending &= ~__ballot_sync(kFull, ready);
+        }
+        const unsigned accmask = __ballot_sync(kFull, my_acc && valid);
+        int ds_scan = my_ds;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(kFull, ds_scan, o);
+            if (lane >= o) ds_scan += v;
+        }
+        const long long ssum_lane = ssum + ds_scan;
+        double e_lane;
+        if (A.int_energy) {
+            double d_scan = my_d;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double v = __shfl_up_sync(kFull, d_scan, o);
+                if (lane >= o) d_scan = __dadd_rn(d_scan, v);
+            }
+            const bool any_before = (accmask & ((2u << lane) - 1u)) != 0u;
+            e_lane = any_before ? __dadd_rn(e, d_scan) : e;
+        } else {
+            double run = e;
+            e_lane = e;
+            for (int k = 0; k <= last; ++k) {
+                const double dk = __shfl_sync(kFull, my_d, k);
+                if ((accmask >> k) & 1u) run = __dadd_rn(run, dk);
+                if (lane == k) e_lane = run;
+            }
+        }
+        if (A.record >= 1 && valid) {
+            const int64_t col = it0 + a;
+            A.obs_e[(int64_t)slot * A.ncols + col] = e_lane;
+            A.obs_m[(int64_t)slot * A.ncols + col] = __ddiv_rn((double)ssum_lane, nsd);
+        }
+        e = __shfl_sync(kFull, e_lane, last);
+        ssum = __shfl_sync(kFull, ssum_lane, last);
+    };
+    auto do_round = [&](int64_t rnd) {
+        if (slot < R && lane == 0) {
+            s_e[slot] = e;
+            s_ss[slot] = ssum;
+        }
+        __syncthreads();
+        if (slot == 0) {  // disjoint pairs, one lane each (kernels.py:116-148)
+            const int first = (int)(rnd % 2), n_pairs = (R - first) / 2;
+            int acc = 0, ties = 0;
+            for (int p = lane; p < n_pairs; p += 32) {
+                const int i = first + 2 * p, j = i + 1;
+                const double u = stream_uniform(A.seed, (uint64_t)(R + p), (uint64_t)rnd);
+                const double x = __dmul_rn(__dsub_rn(X.betas[i], X.betas[j]), __dsub_rn(s_e[i], s_e[j]));
+                double prob;
+                if (x >= 0.0) {
+                    prob = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-x)));
+                } else {
+                    const double ex = exp(x);
+                    prob = __ddiv_rn(ex, __dadd_rn(1.0, ex));
+                }
+                if (fabs(u - prob) <= 4.0 * 2.220446049250313e-16 * fmax(prob, 2.2250738585072014e-308)) ++ties;
+                if (u < prob) {
+                    const int tr = s_s2r[i]; s_s2r[i] = s_s2r[j]; s_s2r[j] = tr;
+                    const double te = s_e[i]; s_e[i] = s_e[j]; s_e[j] = te;
+                    const long long ts = s_ss[i]; s_ss[i] = s_ss[j]; s_ss[j] = ts;
+                    ++acc;
+                }
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                acc += __shfl_down_sync(kFull, acc, o);
+                ties += __shfl_down_sync(kFull, ties, o);
+            }
+            if (lane == 0 && X.counters) {
+                if (acc) atomicAdd((unsigned long long*)&X.counters[0], (unsigned long long)acc);
+                if (ties) atomicAdd((unsigned long long*)&X.counters[1], (unsigned long long)ties);
+            }
+        }
+        __syncthreads();
+        if (slot < R) {
+            latw = s_lat + (int64_t)s_s2r[slot] * nwords;
+            e = s_e[slot];
+            ssum = s_ss[slot];
+        }
+    };
+    // Records stream through registers one group of kGroup windows ahead, so
+    // their L2 latency hides behind the current group's commits.
+    constexpr int kGroup = 4;
+    const int64_t nwin = (C.n + 31) / 32;
+    int cs[kGroup], ns[kGroup];
+    uint32_t ca[kGroup], na[kGroup], cc[kGroup], nc[kGroup];
+#pragma unroll
+    for (int q = 0; q < kGroup; ++q) {
+        const int64_t a = (int64_t)q * 32 + lane;
+        const bool ok = slot < R && a < C.n;
+        cs[q] = ok ? rs[a] : 0;
+        ca[q] = ok ? ra[a] : 0u;
+        cc[q] = ok ? rc[a] : 0u;
+    }
+    for (int64_t g = 0; g < nwin; g += kGroup) {
+#pragma unroll
+        for (int q = 0; q < kGroup; ++q) {  // prefetch the next group
+            const int64_t a = (g + kGroup + q) * 32 + lane;
+            const bool ok = slot < R && a < C.n;
+            ns[q] = ok ? rs[a] : 0;
+            na[q] = ok ? ra[a] : 0u;
+            nc[q] = ok ? rc[a] : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < kGroup; ++q) {
+            const int64_t w0 = (g + q) * 32;
+            if (w0 >= C.n) break;
+            const int64_t wend = min(w0 + 32, C.n);
+            int64_t lo = w0;
+            while (lo < wend) {  // rounds may cut the window (several, when I < 32)
+                const int64_t hi = min(wend, bnd);
+                if (hi > lo) commit(w0, lo, hi, cs[q], ca[q], cc[q]);
+                lo = hi;
+                if (bnd == hi && hi <= wend) {
+                    do_round(round);
+                    bnd = next_boundary(hi, round);
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kGroup; ++q) {
+            cs[q] = ns[q];
+            ca[q] = na[q];
+            cc[q] = nc[q];
+        }
+    }
+    if (slot < R && lane == 0) {
+        s_e[slot] = e;
+        s_ss[slot] = ssum;
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < R * nwords; k += blockDim.x) A.bits[k] = s_lat[k];
+    if ((int)threadIdx.x < R) {
+        const_cast<int64_t*>(A.slot_to_row)[threadIdx.x] = s_s2r[threadIdx.x];
+        A.energies[threadIdx.x] = s_e[threadIdx.x];
+        A.spin_sums[threadIdx.x] = s_ss[threadIdx.x];
+        if (C.last) {
+            A.positions[threadIdx.x] += 2 * (uint64_t)(C.a0 + C.n);
+            A.iters_done[threadIdx.x] = A.start_iter + C.a0 + C.n;
+        }
+    }
+}
+
 int64_t advance_chunk(int64_t nslots) {
     // attempts per slot per phase-1/phase-2 pass: ~16M records (~200 MiB)
     int64_t c = (int64_t(1) << 24) / std::max<int64_t>(1, nslots);
@@ -829,7 +1051,8 @@ static int draw_stream(DrawStream** out) {
     return PTMH_OK;
 }
 
-int launch_advance_2phase(const AdvanceArgs& a, void* ws, int64_t ws_bytes, cudaStream_t s) {
+int launch_advance_2phase(const AdvanceArgs& a, void* ws, int64_t ws_bytes, cudaStream_t s,
+                          const ExactRounds* rounds) {
     const int64_t nslots = a.hi - a.lo;
     if (nslots <= 0 || a.nsteps <= 0) return PTMH_OK;
     const int64_t stride = advance_stride(nslots, a.nsteps);
@@ -843,8 +1066,18 @@ int launch_advance_2phase(const AdvanceArgs& a, void* ws, int64_t ws_bytes, cuda
     // (PTMH_EXACT_WINDOWS=0 forces the warp path, =2 the window path at any
     // L: A/B in tools/, dependent-heavy windows in tests)
     const char* ew = getenv("PTMH_EXACT_WINDOWS");
-    const bool windows = a.bits && a.int_energy && a.record == 0 && a.L <= 4096 &&
+    const bool windows = !rounds && a.bits && a.int_energy && a.record == 0 && a.L <= 4096 &&
                          (ew && ew[0] == '2' ? a.L >= 3 : a.L >= 512) && !(ew && ew[0] == '0');
+    size_t res_smem = 0;
+    if (rounds) {  // exact_resident_kernel: one CTA, a warp per slot, every lattice in shared memory
+        res_smem = (size_t)nslots * (size_t)((a.L * a.L + 31) / 32) * 4;
+        if (a.lo != 0 || nslots > 32 || !a.bits || res_smem > 200 * 1024) {
+            set_error("resident exact run: needs every slot (<= 32) and bit lattices in shared memory");
+            return PTMH_ERR_ARG;
+        }
+        PTMH_CUDA(cudaFuncSetAttribute(exact_resident_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)res_smem));
+    }
     const int64_t one = nslots * stride * 12 + nslots * (stride / kSW) * 4;
     DrawStream* ds = nullptr;
     std::unique_lock<std::mutex> lk;
@@ -879,7 +1112,9 @@ int launch_advance_2phase(const AdvanceArgs& a, void* ws, int64_t ws_bytes, cuda
             PTMH_CUDA(cudaStreamWaitEvent(sc, ds->drawn[b], 0));
         }
         CommitArgs C{a, a0, n, stride, rs, ra, rc, rind, a0 + n >= a.nsteps};
-        if (windows)
+        if (rounds)
+            exact_resident_kernel<<<1, (unsigned)(32 * nslots), res_smem, sc>>>(C, *rounds);
+        else if (windows)
             commit_w_kernel<<<(unsigned)nslots, 256, 0, sc>>>(C);
         else if (a.bits)
             commit_kernel<true><<<ceil_div(nslots, 4), 128, 0, sc>>>(C);

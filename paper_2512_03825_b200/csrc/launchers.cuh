@@ -39,7 +39,15 @@ int64_t fill_ws_bytes(int64_t n, int64_t rows_per_batch);
 int launch_fill_parallel(int8_t* spins, int64_t rows, int64_t n, int64_t up_count, uint64_t seed,
                          uint64_t stream0, uint64_t pos0, void* ws, int64_t ws_bytes, cudaStream_t s);
 int launch_advance(const AdvanceArgs& a, cudaStream_t s);
-int launch_advance_2phase(const AdvanceArgs& a, void* ws, int64_t ws_bytes, cudaStream_t s);
+// swap rounds run inside the resident exact commit (exact.cu)
+struct ExactRounds {
+    int64_t swap_every;   // attempts per interval (0: no rounds)
+    int64_t total_iters;  // N: rounds fire at completed = (k+1) * I < N
+    const double* betas;  // by slot
+    int64_t* counters;    // accepted, near ties
+};
+int launch_advance_2phase(const AdvanceArgs& a, void* ws, int64_t ws_bytes, cudaStream_t s,
+                          const ExactRounds* rounds = nullptr);
 int64_t advance_ws_bytes(int64_t nslots, int64_t nsteps);
 int launch_bits_pack(const int8_t* spins, int64_t rows, int64_t L, uint32_t* bits, cudaStream_t s);
 int launch_bits_unpack(const uint32_t* bits, int64_t rows, int64_t L, int8_t* spins, cudaStream_t s);

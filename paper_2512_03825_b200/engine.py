@@ -158,6 +158,30 @@ class ExactEngine(_Base):
                   start_iter, nsteps, _P(obs_e), _P(obs_m), ncols, record, _P(states), self._s())
         _lib.call("ptmh_bits_pack", _P(self.spins), self.R, self.L, _P(self.bits), self._s())
 
+    def resident_ok(self, record: int) -> bool:
+        """Whether run_resident applies: every slot in one CTA (R <= 32), bit
+        lattices in shared memory, no per-attempt state snapshots."""
+        return (self.R <= 32 and record <= 1 and self.L <= 4096
+                and self.R * ((self.L * self.L + 31) // 32) * 4 <= 200 * 1024)
+
+    def run_resident(self, start_iter: int, nsteps: int, swap_every: int, total_iters: int,
+                     obs_e=None, obs_m=None) -> None:
+        """Iterations start_iter .. start_iter+nsteps-1 WITH their swap rounds
+        (executor.py:111-125, 227-262) in chunked launches: draws on the whole
+        GPU, one CTA commits every slot in shared memory and runs the rounds
+        (csrc/exact.cu, exact_resident_kernel)."""
+        if nsteps <= 0:
+            return
+        need = int(_lib.LIB.ptmh_advance_workspace_bytes(self.R, nsteps))
+        if getattr(self, "_ws", None) is None or self._ws.numel() < need:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=self.dev)
+        ncols = obs_e.shape[1] if obs_e is not None else 0
+        _lib.call("ptmh_exact_run_resident", _P(self.bits), self.L, _P(self.slot_to_row), self.R,
+                  _P(self.tbl), _P(self.dcls), self.int_energy, _P(self.energies), _P(self.spin_sums),
+                  _P(self.positions), _P(self.iters_done), self.seed, start_iter, nsteps, swap_every,
+                  total_iters, _P(self.betas), _P(self.counters), _P(obs_e), _P(obs_m), ncols,
+                  _P(self._ws), self._ws.numel(), self._s())
+
     def exchange(self, round_index: int) -> int:
         """One swap round (executor.py:250-262, kernels.py:116-148); returns
         the number of pairs attempted."""

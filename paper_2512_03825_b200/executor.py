@@ -59,7 +59,10 @@ class SimulationConfig:
     record_every: int = 1
     device: int | None = None
     return_final_state: bool = False
-    kernel: str = "auto"  # checkerboard: "sweep" (2 launches/sweep), "resident" (1 launch/run)
+    # checkerboard: "sweep" (launches per interval), "resident" (1 launch/run);
+    # exact: "sweep" (launches per interval), "auto"/"resident": rounds inside
+    # the commit launches when every slot fits one CTA (R <= 32)
+    kernel: str = "auto"
 
     def validate(self) -> None:
         if self.side < 2:
@@ -242,16 +245,28 @@ def _run_exact(config: SimulationConfig) -> RunRecord:
         snaps = np.zeros((n_rounds, R), dtype=np.int64) if rec_flag >= 1 and n_rounds else None
         completed = 1
         try:
-            for target, ri in plan:
-                if target > completed:
-                    eng.advance(completed, target - completed, obs_e, obs_m, rec_flag, states)
-                completed = target
-                if ri is None:
-                    continue
-                if snaps is not None:
-                    snaps[ri, :] = completed  # == iters_done of every slot
-                rounds += 1
-                attempted += eng.exchange(ri)
+            if config.kernel != "sweep" and eng.resident_ok(rec_flag):
+                # few small lattices (the reference's C1): the whole run with its
+                # rounds in chunked launches (csrc/exact.cu, exact_resident_kernel)
+                eng.run_resident(1, N - 1, I, N, obs_e, obs_m)
+                for target, ri in plan:
+                    if ri is None:
+                        continue
+                    if snaps is not None:
+                        snaps[ri, :] = target
+                    rounds += 1
+                    attempted += max(0, (R - ri % 2) // 2)
+            else:
+                for target, ri in plan:
+                    if target > completed:
+                        eng.advance(completed, target - completed, obs_e, obs_m, rec_flag, states)
+                    completed = target
+                    if ri is None:
+                        continue
+                    if snaps is not None:
+                        snaps[ri, :] = completed  # == iters_done of every slot
+                    rounds += 1
+                    attempted += eng.exchange(ri)
             _sync(dev)
         except BaseException as exc:  # noqa: BLE001 - any failure invalidates the run
             errors.append(exc)
