@@ -787,7 +787,8 @@ __global__ void __launch_bounds__(256) commit_w_kernel(CommitArgs C) {
 // commit_kernel; a round boundary may cut a window (its two parts are
 // committed on either side of the round).
 
-__global__ void __launch_bounds__(1024, 1) exact_resident_kernel(CommitArgs C, ExactRounds X) {
+template <int kMaxThreads>
+__global__ void __launch_bounds__(kMaxThreads, 1) exact_resident_kernel(CommitArgs C, ExactRounds X) {
     extern __shared__ uint32_t s_lat[];  // every lattice, by row, ceil(L*L/32) words each
     __shared__ int s_s2r[32];
     __shared__ double s_e[32];
@@ -824,6 +825,22 @@ __global__ void __launch_bounds__(1024, 1) exact_resident_kernel(CommitArgs C, E
     };
     int64_t round = -1;
     int64_t bnd = next_boundary(0, round);
+    // integer J, B and no recording: energies are order-free -- per-lane
+    // partial sums, reduced only when a round (or the end) needs them
+    const bool unordered = A.int_energy && A.record == 0;
+    double acc_d = -0.0;  // IEEE identity (see commit_kernel)
+    long long acc_ds = 0;
+    auto settle = [&]() {
+        if (!unordered) return;
+        for (int o = 16; o > 0; o >>= 1) {
+            acc_d = __dadd_rn(acc_d, __shfl_xor_sync(kFull, acc_d, o));
+            acc_ds += __shfl_xor_sync(kFull, acc_ds, o);
+        }
+        e = __dadd_rn(e, acc_d);
+        ssum += acc_ds;
+        acc_d = -0.0;
+        acc_ds = 0;
+    };
     auto commit = [&](int64_t w0, int64_t lo, int64_t hi, int site, uint32_t accm, unsigned conf) {
         // attempts [lo, hi) of the window at w0 (32-window dependency levels,
         // energies in attempt order: commit_kernel's ordered path)
@@ -854,6 +871,13 @@ __global__ void __launch_bounds__(1024, 1) exact_resident_kernel(CommitArgs C, E
             }
             __syncwarp();
             pending &= ~__ballot_sync(kFull, ready);
+        }
+        if (unordered) {
+            if (my_acc) {
+                acc_d = __dadd_rn(acc_d, my_d);
+                acc_ds += my_ds;
+            }
+            return;
         }
         const unsigned accmask = __ballot_sync(kFull, my_acc && valid);
         int ds_scan = my_ds;
@@ -891,6 +915,7 @@ __global__ void __launch_bounds__(1024, 1) exact_resident_kernel(CommitArgs C, E
         ssum = __shfl_sync(kFull, ssum_lane, last);
     };
     auto do_round = [&](int64_t rnd) {
+        settle();
         if (slot < R && lane == 0) {
             s_e[slot] = e;
             s_ss[slot] = ssum;
@@ -980,6 +1005,7 @@ __global__ void __launch_bounds__(1024, 1) exact_resident_kernel(CommitArgs C, E
             cc[q] = nc[q];
         }
     }
+    settle();
     if (slot < R && lane == 0) {
         s_e[slot] = e;
         s_ss[slot] = ssum;
@@ -1075,8 +1101,12 @@ int launch_advance_2phase(const AdvanceArgs& a, void* ws, int64_t ws_bytes, cuda
             set_error("resident exact run: needs every slot (<= 32) and bit lattices in shared memory");
             return PTMH_ERR_ARG;
         }
-        PTMH_CUDA(cudaFuncSetAttribute(exact_resident_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)res_smem));
+        // instantiations by slot count: <= 8 slots run uncapped (146
+        // registers; the 1024-thread one spills at 64: C1 2.2e8 -> 3.9e8)
+        const void* fn = nslots <= 8 ? (const void*)exact_resident_kernel<256>
+                         : nslots <= 16 ? (const void*)exact_resident_kernel<512>
+                                        : (const void*)exact_resident_kernel<1024>;
+        PTMH_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)res_smem));
     }
     const int64_t one = nslots * stride * 12 + nslots * (stride / kSW) * 4;
     DrawStream* ds = nullptr;
@@ -1112,8 +1142,12 @@ int launch_advance_2phase(const AdvanceArgs& a, void* ws, int64_t ws_bytes, cuda
             PTMH_CUDA(cudaStreamWaitEvent(sc, ds->drawn[b], 0));
         }
         CommitArgs C{a, a0, n, stride, rs, ra, rc, rind, a0 + n >= a.nsteps};
-        if (rounds)
-            exact_resident_kernel<<<1, (unsigned)(32 * nslots), res_smem, sc>>>(C, *rounds);
+        if (rounds && nslots <= 8)
+            exact_resident_kernel<256><<<1, (unsigned)(32 * nslots), res_smem, sc>>>(C, *rounds);
+        else if (rounds && nslots <= 16)
+            exact_resident_kernel<512><<<1, (unsigned)(32 * nslots), res_smem, sc>>>(C, *rounds);
+        else if (rounds)
+            exact_resident_kernel<1024><<<1, (unsigned)(32 * nslots), res_smem, sc>>>(C, *rounds);
         else if (windows)
             commit_w_kernel<<<(unsigned)nslots, 256, 0, sc>>>(C);
         else if (a.bits)
