@@ -221,11 +221,11 @@ __device__ __forceinline__ uint32_t ld_other(const uint32_t* p) {
     return kNC ? __ldg(p) : __ldcg(p);
 }
 
-// One thread's strip: word column k of lattice rows i0 .. i0+kRows-1 of one
-// colour (kStats doubles as the colour: colour 0 resets the lattice's stats,
-// colour 1 recomputes them).  Returns the thread's (S, Bond) contributions in
-// sumS / sumB; the caller reduces them (flush_stats).
-template <int kRows, bool kStats, bool kNC>
+// One thread's strip: word column k of lattice rows i0 .. i0+kRows-1 of
+// colour kColor.  kStats: colour 0 resets the lattice's stats, colour 1
+// recomputes them -- the thread's (S, Bond) contributions in sumS / sumB,
+// which the caller reduces (flush_stats).
+template <int kRows, int kColor, bool kStats, bool kNC>
 __device__ __forceinline__ void ferro_strip(uint32_t* __restrict__ packed, int L, int WR, int64_t W,
                                             const int32_t* __restrict__ row_to_slot,
                                             const uint32_t* __restrict__ thresh, const RoundKeys32& rk,
@@ -233,7 +233,6 @@ __device__ __forceinline__ void ferro_strip(uint32_t* __restrict__ packed, int L
                                             bool active, int64_t lat, int rem,
                                             uint32_t (&tie_m)[kRows][32], uint32_t (&tie_k4)[kRows][32],
                                             int& sumS, int& sumB) {
-    constexpr int kColor = kStats ? 1 : 0;
     const int lane = threadIdx.x & 31;
     const int strip = rem / WR;
     const int k = rem - strip * WR;
@@ -243,7 +242,7 @@ __device__ __forceinline__ void ferro_strip(uint32_t* __restrict__ packed, int L
     uint32_t t3 = 0, t4 = 0;
     uint32_t tie_rows = 0;  // bit rr: row rr has ties
     if (active) {
-        if (!kStats && rem == 0) {  // colour-0 pass: reset, colour-1 pass recomputes
+        if (kColor == 0 && kStats && rem == 0) {  // colour-0 pass: reset, colour-1 pass recomputes
             stats[2 * lat] = 0;
             stats[2 * lat + 1] = 0;
         }
@@ -324,7 +323,7 @@ __device__ __forceinline__ void ferro_strip(uint32_t* __restrict__ packed, int L
             tie_rows |= (eq != 0u ? 1u : 0u) << rr;
             const uint32_t Sn = S ^ acc;
             if (acc) __stcg(word_at(own, o, esz), Sn);
-            if (kStats) {
+            if (kColor == 1 && kStats) {
                 // new aligned masks: a flip toggles alignment with all four neighbours
                 const int kk = __popc(a ^ acc) + __popc(b ^ acc) + __popc(c ^ acc) + __popc(d ^ acc);
                 sumB += 2 * kk - 128;                         // sum of s*nb = 2k - 4 per site
@@ -365,7 +364,7 @@ __device__ __forceinline__ void ferro_strip(uint32_t* __restrict__ packed, int L
                 const uint4 r2 =
                     philox4x32_10(make_uint4(w32 * 32u + (uint32_t)bit, ctr1, (uint32_t)slot, 1u), rk);
                 if ((r2.x >> 8) < t24) {
-                    if (kStats) {
+                    if (kColor == 1 && kStats) {
                         sumS += ((Sw >> bit) & 1u) ? -2 : 2;
                         sumB += k4 ? -8 : -4;
                     }
@@ -393,7 +392,8 @@ __global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_half_sweep_ferro(
     const int64_t lat = active ? tid / per_lat : 0;
     const int rem = (int)(tid - lat * per_lat);
     int sumS = 0, sumB = 0;
-    ferro_strip<kRows, kStats, true>(packed, L, WR, W, row_to_slot, thresh, rk, ctr1, stats, esz, active,
+    ferro_strip<kRows, kStats ? 1 : 0, true, true>(packed, L, WR, W, row_to_slot, thresh, rk, ctr1, stats, esz,
+                                                   active,
                                      lat, rem, tie_m[warp], tie_k4[warp], sumS, sumB);
     if (kStats) flush_stats(stats, lat, active, sumS, sumB);
 }
@@ -473,18 +473,27 @@ __global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_sweeps_persistent(
         const uint32_t lat = r / subs, sub = r - lat * subs;
         const uint32_t ctr1 = ctr_base + phase;
         int sumS = 0, sumB = 0;
+        // (S, Bond) are only read after the launch: the last sweep's colour 0
+        // resets them and its colour 1 recomputes them; earlier sweeps skip
+        // the popcounts and the reduction
+        const bool last_sweep = phase + 2 >= n_phases;
+#define PTMH_STRIP(C, ST)                                                                                 \
+    for (uint32_t g = 0; g < group; ++g)                                                                  \
+        ferro_strip<kRows, C, ST, true>(packed, L, WR, W, row_to_slot, thresh, rk, ctr1, stats, esz, true, \
+                                        lat, (int)((sub * group + g) * 256 + threadIdx.x), tie_m[warp],   \
+                                        tie_k4[warp], sumS, sumB)
         if ((ctr1 & 1u) == 0) {
-            for (uint32_t g = 0; g < group; ++g)
-                ferro_strip<kRows, false, true>(packed, L, WR, W, row_to_slot, thresh, rk, ctr1, stats, esz,
-                                                true, lat, (int)((sub * group + g) * 256 + threadIdx.x),
-                                                tie_m[warp], tie_k4[warp], sumS, sumB);
-        } else {
-            for (uint32_t g = 0; g < group; ++g)
-                ferro_strip<kRows, true, true>(packed, L, WR, W, row_to_slot, thresh, rk, ctr1, stats, esz,
-                                               true, lat, (int)((sub * group + g) * 256 + threadIdx.x),
-                                               tie_m[warp], tie_k4[warp], sumS, sumB);
+            if (last_sweep)
+                PTMH_STRIP(0, true);
+            else
+                PTMH_STRIP(0, false);
+        } else if (last_sweep) {
+            PTMH_STRIP(1, true);
             flush_stats(stats, lat, true, sumS, sumB);
+        } else {
+            PTMH_STRIP(1, false);
         }
+#undef PTMH_STRIP
         __syncthreads();  // every store of this item is issued before the release
         if (threadIdx.x == 0) red_release_gpu_add(&sync[2 + lat], 1u);
     }
