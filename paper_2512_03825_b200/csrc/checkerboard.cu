@@ -232,6 +232,7 @@ __device__ __forceinline__ void ferro_strip(uint32_t* __restrict__ packed, int L
                                             uint32_t ctr1, int64_t* __restrict__ stats, uint32_t esz,
                                             bool active, int64_t lat, int rem,
                                             uint32_t (&tie_m)[kRows][32], uint32_t (&tie_k4)[kRows][32],
+                                            uint32_t (&tie_sn)[kRows][32],
                                             int& sumS, int& sumB) {
     const int lane = threadIdx.x & 31;
     const int strip = rem / WR;
@@ -320,6 +321,7 @@ __device__ __forceinline__ void ferro_strip(uint32_t* __restrict__ packed, int L
             // ties (top byte equal): bookkeeping only, resolved after the loop
             tie_m[rr][lane] = eq;
             tie_k4[rr][lane] = eq & K4;
+            tie_sn[rr][lane] = S ^ acc;  // the row's word as stored: the tie walk starts from it
             tie_rows |= (eq != 0u ? 1u : 0u) << rr;
             const uint32_t Sn = S ^ acc;
             if (acc) __stcg(word_at(own, o, esz), Sn);
@@ -353,7 +355,7 @@ __device__ __forceinline__ void ferro_strip(uint32_t* __restrict__ packed, int L
                 m = tie_m[rr][lane];
                 mk4 = tie_k4[rr][lane];
                 w32 = (uint32_t)((i0 + rr) * WR + k);
-                Sw = __ldcg(packed + own_base + w32);
+                Sw = tie_sn[rr][lane];  // (shared memory: no L2 round trip per tie row)
                 dirty = false;
             }
             if (m != 0) {
@@ -384,7 +386,7 @@ __global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_half_sweep_ferro(
     const int32_t* __restrict__ row_to_slot, const uint32_t* __restrict__ thresh, const RoundKeys32 rk,
     uint32_t ctr1, int64_t* __restrict__ stats, uint32_t esz) {
     constexpr int kWarps = 8;
-    __shared__ uint32_t tie_m[kWarps][kRows][32], tie_k4[kWarps][kRows][32];
+    __shared__ uint32_t tie_m[kWarps][kRows][32], tie_k4[kWarps][kRows][32], tie_sn[kWarps][kRows][32];
     const int warp = threadIdx.x >> 5;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t per_lat = (int64_t)(L / kRows) * WR;
@@ -394,7 +396,7 @@ __global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_half_sweep_ferro(
     int sumS = 0, sumB = 0;
     ferro_strip<kRows, kStats ? 1 : 0, true, true>(packed, L, WR, W, row_to_slot, thresh, rk, ctr1, stats, esz,
                                                    active,
-                                     lat, rem, tie_m[warp], tie_k4[warp], sumS, sumB);
+                                     lat, rem, tie_m[warp], tie_k4[warp], tie_sn[warp], sumS, sumB);
     if (kStats) flush_stats(stats, lat, active, sumS, sumB);
 }
 
@@ -442,7 +444,12 @@ __global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_sweeps_persistent(
     uint32_t ctr_base, uint32_t n_phases, int64_t* __restrict__ stats, uint32_t esz,
     uint32_t* __restrict__ sync, uint32_t group) {
     constexpr int kWarps = 8;
-    __shared__ uint32_t tie_m[kWarps][kRows][32], tie_k4[kWarps][kRows][32];
+    // tie scratch (3 x kRows x 32 words per warp: 48 KB at kRows = 16) in
+    // dynamic shared memory; cb_sweeps_persistent_smem() bytes
+    extern __shared__ uint32_t s_ties[];
+    uint32_t(*tie_m)[kRows][32] = reinterpret_cast<uint32_t(*)[kRows][32]>(s_ties);
+    uint32_t(*tie_k4)[kRows][32] = tie_m + kWarps;
+    uint32_t(*tie_sn)[kRows][32] = tie_m + 2 * kWarps;
     __shared__ uint32_t s_item[2];
     const int warp = threadIdx.x >> 5;
     // items per lattice and phase (the host picks group so that a phase still
@@ -481,7 +488,7 @@ __global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_sweeps_persistent(
     for (uint32_t g = 0; g < group; ++g)                                                                  \
         ferro_strip<kRows, C, ST, true>(packed, L, WR, W, row_to_slot, thresh, rk, ctr1, stats, esz, true, \
                                         lat, (int)((sub * group + g) * 256 + threadIdx.x), tie_m[warp],   \
-                                        tie_k4[warp], sumS, sumB)
+                                        tie_k4[warp], tie_sn[warp], sumS, sumB)
         if ((ctr1 & 1u) == 0) {
             if (last_sweep)
                 PTMH_STRIP(0, true);
@@ -824,6 +831,8 @@ constexpr int kFastRows = PTMH_FERRO_ROWS;
 
 // one persistent launch for every half-sweep: the ferro kernel with whole
 // 256-thread blocks per lattice (L % 512 == 0)
+static size_t persistent_smem(int krows) { return (size_t)3 * 8 * krows * 32 * 4; }
+
 bool cb_sweeps_persistent_applies(int64_t L, uint32_t always_mask, int64_t n_sweeps) {
     const bool ferro = (always_mask & kSymmetricFlag) && (always_mask & 0x3ffu) == 0x078u;
     return ferro && n_sweeps > 0 && L >= 1024 && L % 512 == 0;
@@ -849,7 +858,12 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
         if (cached_slots[dev] == 0) {
             int sms = 0, occ = 0;
             PTMH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-            PTMH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cb_sweeps_persistent<16>, 256, 0));
+            for (const void* fn : {(const void*)cb_sweeps_persistent<16>, (const void*)cb_sweeps_persistent<8>,
+                                   (const void*)cb_sweeps_persistent<4>, (const void*)cb_sweeps_persistent<2>})
+                PTMH_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)persistent_smem(16)));
+            PTMH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cb_sweeps_persistent<16>, 256,
+                                                                    persistent_smem(16)));
             cached_slots[dev] = sms * std::max(occ, 1);
         }
         const int64_t slots = cached_slots[dev];
@@ -892,16 +906,16 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
         const unsigned grid = (unsigned)std::min<int64_t>(items, slots);
         const uint32_t c0 = (uint32_t)(2 * first_sweep), np = (uint32_t)(2 * n_sweeps);
         if (krows == 16)
-            cb_sweeps_persistent<16><<<grid, 256, 0, s>>>(packed, rows, (int)L, WR, W, row_to_slot, thresh, rk,
+            cb_sweeps_persistent<16><<<grid, 256, persistent_smem(16), s>>>(packed, rows, (int)L, WR, W, row_to_slot, thresh, rk,
                                                            c0, np, stats, 4u, sync, (uint32_t)group);
         else if (krows == 8)
-            cb_sweeps_persistent<8><<<grid, 256, 0, s>>>(packed, rows, (int)L, WR, W, row_to_slot, thresh, rk,
+            cb_sweeps_persistent<8><<<grid, 256, persistent_smem(8), s>>>(packed, rows, (int)L, WR, W, row_to_slot, thresh, rk,
                                                           c0, np, stats, 4u, sync, (uint32_t)group);
         else if (krows == 4)
-            cb_sweeps_persistent<4><<<grid, 256, 0, s>>>(packed, rows, (int)L, WR, W, row_to_slot, thresh, rk,
+            cb_sweeps_persistent<4><<<grid, 256, persistent_smem(4), s>>>(packed, rows, (int)L, WR, W, row_to_slot, thresh, rk,
                                                           c0, np, stats, 4u, sync, (uint32_t)group);
         else
-            cb_sweeps_persistent<2><<<grid, 256, 0, s>>>(packed, rows, (int)L, WR, W, row_to_slot, thresh, rk,
+            cb_sweeps_persistent<2><<<grid, 256, persistent_smem(2), s>>>(packed, rows, (int)L, WR, W, row_to_slot, thresh, rk,
                                                           c0, np, stats, 4u, sync, (uint32_t)group);
         PTMH_LAUNCH_CHECK();
         return PTMH_OK;
