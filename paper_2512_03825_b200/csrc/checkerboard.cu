@@ -850,7 +850,7 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
     const bool ferro = (always_mask & kSymmetricFlag) && (always_mask & 0x3ffu) == 0x078u &&
                        rows * 2 * W < (1LL << 32);  // 32-bit word offsets in the tie queue
     if (sync && ferro && cb_sweeps_persistent_applies(L, always_mask, n_sweeps) &&
-        2 * n_sweeps * rows * (L * L / 65536) < (1LL << 31)) {
+        2 * n_sweeps * rows * (L * L / 32768) < (1LL << 31)) {  // item count at 2 rows per thread
         static int cached_slots[256] = {};  // resident CTAs per device
         int dev = 0;
         PTMH_CUDA(cudaGetDevice(&dev));
