@@ -89,3 +89,39 @@ def test_peer_buffers_ipc_two_processes(tmp_path):
         assert d["flags"].tolist() == [(r + 1) * 100 + g for r in range(world)]
         for r in range(world):
             assert d["stats"][r].tolist() == [r + 7, r + 7]
+
+
+def test_resident_sharded_driver_world1():
+    """distributed.resident_sharded (peer-buffer rounds, then the slots /
+    counters / observables combination) over NCCL at world 1, in two
+    segments with recording: equal to the engine's own resident run."""
+    from paper_2512_03825_b200 import build_ladder
+    from paper_2512_03825_b200.distributed import PeerBuffers, ShardedCheckerboard, resident_sharded
+    from paper_2512_03825_b200.engine import CheckerboardEngine
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        L, R, total, every, rec, seed = 64, 12, 24, 1, 2, 23
+        temps = build_ladder(R)
+        ref = CheckerboardEngine(L, R, temps, seed, 1.0, 0.0, 0.5, 0)
+        ref.init_state()
+        roe = torch.zeros((R, total // rec), dtype=torch.float64, device="cuda")
+        rom = torch.zeros_like(roe)
+        ref.run_resident(0, 10, total, every, record_every=rec, obs_e=roe, obs_m=rom)
+        ref.run_resident(10, total - 10, total, every, record_every=rec, obs_e=roe, obs_m=rom)
+        drv = ShardedCheckerboard(L, R, temps, seed, device=0)
+        drv.init_state()
+        peers = PeerBuffers(R, torch.device("cuda", 0))
+        oe = torch.zeros_like(roe)
+        om = torch.zeros_like(rom)
+        resident_sharded(drv, peers, 0, 10, total, every, record_every=rec, obs_e=oe, obs_m=om)
+        resident_sharded(drv, peers, 10, total - 10, total, every, record_every=rec, obs_e=oe, obs_m=om)
+        torch.cuda.synchronize()
+        assert np.array_equal(drv.eng.final_spins(), ref.final_spins())
+        assert torch.equal(drv.eng.slot_to_row, ref.slot_to_row)
+        assert torch.equal(drv.eng.row_to_slot, ref.row_to_slot)
+        assert drv.eng.swap_counts() == ref.swap_counts()
+        assert torch.equal(oe, roe) and torch.equal(om, rom)
+        peers.close()
+    finally:
+        dist.destroy_process_group()
