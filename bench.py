@@ -232,10 +232,11 @@ def main():
             times.append(dt)
         tot = sum(times)
         val = args.steps * R * per_slot / tot
-        line = {"metric": metric, "value": val, "unit": "attempts/s", "n_gpus": 0, "steps": args.steps,
+        line = {"metric": metric, "value": val, "unit": "attempts/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
                 "scaling": "none", "vs_baseline": None, "dtype": "int8/f64", "data": "synthetic",
                 "impl": "reference", "config": config,
+                "note": "the reference runs on the host CPU (rank 0 only); n_gpus is the job's GPU count",
                 "cpu_baseline": {"value": val, "unit": "attempts/s", "cores": threads, "kind": "port",
                                  "sample": f"{R} slots x {per_slot} random-site attempts per step "
                                            f"(reference chain kernels.py:62-113, C port, "
