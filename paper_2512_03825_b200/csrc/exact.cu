@@ -663,6 +663,15 @@ __global__ void __launch_bounds__(256) commit_w_kernel(CommitArgs C) {
     long long acc_ds = 0;
     const int32_t* rs = C.rec_site + s * C.stride;
     const uint32_t* ra = C.rec_acc + s * C.stride;
+    // the next window's records are loaded while this one commits
+    int nst[4];
+    uint32_t nam[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int64_t a = q * 256 + threadIdx.x;
+        nst[q] = a < C.n ? rs[a] : 0;
+        nam[q] = a < C.n ? ra[a] : 0u;
+    }
     for (int64_t w0 = 0; w0 < C.n; w0 += kWin) {
         if (threadIdx.x < kWin / 32) dep_bits[threadIdx.x] = 0;
         __syncthreads();
@@ -674,8 +683,11 @@ __global__ void __launch_bounds__(256) commit_w_kernel(CommitArgs C) {
         for (int q = 0; q < 4; ++q) {
             const int64_t a = w0 + q * 256 + threadIdx.x;
             on[q] = a < C.n;
-            st[q] = on[q] ? rs[a] : 0;
-            am[q] = on[q] ? ra[a] : 0u;
+            st[q] = nst[q];
+            am[q] = nam[q];
+            const int64_t an = a + kWin;
+            nst[q] = an < C.n ? rs[an] : 0;
+            nam[q] = an < C.n ? ra[an] : 0u;
         }
         int sp[4], nb[4];
 #pragma unroll
