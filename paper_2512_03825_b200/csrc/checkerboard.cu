@@ -320,9 +320,9 @@ __device__ __forceinline__ void ferro_strip(uint32_t* __restrict__ packed, int L
             acc |= bor & upm;
             // ties (top byte equal): bookkeeping only, resolved after the loop
             tie_m[rr][lane] = eq;
-            tie_k4[rr][lane] = eq & K4;
+            tie_k4[rr][lane] = K4;  // read at tie bits only
             tie_sn[rr][lane] = S ^ acc;  // the row's word as stored: the tie walk starts from it
-            tie_rows |= (eq != 0u ? 1u : 0u) << rr;
+            if (eq) tie_rows |= 1u << rr;
             const uint32_t Sn = S ^ acc;
             if (acc) __stcg(word_at(own, o, esz), Sn);
             if (kColor == 1 && kStats) {
