@@ -321,7 +321,7 @@ __device__ __forceinline__ void ferro_strip(uint32_t* __restrict__ packed, int L
             // ties (top byte equal): bookkeeping only, resolved after the loop
             tie_m[rr][lane] = eq;
             tie_k4[rr][lane] = K4;  // read at tie bits only
-            tie_sn[rr][lane] = S ^ acc;  // the row's word as stored: the tie walk starts from it
+            if (kRows <= 16) tie_sn[rr][lane] = S ^ acc;  // the row's word as stored: the tie walk starts from it
             if (eq) tie_rows |= 1u << rr;
             const uint32_t Sn = S ^ acc;
             if (acc) __stcg(word_at(own, o, esz), Sn);
@@ -355,7 +355,9 @@ __device__ __forceinline__ void ferro_strip(uint32_t* __restrict__ packed, int L
                 m = tie_m[rr][lane];
                 mk4 = tie_k4[rr][lane];
                 w32 = (uint32_t)((i0 + rr) * WR + k);
-                Sw = tie_sn[rr][lane];  // (shared memory: no L2 round trip per tie row)
+                // (shared memory: no L2 round trip per tie row; 32-row strips
+                // keep only two scratch arrays to fit three CTAs per SM)
+                Sw = kRows <= 16 ? tie_sn[rr][lane] : __ldcg(packed + own_base + w32);
                 dirty = false;
             }
             if (m != 0) {
@@ -449,7 +451,7 @@ __global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_sweeps_persistent(
     extern __shared__ uint32_t s_ties[];
     uint32_t(*tie_m)[kRows][32] = reinterpret_cast<uint32_t(*)[kRows][32]>(s_ties);
     uint32_t(*tie_k4)[kRows][32] = tie_m + kWarps;
-    uint32_t(*tie_sn)[kRows][32] = tie_m + 2 * kWarps;
+    uint32_t(*tie_sn)[kRows][32] = kRows <= 16 ? tie_m + 2 * kWarps : tie_m;  // (unused at 32 rows)
     __shared__ uint32_t s_item[2];
     const int warp = threadIdx.x >> 5;
     // items per lattice and phase (the host picks group so that a phase still
@@ -831,7 +833,7 @@ constexpr int kFastRows = PTMH_FERRO_ROWS;
 
 // one persistent launch for every half-sweep: the ferro kernel with whole
 // 256-thread blocks per lattice (L % 512 == 0)
-static size_t persistent_smem(int krows) { return (size_t)3 * 8 * krows * 32 * 4; }
+static size_t persistent_smem(int krows) { return (size_t)(krows <= 16 ? 3 : 2) * 8 * krows * 32 * 4; }
 
 bool cb_sweeps_persistent_applies(int64_t L, uint32_t always_mask, int64_t n_sweeps) {
     const bool ferro = (always_mask & kSymmetricFlag) && (always_mask & 0x3ffu) == 0x078u;
@@ -858,10 +860,11 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
         if (cached_slots[dev] == 0) {
             int sms = 0, occ = 0;
             PTMH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-            for (const void* fn : {(const void*)cb_sweeps_persistent<16>, (const void*)cb_sweeps_persistent<8>,
-                                   (const void*)cb_sweeps_persistent<4>, (const void*)cb_sweeps_persistent<2>})
+            for (const void* fn : {(const void*)cb_sweeps_persistent<32>, (const void*)cb_sweeps_persistent<16>,
+                                   (const void*)cb_sweeps_persistent<8>, (const void*)cb_sweeps_persistent<4>,
+                                   (const void*)cb_sweeps_persistent<2>})
                 PTMH_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)persistent_smem(16)));
+                                               (int)persistent_smem(32)));
             PTMH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cb_sweeps_persistent<16>, 256,
                                                                     persistent_smem(16)));
             cached_slots[dev] = sms * std::max(occ, 1);
@@ -882,6 +885,8 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
         int krows = 2;
         if (er) {
             krows = atoi(er);
+        } else if (rows * (L * L / (256LL * 64 * 32)) >= 8 * slots) {
+            krows = 32;  // plenty of items (C4): longest strips (C4 +2.6 %, C3 -4 %)
         } else {
             for (int k : {16, 8, 4}) {
                 if (rows * (L * L / (256LL * 64 * k)) >= slots) {
@@ -890,7 +895,7 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
                 }
             }
         }
-        if (krows != 2 && krows != 4 && krows != 8 && krows != 16) krows = 16;
+        if (krows != 2 && krows != 4 && krows != 8 && krows != 16 && krows != 32) krows = 16;
         // 256-thread blocks per item: amortise the per-item scheduling over
         // several blocks while a phase keeps >= 8 items per resident CTA
         // (PTMH_PERSIST_ITEMS_PER_SLOT overrides the 8; tests use 0 to force
@@ -905,7 +910,10 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
         const int64_t items = 2 * n_sweeps * rows * (blocks / group);
         const unsigned grid = (unsigned)std::min<int64_t>(items, slots);
         const uint32_t c0 = (uint32_t)(2 * first_sweep), np = (uint32_t)(2 * n_sweeps);
-        if (krows == 16)
+        if (krows == 32)
+            cb_sweeps_persistent<32><<<grid, 256, persistent_smem(32), s>>>(packed, rows, (int)L, WR, W, row_to_slot, thresh, rk,
+                                                           c0, np, stats, 4u, sync, (uint32_t)group);
+        else if (krows == 16)
             cb_sweeps_persistent<16><<<grid, 256, persistent_smem(16), s>>>(packed, rows, (int)L, WR, W, row_to_slot, thresh, rk,
                                                            c0, np, stats, 4u, sync, (uint32_t)group);
         else if (krows == 8)

@@ -278,6 +278,8 @@ def test_full_states_match_oracle(mods, L, R, sweeps, every, rec_every):
     (512, 9, 0, 6, "0", "4"),      # L = 512, grouped 4-row items
     (1024, 16, 1, 4, None, None),  # auto: 2 rows per thread (a rank's C3 shard at 16 GPUs)
     (1536, 3, 2, 3, None, "16"),   # 9 blocks per lattice and phase (odd), WR = 24
+    (2048, 4, 1, 3, None, "32"),   # 32 rows per thread (the C4 choice), ties from L2
+    (1024, 8, 0, 2, "0", "32"),    # 32 rows, grouped
 ])
 def test_persistent_sweeps_equal_per_launch_path(mods, monkeypatch, L, R, first, nsweeps, per_slot, rows):
     """The one-launch dataflow path (cb_sweeps_persistent) and the per-launch
