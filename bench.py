@@ -359,7 +359,10 @@ def main():
     elif persistent:  # one launch per interval: all 2*every half-sweeps
         launch_ms = statistics.mean(sweep_ms)
         bytes_per_launch = ALG_BYTES_PER_ATTEMPT * local_rows * L * L * every
-        kernel_name = "cb_sweeps_persistent<16>"
+        # rows per thread as the launcher picks them (csrc/checkerboard.cu)
+        slots = 3 * torch.cuda.get_device_properties(dev).multi_processor_count
+        krows = 32 if local_rows * (L * L // (256 * 64 * 32)) >= 8 * slots else 16
+        kernel_name = f"cb_sweeps_persistent<{krows}>"
     else:
         launch_ms = statistics.mean(sweep_ms) / (2.0 * every)  # two colour launches per sweep
         bytes_per_launch = ALG_BYTES_PER_ATTEMPT * local_rows * L * L / 2
