@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(128) commit_kernel(CommitArgs C) {
     }
 }
 
-// ---------------------------------------- 1024-attempt windows (L >= 512) --
+// ------------------------------------------ 1024-attempt windows (L >= 16) --
 // For integer J, B and no per-attempt recording (the energy sum is then
 // order-free) and lattices large enough that attempts rarely touch, a slot's
 // attempts are committed 1024 at a time by a whole CTA:
@@ -1099,13 +1099,14 @@ int launch_advance_2phase(const AdvanceArgs& a, void* ws, int64_t ws_bytes, cuda
         return PTMH_ERR_ARG;
     }
     const int nbuf = a.nsteps > stride ? 2 : 1;
-    // 1024-attempt CTA windows: bit lattices, order-free energy sums, and
-    // L >= 512 so that a window holds few dependent attempts
+    // 1024-attempt CTA windows: bit lattices, order-free energy sums, L >= 16
+    // (measured against the warp-per-slot commit: 256^2 x 64 slots 2.0e9 ->
+    // 1.2e10, 128^2 x 256 4.8e9 -> 1.4e10, 32^2 x 256 3.6e9 -> 4.7e9; equal at 8^2)
     // (PTMH_EXACT_WINDOWS=0 forces the warp path, =2 the window path at any
     // L: A/B in tools/, dependent-heavy windows in tests)
     const char* ew = getenv("PTMH_EXACT_WINDOWS");
     const bool windows = !rounds && a.bits && a.int_energy && a.record == 0 && a.L <= 4096 &&
-                         (ew && ew[0] == '2' ? a.L >= 3 : a.L >= 512) && !(ew && ew[0] == '0');
+                         (ew && ew[0] == '2' ? a.L >= 3 : a.L >= 16) && !(ew && ew[0] == '0');
     size_t res_smem = 0;
     if (rounds) {  // exact_resident_kernel: one CTA, a warp per slot, every lattice in shared memory
         res_smem = (size_t)nslots * (size_t)((a.L * a.L + 31) / 32) * 4;
