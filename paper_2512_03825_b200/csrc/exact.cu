@@ -638,8 +638,18 @@ __global__ void __launch_bounds__(256, PTMH_DRAW_MINB) draw_w_kernel(DrawArgs D)
     }
 }
 
+// kRec: per-attempt E and M recorded (record 1).  With integer J and B every
+// partial sum is exact, so the window's energies in attempt order are a
+// CTA-wide prefix sum of the accepted increments (the -0.0 identity and the
+// "no accepted attempt yet" rule keep the reference's signed zeros).
+template <bool kRec>
 __global__ void __launch_bounds__(256) commit_w_kernel(CommitArgs C) {
     __shared__ uint32_t dep_bits[kWin / 32];
+    __shared__ double s_d[kRec ? kWin : 1];
+    __shared__ int s_ds[kRec ? kWin : 1];
+    __shared__ double w_d[8];
+    __shared__ long long w_ds[8];
+    __shared__ int w_cnt[8];
     __shared__ int dep_list[kWin];
     __shared__ double red_d[8];
     __shared__ long long red_s[8];
@@ -661,6 +671,9 @@ __global__ void __launch_bounds__(256) commit_w_kernel(CommitArgs C) {
     };
     double acc_d = -0.0;  // IEEE identity (see commit_kernel)
     long long acc_ds = 0;
+    double e_run = kRec ? A.energies[slot] : 0.0;  // energy / spin sum before the window
+    long long s_run = kRec ? A.spin_sums[slot] : 0;
+    const double nsd = (double)((int64_t)Li * Li);
     const int32_t* rs = C.rec_site + s * C.stride;
     const uint32_t* ra = C.rec_acc + s * C.stride;
     // the next window's records are loaded while this one commits
@@ -674,6 +687,12 @@ __global__ void __launch_bounds__(256) commit_w_kernel(CommitArgs C) {
     }
     for (int64_t w0 = 0; w0 < C.n; w0 += kWin) {
         if (threadIdx.x < kWin / 32) dep_bits[threadIdx.x] = 0;
+        if (kRec)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                s_d[q * 256 + threadIdx.x] = -0.0;
+                s_ds[q * 256 + threadIdx.x] = 0;
+            }
         __syncthreads();
         // ---- free attempts: one parallel pass
         int st[4];
@@ -709,8 +728,13 @@ __global__ void __launch_bounds__(256) commit_w_kernel(CommitArgs C) {
             const double d = A.dcls[cls];
             if ((d <= 0.0) || ((am[q] >> cls) & 1u)) {
                 atomicXor(&latw[st[q] >> 5], 1u << (st[q] & 31));
-                acc_d = __dadd_rn(acc_d, d);
-                acc_ds += -2 * sp[q];
+                if (kRec) {
+                    s_d[q * 256 + threadIdx.x] = d;
+                    s_ds[q * 256 + threadIdx.x] = -2 * sp[q];
+                } else {
+                    acc_d = __dadd_rn(acc_d, d);
+                    acc_ds += -2 * sp[q];
+                }
             }
         }
         __syncthreads();
@@ -750,8 +774,13 @@ __global__ void __launch_bounds__(256) commit_w_kernel(CommitArgs C) {
                         const double d = A.dcls[cls];
                         if ((d <= 0.0) || ((amk >> cls) & 1u)) {
                             atomicXor(&latw[x >> 5], 1u << (x & 31));
-                            acc_d = __dadd_rn(acc_d, d);
-                            acc_ds += -2 * spx;
+                            if (kRec) {
+                                s_d[a - w0] = d;
+                                s_ds[a - w0] = -2 * spx;
+                            } else {
+                                acc_d = __dadd_rn(acc_d, d);
+                                acc_ds += -2 * spx;
+                            }
                         }
                     }
                     __syncwarp();
@@ -760,6 +789,82 @@ __global__ void __launch_bounds__(256) commit_w_kernel(CommitArgs C) {
             }
         }
         __syncthreads();
+        if (kRec) {
+            // prefix over the window in attempt order: thread t owns attempts
+            // 4t .. 4t+3 (local scan), warps scan thread totals, warp totals
+            // are scanned through shared memory
+            double ld[4];
+            int lds[4], lcnt[4];
+            double run_d = -0.0;
+            int run_ds = 0, run_c = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int k = 4 * (int)threadIdx.x + j;
+                run_d = __dadd_rn(run_d, s_d[k]);
+                run_ds += s_ds[k];
+                run_c += s_ds[k] != 0;
+                ld[j] = run_d;
+                lds[j] = run_ds;
+                lcnt[j] = run_c;
+            }
+            double xd = run_d;  // inclusive scan of thread totals within the warp
+            int xds = run_ds, xc = run_c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double vd = __shfl_up_sync(kFull, xd, o);
+                const int vds = __shfl_up_sync(kFull, xds, o), vc = __shfl_up_sync(kFull, xc, o);
+                if (lane >= o) {
+                    xd = __dadd_rn(xd, vd);
+                    xds += vds;
+                    xc += vc;
+                }
+            }
+            if (lane == 31) {
+                w_d[warp] = xd;
+                w_ds[warp] = xds;
+                w_cnt[warp] = xc;
+            }
+            __syncthreads();
+            double pd = -0.0;  // exclusive prefix of this thread
+            long long pds = 0;
+            int pc = 0;
+            for (int k = 0; k < warp; ++k) {
+                pd = __dadd_rn(pd, w_d[k]);
+                pds += w_ds[k];
+                pc += w_cnt[k];
+            }
+            {  // exclusive within the warp: the previous lane's inclusive value
+                const double ud = __shfl_up_sync(kFull, xd, 1);
+                const int uds = __shfl_up_sync(kFull, xds, 1), uc = __shfl_up_sync(kFull, xc, 1);
+                if (lane > 0) {
+                    pd = __dadd_rn(pd, ud);
+                    pds += uds;
+                    pc += uc;
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int64_t aa = w0 + 4 * (int)threadIdx.x + j;
+                if (aa >= C.n) break;
+                const int cnt = pc + lcnt[j];
+                const double e_a = cnt > 0 ? __dadd_rn(e_run, __dadd_rn(pd, ld[j])) : e_run;
+                const long long s_a = s_run + pds + lds[j];
+                const int64_t col = A.start_iter + C.a0 + aa;
+                A.obs_e[slot * A.ncols + col] = e_a;
+                A.obs_m[slot * A.ncols + col] = __ddiv_rn((double)s_a, nsd);
+            }
+            double td = -0.0;  // window totals (every thread alike)
+            long long tds = 0;
+            int tc = 0;
+            for (int k = 0; k < 8; ++k) {
+                td = __dadd_rn(td, w_d[k]);
+                tds += w_ds[k];
+                tc += w_cnt[k];
+            }
+            if (tc > 0) e_run = __dadd_rn(e_run, td);
+            s_run += tds;
+            __syncthreads();  // w_* and s_d are rewritten by the next window
+        }
     }
     // order-free sums (integer-valued d): warp shuffles, then the CTA
     for (int o = 16; o > 0; o >>= 1) {
@@ -778,8 +883,8 @@ __global__ void __launch_bounds__(256) commit_w_kernel(CommitArgs C) {
             td = __dadd_rn(td, red_d[k]);
             ts += red_s[k];
         }
-        A.energies[slot] = __dadd_rn(A.energies[slot], td);
-        A.spin_sums[slot] += ts;
+        A.energies[slot] = kRec ? e_run : __dadd_rn(A.energies[slot], td);
+        A.spin_sums[slot] = kRec ? s_run : A.spin_sums[slot] + ts;
         if (C.last) {
             A.positions[slot] += 2 * (uint64_t)(C.a0 + C.n);
             A.iters_done[slot] = A.start_iter + C.a0 + C.n;
@@ -1105,7 +1210,7 @@ int launch_advance_2phase(const AdvanceArgs& a, void* ws, int64_t ws_bytes, cuda
     // (PTMH_EXACT_WINDOWS=0 forces the warp path, =2 the window path at any
     // L: A/B in tools/, dependent-heavy windows in tests)
     const char* ew = getenv("PTMH_EXACT_WINDOWS");
-    const bool windows = !rounds && a.bits && a.int_energy && a.record == 0 && a.L <= 4096 &&
+    const bool windows = !rounds && a.bits && a.int_energy && a.record <= 1 && a.L <= 4096 &&
                          (ew && ew[0] == '2' ? a.L >= 3 : a.L >= 16) && !(ew && ew[0] == '0');
     size_t res_smem = 0;
     if (rounds) {  // exact_resident_kernel: one CTA, a warp per slot, every lattice in shared memory
@@ -1161,8 +1266,10 @@ int launch_advance_2phase(const AdvanceArgs& a, void* ws, int64_t ws_bytes, cuda
             exact_resident_kernel<512><<<1, (unsigned)(32 * nslots), res_smem, sc>>>(C, *rounds);
         else if (rounds)
             exact_resident_kernel<1024><<<1, (unsigned)(32 * nslots), res_smem, sc>>>(C, *rounds);
+        else if (windows && a.record == 1)
+            commit_w_kernel<true><<<(unsigned)nslots, 256, 0, sc>>>(C);
         else if (windows)
-            commit_w_kernel<<<(unsigned)nslots, 256, 0, sc>>>(C);
+            commit_w_kernel<false><<<(unsigned)nslots, 256, 0, sc>>>(C);
         else if (a.bits)
             commit_kernel<true><<<ceil_div(nslots, 4), 128, 0, sc>>>(C);
         else
