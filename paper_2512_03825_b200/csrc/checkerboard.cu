@@ -382,7 +382,9 @@ __device__ __forceinline__ void ferro_strip(uint32_t* __restrict__ packed, int L
 }
 
 
-template <int kRows, bool kStats>
+// kColor; kStats: this sweep's (S, Bond) are needed (the launcher passes it
+// for the last sweep of the call only: colour 0 resets, colour 1 recomputes)
+template <int kRows, int kColor, bool kStats>
 __global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_half_sweep_ferro(
     uint32_t* __restrict__ packed, int64_t rows, int L, int WR, int64_t W,
     const int32_t* __restrict__ row_to_slot, const uint32_t* __restrict__ thresh, const RoundKeys32 rk,
@@ -396,10 +398,9 @@ __global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_half_sweep_ferro(
     const int64_t lat = active ? tid / per_lat : 0;
     const int rem = (int)(tid - lat * per_lat);
     int sumS = 0, sumB = 0;
-    ferro_strip<kRows, kStats ? 1 : 0, true, true>(packed, L, WR, W, row_to_slot, thresh, rk, ctr1, stats, esz,
-                                                   active,
-                                     lat, rem, tie_m[warp], tie_k4[warp], tie_sn[warp], sumS, sumB);
-    if (kStats) flush_stats(stats, lat, active, sumS, sumB);
+    ferro_strip<kRows, kColor, kStats, true>(packed, L, WR, W, row_to_slot, thresh, rk, ctr1, stats, esz, active,
+                                             lat, rem, tie_m[warp], tie_k4[warp], tie_sn[warp], sumS, sumB);
+    if (kColor == 1 && kStats) flush_stats(stats, lat, active, sumS, sumB);
 }
 
 // ---------------------------------------- persistent multi-sweep ferro path --
@@ -931,24 +932,28 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
     for (int64_t t = first_sweep; t < first_sweep + n_sweeps; ++t) {
         for (int color = 0; color < 2; ++color) {
             const uint32_t ctr1 = (uint32_t)(2 * t + color);
-            if (fast && ferro && L >= 1024) {  // long rows: amortise the per-thread setup over 16
+            const bool last = t + 1 == first_sweep + n_sweeps;  // only its (S, Bond) are read
+            if (fast && ferro) {  // long rows (L >= 1024): amortise the per-thread setup over 16
                 const int WR = (int)(L / 64);
-                const int64_t threads = rows * (L / 16) * WR;
-                if (color == 0)
-                    cb_half_sweep_ferro<16, false><<<ceil_div(threads, 256), 256, 0, s>>>(
-                        packed, rows, (int)L, WR, W, row_to_slot, thresh, rk, ctr1, stats, 4u);
-                else
-                    cb_half_sweep_ferro<16, true><<<ceil_div(threads, 256), 256, 0, s>>>(
-                        packed, rows, (int)L, WR, W, row_to_slot, thresh, rk, ctr1, stats, 4u);
-            } else if (fast && ferro) {
-                const int WR = (int)(L / 64);
-                const int64_t threads = rows * (L / kFastRows) * WR;
-                if (color == 0)
-                    cb_half_sweep_ferro<kFastRows, false><<<ceil_div(threads, 256), 256, 0, s>>>(
-                        packed, rows, (int)L, WR, W, row_to_slot, thresh, rk, ctr1, stats, 4u);
-                else
-                    cb_half_sweep_ferro<kFastRows, true><<<ceil_div(threads, 256), 256, 0, s>>>(
-                        packed, rows, (int)L, WR, W, row_to_slot, thresh, rk, ctr1, stats, 4u);
+                const bool r16 = L >= 1024;
+                const int64_t threads = rows * (L / (r16 ? 16 : kFastRows)) * WR;
+                const unsigned g = ceil_div(threads, 256);
+#define PTMH_FERRO(R, C, S) \
+    cb_half_sweep_ferro<R, C, S><<<g, 256, 0, s>>>(packed, rows, (int)L, WR, W, row_to_slot, thresh, rk, ctr1, stats, 4u)
+                if (r16) {
+                    if (color == 0) {
+                        if (last) PTMH_FERRO(16, 0, true); else PTMH_FERRO(16, 0, false);
+                    } else {
+                        if (last) PTMH_FERRO(16, 1, true); else PTMH_FERRO(16, 1, false);
+                    }
+                } else {
+                    if (color == 0) {
+                        if (last) PTMH_FERRO(kFastRows, 0, true); else PTMH_FERRO(kFastRows, 0, false);
+                    } else {
+                        if (last) PTMH_FERRO(kFastRows, 1, true); else PTMH_FERRO(kFastRows, 1, false);
+                    }
+                }
+#undef PTMH_FERRO
             } else if (fast) {
                 const int WR = (int)(L / 64);
                 const int64_t threads = rows * (L / kFastRows) * WR;
