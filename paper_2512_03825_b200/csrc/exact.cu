@@ -4,6 +4,16 @@
 //   fill_kernel          kernels.py:26-45   exact-count Fisher-Yates init
 //   row_stats_kernel     kernels.py:48-59   integer energy / spin-sum accumulators
 //   advance_kernel       kernels.py:62-113  random-site MH, incremental E / sum(s)
+//                                           (single pass; full_states recording)
+//   draw_kernel +        kernels.py:62-113  two phases: every draw / site /
+//   commit_kernel                           acceptance bit in parallel, then a
+//                                           warp-per-slot commit in 32-windows
+//   draw_w_kernel +      kernels.py:62-113  integer J, B, L >= 16: 1024-attempt
+//   commit_w_kernel<rec>                    CTA windows (free attempts in one
+//                                           pass, dependents in order)
+//   exact_resident_kernel executor.py:227-262 + the above: <= 32 slots, every
+//                                           lattice in shared memory, swap
+//                                           rounds inside the launch
 //   swap_kernel          kernels.py:116-148 logistic replica exchange (labels only)
 //
 // Parallelism.  The reference chain is sequential per slot, but its draws are
