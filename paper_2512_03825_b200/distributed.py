@@ -55,13 +55,10 @@ class ShardedCheckerboard:
         lo, hi = self.bounds[self.rank]
         if all(h - l == self.maxc for l, h in self.bounds):
             # equal shards (C3: 256 over 1/2/4/8): gather straight into the
-            # stats; NCCL gathers in place (the local rows are already at
-            # their offset), other backends from a copy
-            if dist.get_backend(self.group) == "nccl":
-                dist.all_gather_into_tensor(self.eng.stats, self.eng.local_stats, group=self.group)
-            else:
-                self._send.copy_(self.eng.local_stats)
-                dist.all_gather_into_tensor(self.eng.stats, self._send, group=self.group)
+            # stats, from a separate send buffer (no aliasing of input and
+            # output, which only world-1 runs could test here)
+            self._send.copy_(self.eng.local_stats)
+            dist.all_gather_into_tensor(self.eng.stats, self._send, group=self.group)
             return
         self._send[: hi - lo].copy_(self.eng.local_stats)
         dist.all_gather_into_tensor(self._recv, self._send, group=self.group)
