@@ -399,6 +399,44 @@ def main():
                "d2h_bytes_per_step": int(R * L * L + R * 8 * 3 + 16),
                "path": "kernels.cb_interval -> ptmh_host_cb_interval (pinned int8 lattices)"}
 
+    # ---- end to end across ranks (N > 1): the same interval through the
+    # sharded driver, each rank's int8 lattices copied in from and out to
+    # pinned host memory every step (the host plugin is single-device)
+    if not args.no_e2e and sharded and not resident:
+        loc = eng.spins_int8()
+        host = torch.empty(tuple(loc.shape), dtype=torch.int8).pin_memory()
+        host.copy_(loc)
+        dbuf = torch.empty_like(loc)
+        sweep0, rnd0 = state["sweep"], state["round"]
+
+        def e2e_step(t, r):
+            dbuf.copy_(host, non_blocking=True)
+            eng.load_spins(dbuf)
+            eng.sweeps(t, every)
+            drv.gather_stats()
+            eng.exchange(r)
+            host.copy_(eng.spins_int8(), non_blocking=True)
+
+        for k in range(2):  # warm
+            e2e_step(sweep0, rnd0)
+            sweep0 += every
+            rnd0 += 1
+        n_e2e = max(3, min(args.steps, 10))
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for k in range(n_e2e):
+            e2e_step(sweep0, rnd0)
+            sweep0 += every
+            rnd0 += 1
+        torch.cuda.synchronize()
+        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        e2e = {"value": n_e2e * R * L * L * every / float(dt.item()), "unit": "attempts/s",
+               "h2d_bytes_per_step": int(R * L * L), "d2h_bytes_per_step": int(R * L * L),
+               "path": "distributed.ShardedCheckerboard, per-rank int8 lattices from / to pinned host "
+                       "memory each step (bytes summed over ranks); wall clock, max over ranks"}
+
     # the bit-exact reference chain (sweep_mode="exact") on the same shape
     exact = None
     if rank == 0 and not sharded and not args.no_exact and L <= 4096:

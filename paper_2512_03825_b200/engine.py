@@ -241,8 +241,9 @@ class CheckerboardEngine(_Base):
         """Replace the local lattices with given int8 configurations."""
         s = self._s()
         spins = spins.to(self.dev, torch.int8).contiguous()
-        _lib.call("ptmh_row_stats", _P(spins), self.rows, self.L, _P(self.local_stats), s)
         _lib.call("ptmh_cb_pack", _P(spins), self.rows, self.L, _P(self.packed), s)
+        # (S, Bond) from the packed words: the word-parallel kernel for L % 64 == 0
+        _lib.call("ptmh_cb_row_stats", _P(self.packed), self.rows, self.L, _P(self.local_stats), s)
 
     def sweeps(self, first_sweep: int, n: int) -> None:
         if self.rows == 0 or n <= 0:
