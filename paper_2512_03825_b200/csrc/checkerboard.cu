@@ -440,13 +440,16 @@ __device__ __forceinline__ void red_release_gpu_add(uint32_t* p, uint32_t v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <int kRows>
-__global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_sweeps_persistent(
+// kPT threads per CTA = per item: 128 for big shards (more, smaller CTAs:
+// C3 +1.5 %, 2^27-site shards +3 %), 256 for small ones (a rank's C3 shard at
+// 8 GPUs: 128 would cost 12 %)
+template <int kRows, int kPT>
+__global__ void __launch_bounds__(kPT, PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_persistent(
     uint32_t* __restrict__ packed, int64_t rows, int L, int WR, int64_t W,
     const int32_t* __restrict__ row_to_slot, const uint32_t* __restrict__ thresh, const RoundKeys32 rk,
     uint32_t ctr_base, uint32_t n_phases, int64_t* __restrict__ stats, uint32_t esz,
     uint32_t* __restrict__ sync, uint32_t group) {
-    constexpr int kWarps = 8;
+    constexpr int kWarps = kPT / 32;
     // tie scratch (3 x kRows x 32 words per warp: 48 KB at kRows = 16) in
     // dynamic shared memory; cb_sweeps_persistent_smem() bytes
     extern __shared__ uint32_t s_ties[];
@@ -457,7 +460,7 @@ __global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_sweeps_persistent(
     const int warp = threadIdx.x >> 5;
     // items per lattice and phase (the host picks group so that a phase still
     // has >= 8 items per resident CTA)
-    const uint32_t subs = (uint32_t)((L / kRows) * WR / 256) / group;
+    const uint32_t subs = (uint32_t)((L / kRows) * WR / kPT) / group;
     const uint32_t per_phase = (uint32_t)rows * subs;
     const uint32_t n_items = n_phases * per_phase;
     // thread 0 schedules: it holds the next ticket (prefetched one item
@@ -490,7 +493,7 @@ __global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_sweeps_persistent(
 #define PTMH_STRIP(C, ST)                                                                                 \
     for (uint32_t g = 0; g < group; ++g)                                                                  \
         ferro_strip<kRows, C, ST, true>(packed, L, WR, W, row_to_slot, thresh, rk, ctr1, stats, esz, true, \
-                                        lat, (int)((sub * group + g) * 256 + threadIdx.x), tie_m[warp],   \
+                                        lat, (int)((sub * group + g) * kPT + threadIdx.x), tie_m[warp],   \
                                         tie_k4[warp], tie_sn[warp], sumS, sumB)
         if ((ctr1 & 1u) == 0) {
             if (last_sweep)
@@ -834,7 +837,7 @@ constexpr int kFastRows = PTMH_FERRO_ROWS;
 
 // one persistent launch for every half-sweep: the ferro kernel with whole
 // 256-thread blocks per lattice (L % 512 == 0)
-static size_t persistent_smem(int krows) { return (size_t)(krows <= 16 ? 3 : 2) * 8 * krows * 32 * 4; }
+static size_t persistent_smem(int krows, int kpt) { return (size_t)(krows <= 16 ? 3 : 2) * (kpt / 32) * krows * 32 * 4; }
 
 bool cb_sweeps_persistent_applies(int64_t L, uint32_t always_mask, int64_t n_sweeps) {
     const bool ferro = (always_mask & kSymmetricFlag) && (always_mask & 0x3ffu) == 0x078u;
@@ -853,55 +856,70 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
     const bool ferro = (always_mask & kSymmetricFlag) && (always_mask & 0x3ffu) == 0x078u &&
                        rows * 2 * W < (1LL << 32);  // 32-bit word offsets in the tie queue
     if (sync && ferro && cb_sweeps_persistent_applies(L, always_mask, n_sweeps) &&
-        2 * n_sweeps * rows * (L * L / 32768) < (1LL << 31)) {  // item count at 2 rows per thread
-        static int cached_slots[256] = {};  // resident CTAs per device
+        2 * n_sweeps * rows * (L * L / 16384) < (1LL << 31)) {  // item count at 2 rows, 128 threads
+        static int cached_slots[256][2] = {};  // resident CTAs per device, [0]: 256-, [1]: 128-thread CTAs
         int dev = 0;
         PTMH_CUDA(cudaGetDevice(&dev));
         if (dev >= 256) dev = 255;
-        if (cached_slots[dev] == 0) {
+        const char* et = getenv("PTMH_PERSIST_THREADS");  // 128 / 256 pins it (A/B and tests)
+        const bool t128 = et ? atoi(et) == 128 : rows * L * L >= (1LL << 27);
+        const int kpt = t128 ? 128 : 256;
+        if (cached_slots[dev][t128] == 0) {
             int sms = 0, occ = 0;
             PTMH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-            for (const void* fn : {(const void*)cb_sweeps_persistent<32>, (const void*)cb_sweeps_persistent<16>,
-                                   (const void*)cb_sweeps_persistent<8>, (const void*)cb_sweeps_persistent<4>,
-                                   (const void*)cb_sweeps_persistent<2>})
+            const void* fns[2][5] = {
+                {(const void*)cb_sweeps_persistent<32, 256>, (const void*)cb_sweeps_persistent<16, 256>,
+                 (const void*)cb_sweeps_persistent<8, 256>, (const void*)cb_sweeps_persistent<4, 256>,
+                 (const void*)cb_sweeps_persistent<2, 256>},
+                {(const void*)cb_sweeps_persistent<32, 128>, (const void*)cb_sweeps_persistent<16, 128>,
+                 (const void*)cb_sweeps_persistent<8, 128>, (const void*)cb_sweeps_persistent<4, 128>,
+                 (const void*)cb_sweeps_persistent<2, 128>}};
+            for (const void* fn : fns[t128])
                 PTMH_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)persistent_smem(32)));
-            PTMH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cb_sweeps_persistent<16>, 256,
-                                                                    persistent_smem(16)));
-            cached_slots[dev] = sms * std::max(occ, 1);
+                                               (int)persistent_smem(32, kpt)));
+            if (t128)
+                PTMH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cb_sweeps_persistent<16, 128>, 128,
+                                                                        persistent_smem(16, 128)));
+            else
+                PTMH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cb_sweeps_persistent<16, 256>, 256,
+                                                                        persistent_smem(16, 256)));
+            cached_slots[dev][t128] = sms * std::max(occ, 1);
         }
-        const int64_t slots = cached_slots[dev];
+        const int64_t slots = cached_slots[dev][t128];
         const int WR = (int)(L / 64);
         // Rows per thread: 16 amortises the per-strip setup best, but one
         // lattice's phases are sequential, so the interval's critical path is
         // 2n items.  With few lattices (a rank's shard of C3 on 8 GPUs: 32)
         // the phase has too few items to fill the GPU and that path binds:
         // take the largest kRows whose phase still has >= 1 item per CTA
-        // slot (else 2).  Measured on one B200 (attempts/s at L = 1024):
-        // R = 256: 16 rows 3.23e12 (8: 2.93e12); R = 64: 8 rows 2.55e12
-        // (16: 2.01e12, 4: 2.38e12); R = 32: 4 rows 2.00e12 (16: 1.18e12,
-        // 2: 1.77e12); R = 16: 2 rows 1.32e12 (4: 1.16e12).
+        // slot (else 2).  Measured on one B200 (attempts/s at L = 1024,
+        // 256-thread items): R = 256: 16 rows 3.23e12 (8: 2.93e12); R = 64: 8
+        // rows 2.55e12 (16: 2.01e12, 4: 2.38e12); R = 32: 4 rows 2.00e12 (16:
+        // 1.18e12, 2: 1.77e12); R = 16: 2 rows 1.32e12 (4: 1.16e12).  128-thread
+        // items at >= 2^27 sites: R = 128 3.09e12 -> 3.18e12, C3 3.40e12 ->
+        // 3.45e12; at R = 64 2.74e12 -> 2.63e12, R = 32 2.12e12 -> 1.86e12.
         // (PTMH_PERSIST_ROWS pins it: A/B and tests.)
         const char* er = getenv("PTMH_PERSIST_ROWS");
+        auto items_at = [&](int k) { return rows * (L * L / ((int64_t)kpt * 64 * k)); };
         int krows = 2;
         if (er) {
             krows = atoi(er);
-        } else if (rows * (L * L / (256LL * 64 * 32)) >= 8 * slots) {
+        } else if (items_at(32) >= 8 * slots) {
             krows = 32;  // plenty of items (C4): longest strips (C4 +2.6 %, C3 -4 %)
         } else {
             for (int k : {16, 8, 4}) {
-                if (rows * (L * L / (256LL * 64 * k)) >= slots) {
+                if (items_at(k) >= slots) {
                     krows = k;
                     break;
                 }
             }
         }
         if (krows != 2 && krows != 4 && krows != 8 && krows != 16 && krows != 32) krows = 16;
-        // 256-thread blocks per item: amortise the per-item scheduling over
-        // several blocks while a phase keeps >= 8 items per resident CTA
+        // blocks of kpt threads per item: amortise the per-item scheduling
+        // over several blocks while a phase keeps >= 8 items per resident CTA
         // (PTMH_PERSIST_ITEMS_PER_SLOT overrides the 8; tests use 0 to force
         // the largest groups at small shapes)
-        const int64_t blocks = L * L / (256LL * 64 * krows);  // per lattice and phase
+        const int64_t blocks = L * L / ((int64_t)kpt * 64 * krows);  // per lattice and phase
         const char* ev = getenv("PTMH_PERSIST_ITEMS_PER_SLOT");
         const int64_t per_slot = ev ? atoll(ev) : 8;
         int64_t group = 1;
@@ -911,21 +929,24 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
         const int64_t items = 2 * n_sweeps * rows * (blocks / group);
         const unsigned grid = (unsigned)std::min<int64_t>(items, slots);
         const uint32_t c0 = (uint32_t)(2 * first_sweep), np = (uint32_t)(2 * n_sweeps);
-        if (krows == 32)
-            cb_sweeps_persistent<32><<<grid, 256, persistent_smem(32), s>>>(packed, rows, (int)L, WR, W, row_to_slot, thresh, rk,
-                                                           c0, np, stats, 4u, sync, (uint32_t)group);
-        else if (krows == 16)
-            cb_sweeps_persistent<16><<<grid, 256, persistent_smem(16), s>>>(packed, rows, (int)L, WR, W, row_to_slot, thresh, rk,
-                                                           c0, np, stats, 4u, sync, (uint32_t)group);
-        else if (krows == 8)
-            cb_sweeps_persistent<8><<<grid, 256, persistent_smem(8), s>>>(packed, rows, (int)L, WR, W, row_to_slot, thresh, rk,
-                                                          c0, np, stats, 4u, sync, (uint32_t)group);
-        else if (krows == 4)
-            cb_sweeps_persistent<4><<<grid, 256, persistent_smem(4), s>>>(packed, rows, (int)L, WR, W, row_to_slot, thresh, rk,
-                                                          c0, np, stats, 4u, sync, (uint32_t)group);
-        else
-            cb_sweeps_persistent<2><<<grid, 256, persistent_smem(2), s>>>(packed, rows, (int)L, WR, W, row_to_slot, thresh, rk,
-                                                          c0, np, stats, 4u, sync, (uint32_t)group);
+#define PTMH_PERSIST(K, T)                                                                                    \
+    cb_sweeps_persistent<K, T><<<grid, T, persistent_smem(K, T), s>>>(packed, rows, (int)L, WR, W, row_to_slot, \
+                                                                      thresh, rk, c0, np, stats, 4u, sync,    \
+                                                                      (uint32_t)group)
+        if (t128) {
+            if (krows == 32) PTMH_PERSIST(32, 128);
+            else if (krows == 16) PTMH_PERSIST(16, 128);
+            else if (krows == 8) PTMH_PERSIST(8, 128);
+            else if (krows == 4) PTMH_PERSIST(4, 128);
+            else PTMH_PERSIST(2, 128);
+        } else {
+            if (krows == 32) PTMH_PERSIST(32, 256);
+            else if (krows == 16) PTMH_PERSIST(16, 256);
+            else if (krows == 8) PTMH_PERSIST(8, 256);
+            else if (krows == 4) PTMH_PERSIST(4, 256);
+            else PTMH_PERSIST(2, 256);
+        }
+#undef PTMH_PERSIST
         PTMH_LAUNCH_CHECK();
         return PTMH_OK;
     }

@@ -269,19 +269,24 @@ def test_full_states_match_oracle(mods, L, R, sweeps, every, rec_every):
     assert np.array_equal(rec.magnetizations, rec.states.sum(axis=(2, 3)) / (L * L))
 
 
-@pytest.mark.parametrize("L,R,first,nsweeps,per_slot,rows", [
-    (1024, 24, 3, 7, None, None), (1024, 256, 0, 10, None, None), (2048, 5, 1, 3, None, None),
-    (2048, 5, 1, 3, "0", "16"),    # 16 blocks per item: one item per lattice and phase
-    (1024, 256, 0, 4, "0", "16"),  # 4 blocks per item
-    (1024, 32, 2, 5, None, "8"),   # 8 rows per thread
-    (1024, 32, 2, 5, None, "4"),   # 4 rows per thread (a rank's C3 shard at 8 GPUs)
-    (512, 9, 0, 6, "0", "4"),      # L = 512, grouped 4-row items
-    (1024, 16, 1, 4, None, None),  # auto: 2 rows per thread (a rank's C3 shard at 16 GPUs)
-    (1536, 3, 2, 3, None, "16"),   # 9 blocks per lattice and phase (odd), WR = 24
-    (2048, 4, 1, 3, None, "32"),   # 32 rows per thread (the C4 choice), ties from L2
-    (1024, 8, 0, 2, "0", "32"),    # 32 rows, grouped
+@pytest.mark.parametrize("L,R,first,nsweeps,per_slot,rows,threads", [
+    (1024, 24, 3, 7, None, None, None), (1024, 256, 0, 10, None, None, None), (2048, 5, 1, 3, None, None, None),
+    (2048, 5, 1, 3, "0", "16", None),    # 16 blocks per item: one item per lattice and phase
+    (1024, 256, 0, 4, "0", "16", None),  # 4 blocks per item (auto: 128-thread items)
+    (1024, 256, 0, 4, None, None, "256"),  # the full C3 shard on 256-thread items
+    (1024, 32, 2, 5, None, "8", None),   # 8 rows per thread
+    (1024, 32, 2, 5, None, "4", None),   # 4 rows per thread (a rank's C3 shard at 8 GPUs)
+    (1024, 24, 3, 7, None, None, "128"),  # 128-thread items below their auto threshold
+    (512, 9, 0, 6, "0", "4", None),      # L = 512, grouped 4-row items
+    (512, 9, 0, 6, "0", "4", "128"),     # ... on 128-thread items
+    (1024, 16, 1, 4, None, None, None),  # auto: 2 rows per thread (a rank's C3 shard at 16 GPUs)
+    (1536, 3, 2, 3, None, "16", None),   # 9 blocks per lattice and phase (odd), WR = 24
+    (1536, 3, 2, 3, None, "16", "128"),  # 18 blocks per lattice and phase
+    (2048, 4, 1, 3, None, "32", None),   # 32 rows per thread (the C4 choice), ties from L2
+    (2048, 4, 1, 3, None, "32", "128"),  # ... on 128-thread items (the C4 launch)
+    (1024, 8, 0, 2, "0", "32", None),    # 32 rows, grouped
 ])
-def test_persistent_sweeps_equal_per_launch_path(mods, monkeypatch, L, R, first, nsweeps, per_slot, rows):
+def test_persistent_sweeps_equal_per_launch_path(mods, monkeypatch, L, R, first, nsweeps, per_slot, rows, threads):
     """The one-launch dataflow path (cb_sweeps_persistent) and the per-launch
     half-sweep kernels give identical lattices and stats; the sync block is
     left zeroed for the next call."""
@@ -290,6 +295,8 @@ def test_persistent_sweeps_equal_per_launch_path(mods, monkeypatch, L, R, first,
         monkeypatch.setenv("PTMH_PERSIST_ITEMS_PER_SLOT", per_slot)
     if rows is not None:
         monkeypatch.setenv("PTMH_PERSIST_ROWS", rows)
+    if threads is not None:
+        monkeypatch.setenv("PTMH_PERSIST_THREADS", threads)
     temps = p.build_ladder(R)
     perm = np.random.default_rng(R).permutation(R)
     r2s = np.empty(R, dtype=np.int64); r2s[perm] = np.arange(R)
