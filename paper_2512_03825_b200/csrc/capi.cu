@@ -84,6 +84,8 @@ struct Workspace {
     cudaEvent_t ev_in[64], ev_out[64];  // >= chunks per pipelined call
     cudaEvent_t ev_t0, ev_tab;
     bool events = false;
+    void* pin = nullptr;  // pinned staging of the small per-call arrays (one H2D, one D2H)
+    size_t pin_n = 0;
 };
 
 // one workspace per device (buffers, streams and events are device-bound),
@@ -119,6 +121,18 @@ static int ws_prepare(Workspace& w) {
         PTMH_CUDA(cudaEventCreateWithFlags(&w.ev_tab, cudaEventDisableTiming));
         w.events = true;
     }
+    return PTMH_OK;
+}
+
+static int ws_pinned(Workspace& w, size_t bytes, uint8_t** out) {
+    if (w.pin_n < bytes) {
+        if (w.pin) PTMH_CUDA(cudaFreeHost(w.pin));
+        w.pin = nullptr;
+        w.pin_n = 0;
+        PTMH_CUDA(cudaMallocHost(&w.pin, bytes));
+        w.pin_n = bytes;
+    }
+    *out = static_cast<uint8_t*>(w.pin);
     return PTMH_OK;
 }
 
@@ -639,21 +653,41 @@ int ptmh_host_cb_interval(int8_t* spins, int64_t R, int64_t L, int64_t* slot_to_
         fprintf(stderr, "ptmh: spins %p attr rc=%d type=%d\n", (void*)spins, (int)e, (int)pa.type);
     }
     const int64_t nsite = L * L, W = cb_words(L);
-    int8_t* d_spins; uint32_t *d_packed, *d_thr; int64_t *d_stats, *d_s2r, *d_sums, *d_cnt;
-    int32_t* d_r2s; double *d_b, *d_e;
+    int8_t* d_spins;
+    uint32_t* d_packed;
+    int64_t* d_stats;
     PTMH_TRY(ws_get(g_ws, 0, (size_t)(R * nsite), &d_spins));
     PTMH_TRY(ws_get(g_ws, 13, (size_t)(R * 2 * W), &d_packed));
     PTMH_TRY(ws_get(g_ws, 14, (size_t)(R * 2), &d_stats));
-    PTMH_TRY(ws_get(g_ws, 15, (size_t)(R * 10), &d_thr));
-    PTMH_TRY(ws_get(g_ws, 1, (size_t)R, &d_s2r));
-    PTMH_TRY(ws_get(g_ws, 16, (size_t)R, &d_r2s));
-    PTMH_TRY(ws_get(g_ws, 11, (size_t)R, &d_b));
-    PTMH_TRY(ws_get(g_ws, 4, (size_t)R, &d_e));
-    PTMH_TRY(ws_get(g_ws, 5, (size_t)R, &d_sums));
-    PTMH_TRY(ws_get(g_ws, 12, 2, &d_cnt));
+    // The small arrays travel as one block each way (pinned staging, one H2D
+    // and one D2H instead of nine copies from pageable memory: 8-byte
+    // aligned offsets) -- outputs first: slot_to_row | energies | spin_sums |
+    // counters, then the inputs only: betas | thresholds | row_to_slot.
+    const size_t o_e = 8 * R, o_sums = 16 * R, o_cnt = 24 * R, o_b = o_cnt + 16, o_thr = o_b + 8 * R,
+                 o_r2s = o_thr + 40 * R, n_small = o_r2s + 8 * R, n_out = o_cnt + 16;
+    uint8_t *h_small, *d_small;
+    PTMH_TRY(ws_pinned(g_ws, n_small, &h_small));
+    PTMH_TRY(ws_get(g_ws, 19, n_small, &d_small));
+    memcpy(h_small, slot_to_row, 8 * R);
+    memset(h_small + o_e, 0, o_b - o_e);  // energies, sums (recomputed on the device), counters = 0
+    memcpy(h_small + o_b, betas, 8 * R);
+    memcpy(h_small + o_thr, thr.data(), 40 * R);
+    memcpy(h_small + o_r2s, r2s.data(), 4 * R);
+    int64_t* d_s2r = reinterpret_cast<int64_t*>(d_small);
+    double* d_e = reinterpret_cast<double*>(d_small + o_e);
+    int64_t* d_sums = reinterpret_cast<int64_t*>(d_small + o_sums);
+    int64_t* d_cnt = reinterpret_cast<int64_t*>(d_small + o_cnt);
+    double* d_b = reinterpret_cast<double*>(d_small + o_b);
+    uint32_t* d_thr = reinterpret_cast<uint32_t*>(d_small + o_thr);
+    int32_t* d_r2s = reinterpret_cast<int32_t*>(d_small + o_r2s);
+    // Replica chunks pipeline the lattice copies with the compute.  One chunk
+    // per 2 MiB of int8 lattices, at most 8 (measured per call: C1 (8 KiB) 1
+    // chunk 134 us vs 8: 280 us; C2 (4 MiB) 2: 254 vs 8: 314 us; C5 (16 MiB)
+    // 8: 716 us vs 1: 858 us; C3 (256 MiB) 8: 6.6 ms vs 4: 7.1, 16: 6.7).
     const char* pc = getenv("PTMH_PLUGIN_CHUNKS");  // A/B, tools/ only
-    const int64_t nch = std::min<int64_t>(R, pc ? std::max(1, std::min(64, atoi(pc))) : 8);  // <= 64 (events); 8: 6.6 ms per C3 call, 4: 7.0, 16: 6.7, 32: 8.3
-    uint32_t* d_sync;  // one persistent-sweep sync block per chunk
+    const int64_t nch = std::min<int64_t>(
+        R, pc ? std::max(1, std::min(64, atoi(pc))) : std::max<int64_t>(1, std::min<int64_t>(8, R * nsite >> 21)));
+    uint32_t* d_sync = nullptr;  // one persistent-sweep sync block per chunk
     const int64_t sync_words = ptmh_cb_sync_words(R);
     // Chunk compute: where the persistent path applies, every chunk runs on
     // ONE stream as one persistent launch (it fills the GPU by itself; two
@@ -663,60 +697,73 @@ int ptmh_host_cb_interval(int8_t* spins, int64_t R, int64_t L, int64_t* slot_to_
     // latter (A/B, tools/ only).
     const char* ps = getenv("PTMH_PLUGIN_SYNC");
     const bool plugin_sync = !(ps && ps[0] == '0') && cb_sweeps_persistent_applies(L, always, n_sweeps);
-    PTMH_TRY(ws_get(g_ws, 17, (size_t)(nch * sync_words), &d_sync));
-    PTMH_CUDA(cudaMemsetAsync(d_sync, 0, (size_t)(nch * sync_words) * 4, sc));
-    PTMH_CUDA(cudaMemcpyAsync(d_thr, thr.data(), R * 40, cudaMemcpyHostToDevice, sc));
-    PTMH_CUDA(cudaMemcpyAsync(d_s2r, slot_to_row, R * 8, cudaMemcpyHostToDevice, sc));
-    PTMH_CUDA(cudaMemcpyAsync(d_r2s, r2s.data(), R * 4, cudaMemcpyHostToDevice, sc));
-    PTMH_CUDA(cudaMemcpyAsync(d_b, betas, R * 8, cudaMemcpyHostToDevice, sc));
-    PTMH_CUDA(cudaMemsetAsync(d_cnt, 0, 16, sc));
-    // pipeline over replica chunks: all H2D copies are issued first, then the
-    // compute chain (each chunk waits for its copy), then the D2H copies (each
-    // waits for its chunk), so no queue ever blocks behind a later dependency
-    if (getenv("PTMH_TRACE")) PTMH_CUDA(cudaEventRecord(g_ws.ev_t0, sin));
+    if (plugin_sync) {
+        PTMH_TRY(ws_get(g_ws, 17, (size_t)(nch * sync_words), &d_sync));
+        PTMH_CUDA(cudaMemsetAsync(d_sync, 0, (size_t)(nch * sync_words) * 4, sc));
+    }
     auto chunk = [&](int64_t c, int64_t& lo, int64_t& n) {
         lo = R * c / nch;
         n = R * (c + 1) / nch - lo;
     };
-    for (int64_t c = 0; c < nch; ++c) {
-        int64_t lo, n;
-        chunk(c, lo, n);
-        PTMH_CUDA(cudaMemcpyAsync(d_spins + lo * nsite, spins + lo * nsite, (size_t)(n * nsite),
-                                  cudaMemcpyHostToDevice, sin));
-        PTMH_CUDA(cudaEventRecord(g_ws.ev_in[c], sin));
-    }
-    // the small tables above are on sc: every compute stream starts after them
-    PTMH_CUDA(cudaEventRecord(g_ws.ev_tab, sc));
-    for (int64_t c = 0; c < nch; ++c) {
-        int64_t lo, n;
-        chunk(c, lo, n);
-        cudaStream_t cst = plugin_sync ? g_ws.cs[0] : g_ws.cs[c % kComputeStreams];
-        PTMH_CUDA(cudaStreamWaitEvent(cst, g_ws.ev_tab, 0));
-        PTMH_CUDA(cudaStreamWaitEvent(cst, g_ws.ev_in[c], 0));
+    auto compute = [&](int64_t lo, int64_t n, uint32_t* sync, cudaStream_t cst) -> int {
         PTMH_TRY(launch_cb_pack(d_spins + lo * nsite, n, L, d_packed + lo * 2 * W, cst));
         PTMH_TRY(launch_cb_row_stats(d_packed + lo * 2 * W, n, L, d_stats + 2 * lo, cst));
         PTMH_TRY(launch_cb_sweeps(d_packed + lo * 2 * W, n, L, d_r2s + lo, d_thr, always, seed, first_sweep,
-                                  n_sweeps, d_stats + 2 * lo, cst, plugin_sync ? d_sync + c * sync_words : nullptr));
+                                  n_sweeps, d_stats + 2 * lo, cst, sync));
         PTMH_TRY(launch_cb_unpack(d_packed + lo * 2 * W, n, L, d_spins + lo * nsite, cst));
-        PTMH_CUDA(cudaEventRecord(g_ws.ev_out[c], cst));
-        PTMH_CUDA(cudaStreamWaitEvent(sc, g_ws.ev_out[c], 0));  // the exchange needs every chunk
-    }
-    for (int64_t c = 0; c < nch; ++c) {
-        int64_t lo, n;
-        chunk(c, lo, n);
-        PTMH_CUDA(cudaStreamWaitEvent(sout, g_ws.ev_out[c], 0));
-        PTMH_CUDA(cudaMemcpyAsync(spins + lo * nsite, d_spins + lo * nsite, (size_t)(n * nsite),
-                                  cudaMemcpyDeviceToHost, sout));
-    }
-    if (getenv("PTMH_TRACE")) {  // per-chunk timeline (tools/ only)
-        PTMH_CUDA(cudaStreamSynchronize(sout));
-        PTMH_CUDA(cudaStreamSynchronize(sc));
-        float t_in = 0, t_out = 0;
+        return PTMH_OK;
+    };
+    if (nch == 1 && !getenv("PTMH_TRACE")) {  // small call: everything in order on one stream
+        PTMH_CUDA(cudaMemcpyAsync(d_small, h_small, n_small, cudaMemcpyHostToDevice, sc));
+        PTMH_CUDA(cudaMemcpyAsync(d_spins, spins, (size_t)(R * nsite), cudaMemcpyHostToDevice, sc));
+        PTMH_TRY(compute(0, R, d_sync, sc));
+        PTMH_CUDA(cudaMemcpyAsync(spins, d_spins, (size_t)(R * nsite), cudaMemcpyDeviceToHost, sc));
+    } else {
+        // pipeline over replica chunks: all H2D copies are issued first, then
+        // the compute chain (each chunk waits for its copy), then the D2H
+        // copies (each waits for its chunk), so no queue ever blocks behind a
+        // later dependency
+        // (the small block goes first on the lattice copy queue: the compute
+        // streams see it through ev_in, sc through ev_out.  Issued on sc
+        // beside the chunk copies instead, a C3 call took 9.3 ms, not 6.6.)
+        if (getenv("PTMH_TRACE")) PTMH_CUDA(cudaEventRecord(g_ws.ev_t0, sin));
+        PTMH_CUDA(cudaMemcpyAsync(d_small, h_small, n_small, cudaMemcpyHostToDevice, sin));
         for (int64_t c = 0; c < nch; ++c) {
-            PTMH_CUDA(cudaEventElapsedTime(&t_in, g_ws.ev_t0, g_ws.ev_in[c]));
-            PTMH_CUDA(cudaEventElapsedTime(&t_out, g_ws.ev_t0, g_ws.ev_out[c]));
-            fprintf(stderr, "ptmh trace chunk %ld: h2d done %.3f ms, compute done %.3f ms\n", (long)c, t_in,
-                    t_out);
+            int64_t lo, n;
+            chunk(c, lo, n);
+            PTMH_CUDA(cudaMemcpyAsync(d_spins + lo * nsite, spins + lo * nsite, (size_t)(n * nsite),
+                                      cudaMemcpyHostToDevice, sin));
+            PTMH_CUDA(cudaEventRecord(g_ws.ev_in[c], sin));
+        }
+        // the sync-block reset is on sc: every compute stream starts after it
+        PTMH_CUDA(cudaEventRecord(g_ws.ev_tab, sc));
+        for (int64_t c = 0; c < nch; ++c) {
+            int64_t lo, n;
+            chunk(c, lo, n);
+            cudaStream_t cst = plugin_sync ? g_ws.cs[0] : g_ws.cs[c % kComputeStreams];
+            PTMH_CUDA(cudaStreamWaitEvent(cst, g_ws.ev_tab, 0));
+            PTMH_CUDA(cudaStreamWaitEvent(cst, g_ws.ev_in[c], 0));
+            PTMH_TRY(compute(lo, n, plugin_sync ? d_sync + c * sync_words : nullptr, cst));
+            PTMH_CUDA(cudaEventRecord(g_ws.ev_out[c], cst));
+            PTMH_CUDA(cudaStreamWaitEvent(sc, g_ws.ev_out[c], 0));  // the exchange needs every chunk
+        }
+        for (int64_t c = 0; c < nch; ++c) {
+            int64_t lo, n;
+            chunk(c, lo, n);
+            PTMH_CUDA(cudaStreamWaitEvent(sout, g_ws.ev_out[c], 0));
+            PTMH_CUDA(cudaMemcpyAsync(spins + lo * nsite, d_spins + lo * nsite, (size_t)(n * nsite),
+                                      cudaMemcpyDeviceToHost, sout));
+        }
+        if (getenv("PTMH_TRACE")) {  // per-chunk timeline (tools/ only)
+            PTMH_CUDA(cudaStreamSynchronize(sout));
+            PTMH_CUDA(cudaStreamSynchronize(sc));
+            float t_in = 0, t_out = 0;
+            for (int64_t c = 0; c < nch; ++c) {
+                PTMH_CUDA(cudaEventElapsedTime(&t_in, g_ws.ev_t0, g_ws.ev_in[c]));
+                PTMH_CUDA(cudaEventElapsedTime(&t_out, g_ws.ev_t0, g_ws.ev_out[c]));
+                fprintf(stderr, "ptmh trace chunk %ld: h2d done %.3f ms, compute done %.3f ms\n", (long)c, t_in,
+                        t_out);
+            }
         }
     }
     if (round_index >= 0) {  // energies by slot + the round, one launch
@@ -726,13 +773,14 @@ int ptmh_host_cb_interval(int8_t* spins, int64_t R, int64_t L, int64_t* slot_to_
     } else {
         PTMH_TRY(launch_cb_slot_energies(d_stats, d_s2r, R, J, B, d_e, d_sums, sc));
     }
-    int64_t cnt[2];
-    PTMH_CUDA(cudaMemcpyAsync(slot_to_row, d_s2r, R * 8, cudaMemcpyDeviceToHost, sc));
-    PTMH_CUDA(cudaMemcpyAsync(energies, d_e, R * 8, cudaMemcpyDeviceToHost, sc));
-    PTMH_CUDA(cudaMemcpyAsync(spin_sums, d_sums, R * 8, cudaMemcpyDeviceToHost, sc));
-    PTMH_CUDA(cudaMemcpyAsync(cnt, d_cnt, 16, cudaMemcpyDeviceToHost, sc));
+    PTMH_CUDA(cudaMemcpyAsync(h_small, d_small, n_out, cudaMemcpyDeviceToHost, sc));
     PTMH_CUDA(cudaStreamSynchronize(sc));
     PTMH_CUDA(cudaStreamSynchronize(sout));
+    memcpy(slot_to_row, h_small, 8 * R);
+    memcpy(energies, h_small + o_e, 8 * R);
+    memcpy(spin_sums, h_small + o_sums, 8 * R);
+    int64_t cnt[2];
+    memcpy(cnt, h_small + o_cnt, 16);
     if (accepted) *accepted = cnt[0];
     return PTMH_OK;
 }

@@ -94,8 +94,12 @@ def test_run_matches_oracle(mods, L, R, sweeps, every, seed, J, B, rec_every):
     assert rec.swap_near_ties == 0
 
 
-def test_host_interval_plugin_matches_oracle(mods):
+@pytest.mark.parametrize("chunks", [None, "3"])
+def test_host_interval_plugin_matches_oracle(mods, monkeypatch, chunks):
+    """One stream (small call, the default here) and 3 pipelined chunks."""
     p, _, kernels, _ = mods
+    if chunks is not None:
+        monkeypatch.setenv("PTMH_PLUGIN_CHUNKS", chunks)
     L, R, seed = 64, 8, 21
     temps = p.build_ladder(R)
     betas = 1.0 / temps
