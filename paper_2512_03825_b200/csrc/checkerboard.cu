@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_half_sweep_ferro(
 // All 2n half-sweeps of ptmh_cb_sweeps in ONE launch, as a dataflow over
 // work items instead of 2n grid-wide launches.  An item is (phase, lattice,
 // slice): phase p = colour p & 1 of sweep first + p / 2, a slice = `group`
-// consecutive 256-thread blocks of the lattice's word-column strips.
+// consecutive kPT-thread blocks of the lattice's word-column strips.
 // Resident CTAs take items from a global ticket in phase-major order; an item
 // of phase p waits until every item of phases < p of ITS lattice is done (a
 // per-lattice done counter), because colour c reads only colour 1-c words of
@@ -836,7 +836,7 @@ void fill_class_plan(uint32_t always_mask, int* n_up, int* k, int* sf, int* cls,
 constexpr int kFastRows = PTMH_FERRO_ROWS;
 
 // one persistent launch for every half-sweep: the ferro kernel with whole
-// 256-thread blocks per lattice (L % 512 == 0)
+// 128- or 256-thread blocks per lattice (L % 512 == 0)
 static size_t persistent_smem(int krows, int kpt) { return (size_t)(krows <= 16 ? 3 : 2) * (kpt / 32) * krows * 32 * 4; }
 
 bool cb_sweeps_persistent_applies(int64_t L, uint32_t always_mask, int64_t n_sweeps) {

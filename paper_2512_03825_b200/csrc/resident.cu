@@ -478,14 +478,16 @@ static int launch_resident_t(const ResidentArgs& a, int sms, cudaStream_t s) {
         &per_sm, cb_resident_kernel<kMode, kFerro, kThreads, false>, kThreads, 0));
     const int slots = a.max_ctas > 0 ? std::min(a.max_ctas, sms * std::max(1, per_sm)) : sms * std::max(1, per_sm);
     // Fewer lattices than CTA slots and enough words per lattice: a cluster
-    // of cs CTAs owns each lattice (C2: 64 lattices of 2048 words per colour
-    // on 128 SMs instead of 64).  PTMH_RESIDENT_CLUSTER=1 turns it off.
+    // of cs CTAs owns each lattice (C2: 64 lattices of 1024 words per colour
+    // on 4-CTA clusters of 256 threads, two CTAs per SM).  Measured at C2 with
+    // a round every sweep: 1 CTA per lattice 8.80 us/sweep, clusters of 2
+    // 7.20, 4 6.93, 8 7.01.  PTMH_RESIDENT_CLUSTER=1 turns it off.
     int cs = 1;
     const char* ec = getenv("PTMH_RESIDENT_CLUSTER");  // "1": off; "2", "4", "8": that size
     if (ec && atoi(ec) > 1) {
         cs = atoi(ec);
     } else if (!(ec && ec[0] == '1') && kThreads == 1024) {
-        while (cs < 8 && (int64_t)a.R * cs * 2 <= slots && a.W / (cs * 2) >= 512) cs *= 2;
+        while (cs < 8 && (int64_t)a.R * cs * 2 <= 2 * slots && a.W / (cs * 2) >= 256) cs *= 2;
     }
     // enough blocks to fill the GPU, few enough that no block owns more
     // lattices than its shared-memory tables hold

@@ -184,8 +184,8 @@ def test_one_lattice_matches_oracle_at_1024(mods):
     (64, 700, 6, 1, 17, 1.0, 0.0, 2),   # several lattices per CTA
     (16, 2000, 5, 1, 18, 1.0, 0.0, 1),  # many lattices per CTA, segment gather
     (128, 5, 12, 5, 4, 1.0, 0.1, 2),    # field: class plan
-    (256, 3, 6, 2, 9, -1.0, 0.0, 1),    # antiferromagnet (cluster of 2 CTAs per lattice)
-    (256, 5, 12, 1, 19, 1.0, 0.0, 2),   # ferro, cluster of 2 CTAs per lattice
+    (256, 3, 6, 2, 9, -1.0, 0.0, 1),    # antiferromagnet (cluster of 4 CTAs per lattice)
+    (256, 5, 12, 1, 19, 1.0, 0.0, 2),   # ferro, cluster of 4 CTAs per lattice (the C2 choice)
     (512, 3, 6, 1, 20, 1.0, 0.0, 1),    # cluster of 8 CTAs per lattice
     (2, 7, 50, 3, 5, 1.0, 0.0, 1),
     (6, 4, 25, 0, 6, 0.5, -0.5, 5),     # no exchanges
@@ -207,6 +207,23 @@ def test_resident_run_matches_oracle(mods, L, R, sweeps, every, seed, J, B, rec_
         (ref.swap_rounds, ref.swaps_attempted, ref.swaps_accepted)
     if ref.round_entry_iterations is not None:
         assert np.array_equal(rec.round_entry_iterations[:, 0], ref.round_entry_iterations * L * L)
+
+
+@pytest.mark.parametrize("cluster", ["1", "2", "8"])
+def test_resident_cluster_sizes(mods, monkeypatch, cluster):
+    """C2's lattice size (256^2) on other cluster sizes than the automatic 4."""
+    monkeypatch.setenv("PTMH_RESIDENT_CLUSTER", cluster)
+    p = mods[0]
+    L, R, sweeps, every, seed = 256, 5, 8, 1, 23
+    cfg = p.SimulationConfig(side=L, replicas=R, iterations=sweeps * L * L, swap_interval=every * L * L,
+                             seed=seed, sweep_mode="checkerboard", record_every=2, return_final_state=True,
+                             kernel="resident")
+    rec = p.run(cfg)
+    assert rec.valid, rec.error
+    ref = oracle.run_checkerboard(L, R, sweeps, every, seed, record_every=2)
+    assert np.array_equal(rec.final_spins, ref.final_spins)
+    assert np.array_equal(rec.energies, ref.energies)
+    assert rec.swaps_accepted == ref.swaps_accepted
 
 
 def test_resident_segments_compose(mods):
