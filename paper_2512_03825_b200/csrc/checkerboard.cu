@@ -233,9 +233,10 @@ __device__ __forceinline__ void ferro_strip(uint32_t* __restrict__ packed, int L
                                             bool active, int64_t lat, int rem,
                                             uint32_t (&tie_m)[kRows][32], uint32_t (&tie_k4)[kRows][32],
                                             uint32_t (&tie_sn)[kRows][32],
-                                            int& sumS, int& sumB) {
+                                            int& sumS, int& sumB, int wr_shift = -1,
+                                            const uint32_t* __restrict__ planes = nullptr) {
     const int lane = threadIdx.x & 31;
-    const int strip = rem / WR;
+    const int strip = wr_shift >= 0 ? rem >> wr_shift : rem / WR;
     const int k = rem - strip * WR;
     const int i0 = strip * kRows;
     const uint32_t own_base = (uint32_t)((lat * 2 + kColor) * W);
@@ -249,20 +250,33 @@ __device__ __forceinline__ void ferro_strip(uint32_t* __restrict__ packed, int L
         }
         const uint32_t* __restrict__ other = packed + (lat * 2 + (1 - kColor)) * W;
         uint32_t* __restrict__ own = packed + own_base;
-        slot = row_to_slot[lat];
-        t3 = __ldg(thresh + slot * 10 + 8);
-        t4 = __ldg(thresh + slot * 10 + 9);
         // Threshold plane p of a site is bit p of t4 where K4 is set, else of
         // t3: Tm = K4 ? TB : TA with TA, TB in {0, ~0}.  Written as the
         // integer K4 * (TB - TA) - TA (TM[p] in {-1, 0, 1}, TC[p] = -TA) so
         // the select is one IMAD on the FMA pipe; the ALU pipe, which bounds
-        // this kernel, only does the compare itself.
+        // this kernel, only does the compare itself.  The persistent kernel
+        // hands them over precomputed for the item's lattice (planes: TM[8],
+        // TC[8], t3, t4, slot in shared memory).
         uint32_t TM[8], TC[8];
+        if (planes) {
 #pragma unroll
-        for (int p = 0; p < 8; ++p) {
-            const uint32_t ta = (t3 >> (31 - p)) & 1u, tb = (t4 >> (31 - p)) & 1u;
-            TM[p] = tb - ta;
-            TC[p] = 0u - ta;
+            for (int p = 0; p < 8; ++p) {
+                TM[p] = planes[p];
+                TC[p] = planes[8 + p];
+            }
+            t3 = planes[16];
+            t4 = planes[17];
+            slot = (int)planes[18];
+        } else {
+            slot = row_to_slot[lat];
+            t3 = __ldg(thresh + slot * 10 + 8);
+            t4 = __ldg(thresh + slot * 10 + 9);
+#pragma unroll
+            for (int p = 0; p < 8; ++p) {
+                const uint32_t ta = (t3 >> (31 - p)) & 1u, tb = (t4 >> (31 - p)) & 1u;
+                TM[p] = tb - ta;
+                TC[p] = 0u - ta;
+            }
         }
         const int kl = (k == 0) ? WR - 1 : k - 1;
         const int kr = (k == WR - 1) ? 0 : k + 1;
@@ -399,7 +413,8 @@ __global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_half_sweep_ferro(
     const int rem = (int)(tid - lat * per_lat);
     int sumS = 0, sumB = 0;
     ferro_strip<kRows, kColor, kStats, true>(packed, L, WR, W, row_to_slot, thresh, rk, ctr1, stats, esz, active,
-                                             lat, rem, tie_m[warp], tie_k4[warp], tie_sn[warp], sumS, sumB);
+                                             lat, rem, tie_m[warp], tie_k4[warp], tie_sn[warp], sumS, sumB,
+                                             (WR & (WR - 1)) == 0 ? __ffs(WR) - 1 : -1);
     if (kColor == 1 && kStats) flush_stats(stats, lat, active, sumS, sumB);
 }
 
@@ -457,7 +472,9 @@ __global__ void __launch_bounds__(kPT, PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_pe
     uint32_t(*tie_k4)[kRows][32] = tie_m + kWarps;
     uint32_t(*tie_sn)[kRows][32] = kRows <= 16 ? tie_m + 2 * kWarps : tie_m;  // (unused at 32 rows)
     __shared__ uint32_t s_item[2];
+    __shared__ uint32_t s_planes[2][20];  // the item's lattice: TM[8], TC[8], t3, t4, slot
     const int warp = threadIdx.x >> 5;
+    const int wr_shift = (WR & (WR - 1)) == 0 ? __ffs(WR) - 1 : -1;
     // items per lattice and phase (the host picks group so that a phase still
     // has >= 8 items per resident CTA)
     const uint32_t subs = (uint32_t)((L / kRows) * WR / kPT) / group;
@@ -472,6 +489,20 @@ __global__ void __launch_bounds__(kPT, PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_pe
             if (next < n_items) {
                 const uint32_t phase = next / per_phase;
                 const uint32_t lat = (next - phase * per_phase) / subs;
+                // the lattice's threshold planes, once per item instead of per
+                // thread (the loads overlap the dependency poll)
+                const int slot = row_to_slot[lat];
+                const uint32_t t3 = __ldg(thresh + slot * 10 + 8), t4 = __ldg(thresh + slot * 10 + 9);
+                uint32_t* pl = s_planes[it & 1];
+#pragma unroll
+                for (int p = 0; p < 8; ++p) {
+                    const uint32_t ta = (t3 >> (31 - p)) & 1u, tb = (t4 >> (31 - p)) & 1u;
+                    pl[p] = tb - ta;
+                    pl[8 + p] = 0u - ta;
+                }
+                pl[16] = t3;
+                pl[17] = t4;
+                pl[18] = (uint32_t)slot;
                 if (phase > 0)
                     while (ld_acquire_gpu(&sync[2 + lat]) < phase * subs) __nanosleep(32);
             }
@@ -494,7 +525,7 @@ __global__ void __launch_bounds__(kPT, PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_pe
     for (uint32_t g = 0; g < group; ++g)                                                                  \
         ferro_strip<kRows, C, ST, true>(packed, L, WR, W, row_to_slot, thresh, rk, ctr1, stats, esz, true, \
                                         lat, (int)((sub * group + g) * kPT + threadIdx.x), tie_m[warp],   \
-                                        tie_k4[warp], tie_sn[warp], sumS, sumB)
+                                        tie_k4[warp], tie_sn[warp], sumS, sumB, wr_shift, s_planes[it & 1])
         if ((ctr1 & 1u) == 0) {
             if (last_sweep)
                 PTMH_STRIP(0, true);
