@@ -360,7 +360,7 @@ def main():
         launch_ms = statistics.mean(sweep_ms)
         bytes_per_launch = ALG_BYTES_PER_ATTEMPT * local_rows * L * L * every
         # rows per thread as the launcher picks them (csrc/checkerboard.cu)
-        kpt = 128 if local_rows * L * L >= (1 << 27) else 256  # threads per item
+        kpt = 128 if (128 % (L // 64) == 0 or local_rows * L * L >= (1 << 27)) else 256  # threads per item
         slots = (3 * 256 // kpt) * torch.cuda.get_device_properties(dev).multi_processor_count
         items = lambda k: local_rows * (L * L // (kpt * 64 * k))  # noqa: E731
         krows = 32 if items(32) >= 8 * slots else next((k for k in (16, 8, 4) if items(k) >= slots), 2)

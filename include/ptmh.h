@@ -203,13 +203,13 @@ int ptmh_cb_sweeps(uint32_t *packed, int64_t rows, int64_t L,
                    int64_t n_sweeps, int64_t *stats, void *stream);
 
 /* ptmh_cb_sweeps with a caller-owned sync block (uint32, ptmh_cb_sync_words
- * (rows) words, zeroed once; every call leaves it zeroed).  With it, the
+ * (rows, L) words, zeroed once; every call leaves it zeroed).  With it, the
  * J > 0, B = 0, L % 512 == 0, L >= 1024 case runs all 2 * n_sweeps half-sweeps in ONE
- * persistent launch (a per-lattice dataflow over work items, no grid-wide
- * barrier between colours); other cases, or sync == NULL, take the per-launch
- * path.  Results are bit-identical either way.  Calls sharing a sync block
- * must be ordered on one stream. */
-int64_t ptmh_cb_sync_words(int64_t rows);
+ * persistent launch (a dataflow over work items with per-band dependencies,
+ * no grid-wide barrier between colours); other cases, or sync == NULL, take
+ * the per-launch path.  Results are bit-identical either way.  Calls sharing
+ * a sync block must be ordered on one stream. */
+int64_t ptmh_cb_sync_words(int64_t rows, int64_t L);
 int ptmh_cb_sweeps_sync(uint32_t *packed, int64_t rows, int64_t L,
                         const int32_t *row_to_slot, const uint32_t *thresh,
                         uint32_t always_mask, uint64_t seed,

@@ -61,7 +61,7 @@ def _load():
         "ptmh_cb_pack": ([P, i64, i64, P, P], i32),
         "ptmh_cb_unpack": ([P, i64, i64, P, P], i32),
         "ptmh_cb_sweeps": ([P, i64, i64, P, P, u32, u64, i64, i64, P, P], i32),
-        "ptmh_cb_sync_words": ([i64], i64),
+        "ptmh_cb_sync_words": ([i64, i64], i64),
         "ptmh_cb_sweeps_sync": ([P, i64, i64, P, P, u32, u64, i64, i64, P, P, P], i32),
         "ptmh_cb_row_stats": ([P, i64, i64, P, P], i32),
         "ptmh_cb_unpack_slots": ([P, P, i64, i64, P, P], i32),

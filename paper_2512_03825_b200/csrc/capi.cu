@@ -305,7 +305,14 @@ int ptmh_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* row
                             stats, as_stream(stream));
 }
 
-int64_t ptmh_cb_sync_words(int64_t rows) { return 2 + std::max<int64_t>(rows, 0); }
+int64_t ptmh_cb_sync_words(int64_t rows, int64_t L) {
+    // ticket, CTAs out, a counter per lattice, and the persistent kernel's
+    // band counters: at most L^2 / 16384 bands per lattice (128-thread items
+    // of 2-row strips)
+    rows = std::max<int64_t>(rows, 0);
+    const int64_t bands = (L >= 1024 && L % 512 == 0) ? L * L / 16384 : 0;
+    return 2 + rows + rows * bands;
+}
 
 int ptmh_cb_sweeps_sync(uint32_t* packed, int64_t rows, int64_t L, const int32_t* row_to_slot,
                         const uint32_t* thresh, uint32_t always_mask, uint64_t seed, int64_t first_sweep,
@@ -688,7 +695,7 @@ int ptmh_host_cb_interval(int8_t* spins, int64_t R, int64_t L, int64_t* slot_to_
     const int64_t nch = std::min<int64_t>(
         R, pc ? std::max(1, std::min(64, atoi(pc))) : std::max<int64_t>(1, std::min<int64_t>(8, R * nsite >> 21)));
     uint32_t* d_sync = nullptr;  // one persistent-sweep sync block per chunk
-    const int64_t sync_words = ptmh_cb_sync_words(R);
+    const int64_t sync_words = ptmh_cb_sync_words(R, L);
     // Chunk compute: where the persistent path applies, every chunk runs on
     // ONE stream as one persistent launch (it fills the GPU by itself; two
     // of them side by side cost 2x, 16.9 vs 7.2 ms per C3 call); otherwise

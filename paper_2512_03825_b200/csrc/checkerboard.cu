@@ -421,26 +421,28 @@ __global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_half_sweep_ferro(
 // ---------------------------------------- persistent multi-sweep ferro path --
 // All 2n half-sweeps of ptmh_cb_sweeps in ONE launch, as a dataflow over
 // work items instead of 2n grid-wide launches.  An item is (phase, lattice,
-// slice): phase p = colour p & 1 of sweep first + p / 2, a slice = `group`
+// band): phase p = colour p & 1 of sweep first + p / 2, a band = `group`
 // consecutive kPT-thread blocks of the lattice's word-column strips.
 // Resident CTAs take items from a global ticket in phase-major order; an item
-// of phase p waits until every item of phases < p of ITS lattice is done (a
-// per-lattice done counter), because colour c reads only colour 1-c words of
-// its own lattice.  So the tail of one phase overlaps the head of the next,
-// there are no launch gaps, and no CTA ever waits on a ticket that has not
-// been taken by a running CTA (tickets are taken in order), which makes the
-// scheme deadlock-free at any residency.  Random numbers, acceptance and
-// statistics are those of the per-launch kernel: the paths are bit-identical.
-// (Per-warp items were tried: 25 % slower at C3.)
+// of phase p waits for the items it depends on (the neighbouring bands'
+// phase p - 1, or, where items do not span whole rows, all of its lattice's
+// earlier phases: see `bands` below).  So phases overlap, there are no
+// launch gaps, and no CTA ever waits on a ticket that has not been taken by
+// a running CTA (tickets are taken in order and dependencies have smaller
+// tickets), which makes the scheme deadlock-free at any residency.  Random
+// numbers, acceptance and statistics are those of the per-launch kernel: the
+// paths are bit-identical.  (Per-warp items were tried: 25 % slower at C3.)
 //
-// sync (uint32, zeroed, 2 + rows words): [0] ticket, [1] CTAs finished,
-// [2 + lat] items of lattice lat done.  The last CTA out re-zeroes it.
+// sync (uint32, zeroed, ptmh_cb_sync_words(rows, L) words): [0] ticket,
+// [1] CTAs finished, [2 + lat] items of lattice lat done (lattice mode),
+// [2 + rows + lat * subs + band] phases done by that band (band mode).  The
+// last CTA out re-zeroes it.
 //
 // Coherence: own-colour words are read and written at L2 (.cg).  The other
-// colour is read through L1 (ld.global.nc), which is safe because (a) all
-// running items of a lattice are in the same phase, so the words they read
-// are not written while they run, and (b) every item of phase > 0 starts
-// with an ld.acquire.gpu of its dependency counter, which ptxas emits with
+// colour is read through L1 (ld.global.nc), which is safe because (a) the
+// words an item reads are not written while it runs (their next writers
+// depend on it), and (b) every item of phase > 0 starts with an
+// ld.acquire.gpu of its dependency counters, which ptxas emits with
 // CCTL.IVALL: the SM's L1 is invalidated after the words were last written
 // and before they are read.  Phase-0 items read words no item of this launch
 // has written yet.
@@ -455,9 +457,8 @@ __device__ __forceinline__ void red_release_gpu_add(uint32_t* p, uint32_t v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// kPT threads per CTA = per item: 128 for big shards (more, smaller CTAs:
-// C3 +1.5 %, 2^27-site shards +3 %), 256 for small ones (a rank's C3 shard at
-// 8 GPUs: 128 would cost 12 %)
+// kPT threads per CTA = per item: 128 where items cover whole lattice rows
+// (band dependencies, below) or the shard is big, else 256 (the launcher)
 template <int kRows, int kPT>
 __global__ void __launch_bounds__(kPT, PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_persistent(
     uint32_t* __restrict__ packed, int64_t rows, int L, int WR, int64_t W,
@@ -480,9 +481,21 @@ __global__ void __launch_bounds__(kPT, PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_pe
     const uint32_t subs = (uint32_t)((L / kRows) * WR / kPT) / group;
     const uint32_t per_phase = (uint32_t)rows * subs;
     const uint32_t n_items = n_phases * per_phase;
+    // Band dependencies: an item covers a band of whole strip rows when its
+    // blocks span whole lattice rows (kPT % WR == 0).  Its phase-p half-sweep
+    // then reads only its band and the adjacent rows of the two neighbouring
+    // bands, and overwrites only words those bands read in phase p - 1: it
+    // waits for bands sub-1, sub, sub+1 (mod subs) to finish phase p - 1
+    // (band[lat][b] = phases done), not for the whole lattice, so phases of
+    // one lattice pipeline like a wavefront.  The last sweep's colour-1 phase
+    // adds to the (S, Bond) that band 0's colour-0 item reset: it also waits
+    // for band 0.  Otherwise (lattice rows wider than an item) the lattice
+    // counter sync[2 + lat] orders whole phases.
+    const bool bands = (kPT % WR) == 0;
+    uint32_t* const band = sync + 2 + rows;
     // thread 0 schedules: it holds the next ticket (prefetched one item
     // ahead, so the atomic's latency is off the critical path), waits for the
-    // item's lattice to finish the previous phase, and publishes it
+    // item's dependencies, and publishes it
     uint32_t next = threadIdx.x == 0 ? atomicAdd(&sync[0], 1u) : 0u;
     for (int it = 0;; ++it) {
         if (threadIdx.x == 0) {
@@ -503,8 +516,19 @@ __global__ void __launch_bounds__(kPT, PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_pe
                 pl[16] = t3;
                 pl[17] = t4;
                 pl[18] = (uint32_t)slot;
-                if (phase > 0)
-                    while (ld_acquire_gpu(&sync[2 + lat]) < phase * subs) __nanosleep(32);
+                if (phase > 0) {
+                    if (bands) {
+                        const uint32_t sub = next - phase * per_phase - lat * subs;
+                        const uint32_t* b = band + (size_t)lat * subs;
+                        const uint32_t sm = sub == 0 ? subs - 1 : sub - 1, sp = sub + 1 == subs ? 0 : sub + 1;
+                        const bool stats_phase = phase + 1 == n_phases;
+                        while (ld_acquire_gpu(b + sm) < phase || ld_acquire_gpu(b + sub) < phase ||
+                               ld_acquire_gpu(b + sp) < phase || (stats_phase && ld_acquire_gpu(b) < phase))
+                            __nanosleep(32);
+                    } else {
+                        while (ld_acquire_gpu(&sync[2 + lat]) < phase * subs) __nanosleep(32);
+                    }
+                }
             }
             s_item[it & 1] = next;  // double-buffered: the next write is past a barrier
             if (next < n_items) next = atomicAdd(&sync[0], 1u);
@@ -539,12 +563,22 @@ __global__ void __launch_bounds__(kPT, PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_pe
         }
 #undef PTMH_STRIP
         __syncthreads();  // every store of this item is issued before the release
-        if (threadIdx.x == 0) red_release_gpu_add(&sync[2 + lat], 1u);
+        if (threadIdx.x == 0) red_release_gpu_add(bands ? band + (size_t)lat * subs + sub : &sync[2 + lat], 1u);
     }
+    // last CTA out leaves the sync block zeroed (all of its threads clear the
+    // counters: rows * subs band words)
+    __shared__ bool s_last;
     if (threadIdx.x == 0) {
         __threadfence();
-        if (atomicAdd(&sync[1], 1u) == gridDim.x - 1) {  // last CTA out: leave sync zeroed
-            for (int64_t l = 0; l < rows; ++l) sync[2 + l] = 0;
+        s_last = atomicAdd(&sync[1], 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        const int64_t n_cnt = rows + (bands ? rows * (int64_t)subs : 0);
+        for (int64_t l = threadIdx.x; l < n_cnt; l += kPT) sync[2 + l] = 0;
+        __syncthreads();
+        if (threadIdx.x == 0) {
             sync[0] = 0;
             __threadfence();
             sync[1] = 0;
@@ -893,7 +927,11 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
         PTMH_CUDA(cudaGetDevice(&dev));
         if (dev >= 256) dev = 255;
         const char* et = getenv("PTMH_PERSIST_THREADS");  // 128 / 256 pins it (A/B and tests)
-        const bool t128 = et ? atoi(et) == 128 : rows * L * L >= (1LL << 27);
+        // 128-thread items wherever they give band dependencies (an item's
+        // blocks span whole lattice rows: L / 64 divides 128), else only for
+        // big shards (more, smaller CTAs pay there; with lattice-wide phases
+        // they cost small shards 12 %)
+        const bool t128 = et ? atoi(et) == 128 : (128 % (L / 64) == 0 || rows * L * L >= (1LL << 27));
         const int kpt = t128 ? 128 : 256;
         if (cached_slots[dev][t128] == 0) {
             int sms = 0, occ = 0;
@@ -924,11 +962,11 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
         // the phase has too few items to fill the GPU and that path binds:
         // take the largest kRows whose phase still has >= 1 item per CTA
         // slot (else 2).  Measured on one B200 (attempts/s at L = 1024,
-        // 256-thread items): R = 256: 16 rows 3.23e12 (8: 2.93e12); R = 64: 8
-        // rows 2.55e12 (16: 2.01e12, 4: 2.38e12); R = 32: 4 rows 2.00e12 (16:
-        // 1.18e12, 2: 1.77e12); R = 16: 2 rows 1.32e12 (4: 1.16e12).  128-thread
-        // items at >= 2^27 sites: R = 128 3.09e12 -> 3.18e12, C3 3.40e12 ->
-        // 3.45e12; at R = 64 2.74e12 -> 2.63e12, R = 32 2.12e12 -> 1.86e12.
+        // 128-thread items, band dependencies): R = 256: 16 rows 3.43e12 (8:
+        // 3.10e12, 32: 2.86e12); R = 128: 16 rows 3.25e12 (8: 3.12e12); R = 64:
+        // 8 rows 2.93e12 (16: 2.38e12, 4: 2.53e12); R = 32: 4 rows 2.37e12 (8:
+        // 1.99e12, 2: 1.84e12); R = 16: 2 rows 1.76e12 (4: 1.50e12).  256-thread
+        // items: 2-5 % lower at every one of these.
         // (PTMH_PERSIST_ROWS pins it: A/B and tests.)
         const char* er = getenv("PTMH_PERSIST_ROWS");
         auto items_at = [&](int k) { return rows * (L * L / ((int64_t)kpt * 64 * k)); };

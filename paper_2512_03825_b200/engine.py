@@ -219,7 +219,7 @@ class CheckerboardEngine(_Base):
         self.spin_sums = torch.zeros(R, dtype=torch.int64, device=d)
         # zeroed sync block of the persistent sweep path (left zeroed by every call)
         self.persistent = True
-        self._sync = torch.zeros(int(_lib.LIB.ptmh_cb_sync_words(self.rows)), dtype=torch.int32, device=d)
+        self._sync = torch.zeros(int(_lib.LIB.ptmh_cb_sync_words(self.rows, self.L)), dtype=torch.int32, device=d)
 
     @property
     def local_stats(self) -> torch.Tensor:
