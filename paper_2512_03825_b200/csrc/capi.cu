@@ -86,6 +86,7 @@ struct Workspace {
     bool events = false;
     void* pin = nullptr;  // pinned staging of the small per-call arrays (one H2D, one D2H)
     size_t pin_n = 0;
+    bool dirty = false;  // a call returned before its final synchronize (error): drain first
 };
 
 // one workspace per device (buffers, streams and events are device-bound),
@@ -107,6 +108,13 @@ static int device_workspace(Workspace** out) {
 }
 
 static int ws_prepare(Workspace& w) {
+    if (w.dirty) {  // the previous call failed with work in flight: its copies may still use the buffers
+        for (auto& st : w.s)
+            if (st) cudaStreamSynchronize(st);
+        for (auto& st : w.cs)
+            if (st) cudaStreamSynchronize(st);
+    }
+    w.dirty = true;  // cleared by the call's final synchronize
     for (auto& st : w.s)
         if (!st) PTMH_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     for (auto& st : w.cs)
@@ -491,6 +499,7 @@ int ptmh_host_fill_lattice(int8_t* out, int64_t n, int64_t up_count, uint64_t se
     PTMH_TRY(launch_fill(d, 1, n, up_count, seed, stream, position, s));
     PTMH_CUDA(cudaMemcpyAsync(out, d, (size_t)n, cudaMemcpyDeviceToHost, s));
     PTMH_CUDA(cudaStreamSynchronize(s));
+    g_ws.dirty = false;
     if (new_position) *new_position = position + (uint64_t)(n - 1);  // kernels.py:45
     return PTMH_OK;
 }
@@ -512,6 +521,7 @@ int ptmh_host_lattice_energy(const int8_t* spins, int64_t L, double J, double B,
     PTMH_TRY(launch_row_stats(d, 1, L, st, s));
     PTMH_CUDA(cudaMemcpyAsync(h, st, sizeof(h), cudaMemcpyDeviceToHost, s));
     PTMH_CUDA(cudaStreamSynchronize(s));
+    g_ws.dirty = false;
     *energy = B * (double)h[0] - J * (double)h[1];  // kernels.py:59
     return PTMH_OK;
 }
@@ -597,6 +607,7 @@ int ptmh_host_advance_block(int8_t* spins, int64_t rows, int64_t L, const int64_
                                     hi - lo, cudaMemcpyDeviceToHost, s));
     }
     PTMH_CUDA(cudaStreamSynchronize(s));
+    g_ws.dirty = false;
     return PTMH_OK;
 }
 
@@ -632,6 +643,7 @@ int ptmh_host_swap_chunk(int64_t* slot_to_row, double* energies, int64_t* spin_s
     PTMH_CUDA(cudaMemcpyAsync(spin_sums, d_sums, R * 8, cudaMemcpyDeviceToHost, s));
     PTMH_CUDA(cudaMemcpyAsync(cnt, d_cnt, 16, cudaMemcpyDeviceToHost, s));
     PTMH_CUDA(cudaStreamSynchronize(s));
+    g_ws.dirty = false;
     if (accepted) *accepted = cnt[0];
     return PTMH_OK;
 }
@@ -783,6 +795,7 @@ int ptmh_host_cb_interval(int8_t* spins, int64_t R, int64_t L, int64_t* slot_to_
     PTMH_CUDA(cudaMemcpyAsync(h_small, d_small, n_out, cudaMemcpyDeviceToHost, sc));
     PTMH_CUDA(cudaStreamSynchronize(sc));
     PTMH_CUDA(cudaStreamSynchronize(sout));
+    g_ws.dirty = false;
     memcpy(slot_to_row, h_small, 8 * R);
     memcpy(energies, h_small + o_e, 8 * R);
     memcpy(spin_sums, h_small + o_sums, 8 * R);
