@@ -464,7 +464,7 @@ __global__ void __launch_bounds__(kPT, PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_pe
     uint32_t* __restrict__ packed, int64_t rows, int L, int WR, int64_t W,
     const int32_t* __restrict__ row_to_slot, const uint32_t* __restrict__ thresh, const RoundKeys32 rk,
     uint32_t ctr_base, uint32_t n_phases, int64_t* __restrict__ stats, uint32_t esz,
-    uint32_t* __restrict__ sync, uint32_t group) {
+    uint32_t* __restrict__ sync, uint32_t group, bool bands) {
     constexpr int kWarps = kPT / 32;
     // tie scratch (3 x kRows x 32 words per warp: 48 KB at kRows = 16) in
     // dynamic shared memory; cb_sweeps_persistent_smem() bytes
@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(kPT, PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_pe
     // adds to the (S, Bond) that band 0's colour-0 item reset: it also waits
     // for band 0.  Otherwise (lattice rows wider than an item) the lattice
     // counter sync[2 + lat] orders whole phases.
-    const bool bands = (kPT % WR) == 0;
+    // (bands: kPT % WR == 0, checked by the launcher)
     uint32_t* const band = sync + 2 + rows;
     // thread 0 schedules: it holds the next ticket (prefetched one item
     // ahead, so the atomic's latency is off the critical path), waits for the
@@ -998,10 +998,15 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
         const int64_t items = 2 * n_sweeps * rows * (blocks / group);
         const unsigned grid = (unsigned)std::min<int64_t>(items, slots);
         const uint32_t c0 = (uint32_t)(2 * first_sweep), np = (uint32_t)(2 * n_sweeps);
+        // band dependencies pay where a phase has few items per CTA slot
+        // (1024^2 x 128: 3.21 -> 3.25e12); at C3 size and above lattice-wide
+        // phases measure the same or 0.3 % better (fewer polls per item)
+        const char* eb = getenv("PTMH_PERSIST_BANDS");  // "0" / "1" pins it (A/B and tests)
+        const bool bands = kpt % WR == 0 && (eb ? eb[0] == '1' : rows * L * L < (1LL << 28));
 #define PTMH_PERSIST(K, T)                                                                                    \
     cb_sweeps_persistent<K, T><<<grid, T, persistent_smem(K, T), s>>>(packed, rows, (int)L, WR, W, row_to_slot, \
                                                                       thresh, rk, c0, np, stats, 4u, sync,    \
-                                                                      (uint32_t)group)
+                                                                      (uint32_t)group, bands)
         if (t128) {
             if (krows == 32) PTMH_PERSIST(32, 128);
             else if (krows == 16) PTMH_PERSIST(16, 128);

@@ -307,7 +307,9 @@ def test_full_states_match_oracle(mods, L, R, sweeps, every, rec_every):
     (2048, 4, 1, 3, None, "32", "128"),  # ... on 128-thread items (the C4 launch)
     (1024, 8, 0, 2, "0", "32", None),    # 32 rows, grouped
 ])
-def test_persistent_sweeps_equal_per_launch_path(mods, monkeypatch, L, R, first, nsweeps, per_slot, rows, threads):
+@pytest.mark.parametrize("bands", [None, "0", "1"])
+def test_persistent_sweeps_equal_per_launch_path(mods, monkeypatch, L, R, first, nsweeps, per_slot, rows, threads,
+                                                 bands):
     """The one-launch dataflow path (cb_sweeps_persistent) and the per-launch
     half-sweep kernels give identical lattices and stats; the sync block is
     left zeroed for the next call."""
@@ -318,6 +320,8 @@ def test_persistent_sweeps_equal_per_launch_path(mods, monkeypatch, L, R, first,
         monkeypatch.setenv("PTMH_PERSIST_ROWS", rows)
     if threads is not None:
         monkeypatch.setenv("PTMH_PERSIST_THREADS", threads)
+    if bands is not None:  # band dependencies forced on (where items span rows) / off
+        monkeypatch.setenv("PTMH_PERSIST_BANDS", bands)
     temps = p.build_ladder(R)
     perm = np.random.default_rng(R).permutation(R)
     r2s = np.empty(R, dtype=np.int64); r2s[perm] = np.arange(R)
