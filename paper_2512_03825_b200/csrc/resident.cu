@@ -228,6 +228,12 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
     __shared__ double s_bd[kMaxLatPerBlock];       // beta_i - beta_j of the slot's pair (this round)
     __shared__ uint32_t s_pt[kMaxLatPerBlock][2];  // thresholds t3, t4 of the partner slot (ferro)
     __shared__ uint32_t s_mask[kFerro ? kMaxLatPerBlock : 1][18];  // TM[8], TC[8], t3, t4
+    // Next round's swap draws, for runs of <= 32 pairs: a warp the exchange
+    // decisions leave idle computes them while the decisions run, so the
+    // next publish does not wait on a Philox4x64 chain (C1: the draw was 12 %
+    // of a sweep + round).  s_pre_round: the round they belong to, or -1.
+    __shared__ double s_unext[32];
+    __shared__ long long s_pre_round;
     cg::cluster_group cluster = cg::this_cluster();
     const int cs = kCl ? (int)cluster.num_blocks() : 1;
     const int crank = kCl ? (int)cluster.block_rank() : 0;
@@ -254,6 +260,9 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
         s_S[i] = 0;
         s_B[i] = 0;
     }
+    if (threadIdx.x == 0) s_pre_round = -1;
+    const int pre_warp = (nl + 31) / 32;  // first warp without an exchange decision
+    const bool pre = R / 2 <= 32 && (int)blockDim.x >= 32 * (pre_warp + 1);
     if (kCl)
         cluster.sync();
     else
@@ -357,7 +366,8 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
                 const int other = (k == si) ? sj : si;
                 const uint32_t t3 = kFerro ? __ldg(A.thresh + other * 10 + 8) : 0u;
                 const uint32_t t4 = kFerro ? __ldg(A.thresh + other * 10 + 9) : 0u;
-                s_u[i] = stream_uniform(A.seed, (uint64_t)(R + pi), (uint64_t)round);
+                s_u[i] = s_pre_round == round ? s_unext[pi]
+                                               : stream_uniform(A.seed, (uint64_t)(R + pi), (uint64_t)round);
                 s_bd[i] = __dsub_rn(bi, bj);
                 s_pt[i][0] = t3;
                 s_pt[i][1] = t4;
@@ -420,6 +430,11 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
             cg::this_grid().sync();
         }
         // ---- exchange round: the owner of lattice r decides the pair of its slot
+        if (pre && ((int)threadIdx.x >> 5) == pre_warp) {  // (s_u of this round is read: the next is safe)
+            const int lane = threadIdx.x & 31, nf = (int)((round + 1) % 2), np = (R - nf) / 2;
+            if (lane < np) s_unext[lane] = stream_uniform(A.seed, (uint64_t)(R + lane), (uint64_t)(round + 1));
+            if (lane == 0) s_pre_round = round + 1;
+        }
         for (int li = threadIdx.x; li < nl; li += blockDim.x) {
             const int r = lo + li;
             const int k = s_slot[li];
