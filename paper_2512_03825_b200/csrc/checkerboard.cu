@@ -984,6 +984,10 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
             }
         }
         if (krows != 2 && krows != 4 && krows != 8 && krows != 16 && krows != 32) krows = 16;
+        // whole blocks per lattice and phase: L^2 / 64 words must split into
+        // kpt-thread blocks of krows-row strips (L = 1536 with 256-thread
+        // items allows at most 16 rows)
+        while (krows > 2 && (L * L / 64) % ((int64_t)krows * kpt) != 0) krows /= 2;
         // blocks of kpt threads per item: amortise the per-item scheduling
         // over several blocks while a phase keeps >= 8 items per resident CTA
         // (PTMH_PERSIST_ITEMS_PER_SLOT overrides the 8; tests use 0 to force

@@ -303,6 +303,7 @@ def test_full_states_match_oracle(mods, L, R, sweeps, every, rec_every):
     (1024, 16, 1, 4, None, None, None),  # auto: 2 rows per thread (a rank's C3 shard at 16 GPUs)
     (1536, 3, 2, 3, None, "16", None),   # 9 blocks per lattice and phase (odd), WR = 24
     (1536, 3, 2, 3, None, "16", "128"),  # 18 blocks per lattice and phase
+    (1536, 3, 2, 3, None, "32", "256"),  # 32 rows do not split 1536^2 into 256-thread blocks: 16 taken
     (2048, 4, 1, 3, None, "32", None),   # 32 rows per thread (the C4 choice), ties from L2
     (2048, 4, 1, 3, None, "32", "128"),  # ... on 128-thread items (the C4 launch)
     (1024, 8, 0, 2, "0", "32", None),    # 32 rows, grouped
