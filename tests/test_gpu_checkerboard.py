@@ -209,6 +209,34 @@ def test_resident_run_matches_oracle(mods, L, R, sweeps, every, seed, J, B, rec_
         assert np.array_equal(rec.round_entry_iterations[:, 0], ref.round_entry_iterations * L * L)
 
 
+@pytest.mark.parametrize("case", range(24))
+def test_resident_random_shapes_match_oracle(mods, case):
+    """Randomised shapes, couplings and schedules through the resident kernel
+    (every gather mode, clusters, warp-owned lattices) against the oracle."""
+    p = mods[0]
+    rng = np.random.default_rng(1000 + case)
+    L = int(rng.choice([2, 4, 6, 8, 10, 16, 24, 32, 48, 64, 96, 128, 256]))
+    R = int(rng.integers(1, 40 if L <= 64 else 6))
+    sweeps = int(rng.integers(1, 12 if L <= 64 else 5))
+    every = int(rng.integers(0, 4))
+    J = float(rng.choice([1.0, -1.0, 0.5]))
+    B = float(rng.choice([0.0, 0.0, 0.25, -0.5]))
+    rec_every = int(rng.integers(1, min(3, sweeps) + 1))
+    seed = int(rng.integers(1 << 40))
+    cfg = p.SimulationConfig(side=L, replicas=R, iterations=sweeps * L * L, swap_interval=every * L * L,
+                             seed=seed, params=p.IsingParams(J=J, B=B), sweep_mode="checkerboard",
+                             record_every=rec_every, return_final_state=True, kernel="resident")
+    rec = p.run(cfg)
+    assert rec.valid, rec.error
+    ref = oracle.run_checkerboard(L, R, sweeps, every, seed, J=J, B=B, record_every=rec_every)
+    assert np.array_equal(rec.final_spins, ref.final_spins)
+    assert np.array_equal(rec.slot_to_row, ref.slot_to_row)
+    assert np.array_equal(rec.energies, ref.energies)
+    assert np.array_equal(rec.magnetizations, ref.magnetizations)
+    assert (rec.swap_rounds, rec.swaps_attempted, rec.swaps_accepted) == \
+        (ref.swap_rounds, ref.swaps_attempted, ref.swaps_accepted)
+
+
 @pytest.mark.parametrize("cluster", ["1", "2", "8"])
 def test_resident_cluster_sizes(mods, monkeypatch, cluster):
     """C2's lattice size (256^2) on other cluster sizes than the automatic 4."""
