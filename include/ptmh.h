@@ -277,7 +277,10 @@ int ptmh_peer_free(void *dev_ptr);
  * of total_iters, WITH its swap rounds (every swap_every iterations,
  * executor.py:111-125): draws on the whole GPU, then one CTA per chunk
  * commits every slot (R <= 32, bit lattices in shared memory) and runs the
- * rounds in between (csrc/exact.cu, exact_resident_kernel).  slot_to_row,
+ * rounds in between (csrc/exact.cu, exact_resident_kernel).  A call runs
+ * the rounds at completed = start_iter .. start_iter+nsteps-1 (the one at its
+ * first iteration before any attempt; the one at its end belongs to the next
+ * call), so consecutive calls cover every round once.  slot_to_row,
  * energies, spin_sums are updated in place; counters += (accepted, near
  * ties).  Workspace: ptmh_advance_workspace_bytes(R, nsteps).  Bit-exact with
  * the reference's executor loop. */

@@ -1086,6 +1086,12 @@ __global__ void __launch_bounds__(kMaxThreads, 1) exact_resident_kernel(CommitAr
             ssum = s_ss[slot];
         }
     };
+    // A call covers the rounds at completed = start_iter .. start_iter +
+    // nsteps - 1 (each boundary once across consecutive calls): the one at
+    // the call's first iteration runs before its first attempt (swap_every =
+    // 1: the round after the init iteration), the one at its end belongs to
+    // the next call.  Chunk ends inside the call run their boundary's round.
+    if (C.a0 == 0 && I > 0 && it0 % I == 0 && it0 >= I && it0 < X.total_iters) do_round(it0 / I - 1);
     // Records stream through registers one group of kGroup windows ahead, so
     // their L2 latency hides behind the current group's commits.
     constexpr int kGroup = 4;
@@ -1120,7 +1126,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) exact_resident_kernel(CommitAr
                 if (hi > lo) commit(w0, lo, hi, cs[q], ca[q], cc[q]);
                 lo = hi;
                 if (bnd == hi && hi <= wend) {
-                    do_round(round);
+                    if (!(C.last && hi == C.n)) do_round(round);
                     bnd = next_boundary(hi, round);
                 }
             }
