@@ -209,10 +209,11 @@ def test_resident_run_matches_oracle(mods, L, R, sweeps, every, seed, J, B, rec_
         assert np.array_equal(rec.round_entry_iterations[:, 0], ref.round_entry_iterations * L * L)
 
 
-@pytest.mark.parametrize("case", range(24))
+@pytest.mark.parametrize("case", range(32))
 def test_resident_random_shapes_match_oracle(mods, case):
     """Randomised shapes, couplings and schedules through the resident kernel
-    (every gather mode, clusters, warp-owned lattices) against the oracle."""
+    (every gather mode, clusters, warp-owned lattices) and the per-interval
+    path, against the oracle."""
     p = mods[0]
     rng = np.random.default_rng(1000 + case)
     L = int(rng.choice([2, 4, 6, 8, 10, 16, 24, 32, 48, 64, 96, 128, 256]))
@@ -223,9 +224,10 @@ def test_resident_random_shapes_match_oracle(mods, case):
     B = float(rng.choice([0.0, 0.0, 0.25, -0.5]))
     rec_every = int(rng.integers(1, min(3, sweeps) + 1))
     seed = int(rng.integers(1 << 40))
+    kernel = str(rng.choice(["resident", "resident", "sweep", "auto"]))
     cfg = p.SimulationConfig(side=L, replicas=R, iterations=sweeps * L * L, swap_interval=every * L * L,
                              seed=seed, params=p.IsingParams(J=J, B=B), sweep_mode="checkerboard",
-                             record_every=rec_every, return_final_state=True, kernel="resident")
+                             record_every=rec_every, return_final_state=True, kernel=kernel)
     rec = p.run(cfg)
     assert rec.valid, rec.error
     ref = oracle.run_checkerboard(L, R, sweeps, every, seed, J=J, B=B, record_every=rec_every)
