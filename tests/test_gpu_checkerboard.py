@@ -94,13 +94,23 @@ def test_run_matches_oracle(mods, L, R, sweeps, every, seed, J, B, rec_every):
     assert rec.swap_near_ties == 0
 
 
-@pytest.mark.parametrize("chunks", [None, "3"])
-def test_host_interval_plugin_matches_oracle(mods, monkeypatch, chunks):
-    """One stream (small call, the default here) and 3 pipelined chunks."""
+@pytest.mark.parametrize("chunks,case", [(None, -1), ("3", -1)] + [(None, k) for k in range(8)])
+def test_host_interval_plugin_matches_oracle(mods, monkeypatch, chunks, case):
+    """One stream (small call, the default here) and 3 pipelined chunks; then
+    randomised shapes, couplings, fields and chunk counts."""
     p, _, kernels, _ = mods
+    L, R, seed, J, B, nsw = 64, 8, 21, 1.0, 0.0, 3
+    if case >= 0:
+        rng = np.random.default_rng(4000 + case)
+        L = int(rng.choice([2, 4, 6, 10, 32, 64, 96, 128]))
+        R = int(rng.integers(1, 12))
+        seed = int(rng.integers(1 << 40))
+        J = float(rng.choice([1.0, -1.0, 0.5]))
+        B = float(rng.choice([0.0, 0.25, -0.5]))
+        nsw = int(rng.integers(0, 4))
+        chunks = str(rng.choice(["", "1", "2", "5"])) or None
     if chunks is not None:
         monkeypatch.setenv("PTMH_PLUGIN_CHUNKS", chunks)
-    L, R, seed = 64, 8, 21
     temps = p.build_ladder(R)
     betas = 1.0 / temps
     sp = np.empty((R, L, L), dtype=np.int8)
@@ -110,17 +120,17 @@ def test_host_interval_plugin_matches_oracle(mods, monkeypatch, chunks):
     s2r = np.arange(R, dtype=np.int64)
     ref_s2r = s2r.copy()
     stats = oracle.row_stats(ref)
-    thr, always = oracle.cb_tables(betas, 1.0, 0.0)
+    thr, always = oracle.cb_tables(betas, J, B)
     done = 0
     for rnd in range(4):
         e = np.zeros(R); ss = np.zeros(R, dtype=np.int64)
-        acc = kernels.cb_interval(sp, s2r, betas, 1.0, 0.0, seed, done, 3, rnd, e, ss)
+        acc = kernels.cb_interval(sp, s2r, betas, J, B, seed, done, nsw, rnd, e, ss)
         r2s = np.empty(R, dtype=np.int64); r2s[ref_s2r] = np.arange(R)
-        for t in range(done, done + 3):
+        for t in range(done, done + nsw):
             oracle.cb_sweep(ref, r2s, thr, always, seed, t, stats)
-        done += 3
+        done += nsw
         s = stats[ref_s2r]
-        re = 0.0 * s[:, 0] - 1.0 * s[:, 1].astype(np.float64)
+        re = B * s[:, 0] - J * s[:, 1].astype(np.float64)
         rs_ = s[:, 0].copy()
         racc = oracle.swap_chunk(ref_s2r, re, rs_, betas, seed, R, rnd, rnd % 2, 0,
                                  (R - rnd % 2) // 2)
