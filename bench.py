@@ -403,7 +403,7 @@ def main():
     # ---- end to end across ranks (N > 1): the same interval through the
     # sharded driver, each rank's int8 lattices copied in from and out to
     # pinned host memory every step (the host plugin is single-device)
-    if not args.no_e2e and sharded and not resident:
+    if not args.no_e2e and sharded:
         loc = eng.spins_int8()
         host = torch.empty(tuple(loc.shape), dtype=torch.int8).pin_memory()
         host.copy_(loc)
@@ -413,11 +413,15 @@ def main():
         def e2e_step(t, r):
             dbuf.copy_(host, non_blocking=True)
             eng.load_spins(dbuf)
-            eng.sweeps(t, every)
-            drv.gather_stats()
-            eng.exchange(r)
+            if resident:  # one interval (its sweeps + round) per launch per rank, peer-memory round
+                resident_sharded(drv, peers, t, every, big, every)
+            else:
+                eng.sweeps(t, every)
+                drv.gather_stats()
+                eng.exchange(r)
             host.copy_(eng.spins_int8(), non_blocking=True)
 
+        # (an e2e step is one exchange interval, as the host plugin's call at N = 1)
         for k in range(2):  # warm
             e2e_step(sweep0, rnd0)
             sweep0 += every
@@ -435,8 +439,9 @@ def main():
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)
         e2e = {"value": n_e2e * R * L * L * every / float(dt.item()), "unit": "attempts/s",
                "h2d_bytes_per_step": int(R * L * L), "d2h_bytes_per_step": int(R * L * L),
-               "path": "distributed.ShardedCheckerboard, per-rank int8 lattices from / to pinned host "
-                       "memory each step (bytes summed over ranks); wall clock, max over ranks"}
+               "path": "distributed.ShardedCheckerboard" + (" + resident_sharded" if resident else "")
+                       + ", per-rank int8 lattices from / to pinned host memory each step (bytes summed "
+                         "over ranks); wall clock, max over ranks"}
 
     # the bit-exact reference chain (sweep_mode="exact") on the same shape
     exact = None

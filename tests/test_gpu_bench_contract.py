@@ -12,10 +12,14 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("config", ["c3", "c1"])
-def test_our_arm_line(config):
+@pytest.mark.parametrize("config,extra", [("c3", []), ("c1", []),
+                                          # the multi-GPU code paths at one rank: NCCL all-gather per
+                                          # interval (C3), peer-memory resident rounds (C5)
+                                          ("c3", ["--sharded"]), ("c5", ["--sharded"])])
+def test_our_arm_line(config, extra):
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", config, "--steps", "4",
-                          "--warmup", "3", "--no-exact"], capture_output=True, text=True, timeout=900, cwd=ROOT)
+                          "--warmup", "3", "--no-exact"] + extra, capture_output=True, text=True, timeout=900,
+                         cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads(out.stdout.strip().splitlines()[-1])
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
@@ -27,7 +31,10 @@ def test_our_arm_line(config):
     assert rf["bound"] == "hbm" and rf["unit"] == "GB/s" and 0 < rf["frac"] < 1
     assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-9
     cb = line["cpu_baseline"]
-    assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] > 0
+    if extra:  # the coordinator path (N > 1 under torchrun) leaves the CPU baseline to the N = 1 run
+        assert cb is None
+    else:
+        assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] > 0
     e2e = line["e2e"]
     assert e2e["value"] > 0 and e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0
     assert line["gpu_launches"] >= line["steps"]
