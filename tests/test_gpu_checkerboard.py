@@ -412,8 +412,18 @@ def test_host_interval_plugin_at_1024(mods, monkeypatch, plugin_sync):
         assert np.array_equal(s2r, eng.slot_to_row.cpu().numpy())
 
 
+def _random_sharded_cases(n):
+    rng = np.random.default_rng(5000)
+    out = []
+    for _ in range(n):
+        total = int(rng.integers(3, 25))
+        out.append((int(rng.choice([8, 16, 32, 64, 128])), int(rng.integers(4, 60)), int(rng.integers(2, 5)),
+                    total, int(rng.integers(1, 4)), int(rng.integers(1, min(5, total) + 1))))
+    return out
+
+
 @pytest.mark.parametrize("L,R,G,total,every,rec", [(64, 24, 2, 30, 1, 1), (64, 37, 3, 20, 2, 2),
-                                                   (16, 40, 4, 25, 1, 5)])
+                                                   (16, 40, 4, 25, 1, 5)] + _random_sharded_cases(6))
 def test_resident_sharded_virtual_ranks(mods, L, R, G, total, every, rec):
     """The multi-GPU resident kernel (rounds exchanged through peer memory
     and flags, no collective) with G ranks co-running on ONE GPU, each on its
