@@ -328,7 +328,6 @@ def main():
             step()
         torch.cuda.synchronize()
         for it in range(args.steps):
-            flush.zero_()
             # per-launch events in every 4th timed step (they cost ~1-2 us each)
             probe = it % 4 == 0
             ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))] \
@@ -337,6 +336,10 @@ def main():
             if sharded:
                 dist.barrier()
             torch.cuda.synchronize()
+            # L2 flush, then the step: its launches are queued while the GPU
+            # runs the flush, so the timed region (s0 .. s1) holds the step's
+            # GPU work and not the host's launch latency
+            flush.zero_()
             s0.record(stream)
             step(ev)
             s1.record(stream)
