@@ -23,6 +23,7 @@
 #include "common.cuh"
 #include "launchers.cuh"
 #include "philox.cuh"
+#include "strip.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -192,7 +193,7 @@ constexpr int kMaxLatPerBlock = 64;
 // threshold-plane select coefficients in shared memory
 template <bool kFerro>
 __device__ __forceinline__ void resident_set_slot(const ResidentArgs& A, int li, int slot, int* s_slot,
-                                                  uint32_t (*s_mask)[18]) {
+                                                  uint32_t (*s_mask)[19]) {
     s_slot[li] = slot;
     if (kFerro) {
         const uint32_t t3 = __ldg(A.thresh + slot * 10 + 8), t4 = __ldg(A.thresh + slot * 10 + 9);
@@ -204,6 +205,7 @@ __device__ __forceinline__ void resident_set_slot(const ResidentArgs& A, int li,
         }
         s_mask[li][16] = t3;
         s_mask[li][17] = t4;
+        s_mask[li][18] = (uint32_t)slot;
     }
 }
 
@@ -227,7 +229,11 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
     __shared__ double s_u[kMaxLatPerBlock];
     __shared__ double s_bd[kMaxLatPerBlock];       // beta_i - beta_j of the slot's pair (this round)
     __shared__ uint32_t s_pt[kMaxLatPerBlock][2];  // thresholds t3, t4 of the partner slot (ferro)
-    __shared__ uint32_t s_mask[kFerro ? kMaxLatPerBlock : 1][18];  // TM[8], TC[8], t3, t4
+    __shared__ uint32_t s_mask[kFerro ? kMaxLatPerBlock : 1][19];  // TM[8], TC[8], t3, t4, slot
+    // warp-owned 64^2 ferro lattices run the sweep kernels' strip code (2-row
+    // strips, one per lane): its tie scratch, per warp
+    constexpr bool kStrip = kFerro && kMode == kGatherRows && !kCl;
+    __shared__ uint32_t s_tie[kStrip ? kThreads / 32 : 1][3][2][32];
     // Next round's swap draws, for runs of <= 32 pairs: a warp the exchange
     // decisions leave idle computes them while the decisions run, so the
     // next publish does not wait on a Philox4x64 chain (C1: the draw was 12 %
@@ -286,9 +292,29 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
                     uint32_t* own = color ? c0 + W : c0;
                     const uint32_t* oth = color ? c0 : c0 + W;
                     int sS = 0, sB = 0;
-                    for (int w = lane; w < W; w += 32)
-                        resident_word<kMode, kFerro>(A, own, oth, w, color, s_slot[li], ctr1, sS, sB, st,
-                                                     kFerro ? s_mask[li] : nullptr, wr_shift);
+                    if (kStrip && A.strip) {
+                        // L = 64: lane = a 2-row strip (rolling window, one tie walk per strip)
+                        const int wq = (int)threadIdx.x >> 5;
+                        uint32_t(&tm)[2][32] = s_tie[kStrip ? wq : 0][0];
+                        uint32_t(&tk)[2][32] = s_tie[kStrip ? wq : 0][1];
+                        uint32_t(&tn)[2][32] = s_tie[kStrip ? wq : 0][2];
+                        if (color == 0)
+                            ferro_strip<2, 0, false, false>(A.packed, A.L, 1, W, nullptr, A.thresh, A.rk, ctr1,
+                                                            nullptr, 4u, true, lo + li, lane, tm, tk, tn, sS, sB,
+                                                            0, s_mask[li]);
+                        else if (st)
+                            ferro_strip<2, 1, true, false>(A.packed, A.L, 1, W, nullptr, A.thresh, A.rk, ctr1,
+                                                           nullptr, 4u, true, lo + li, lane, tm, tk, tn, sS, sB,
+                                                           0, s_mask[li]);
+                        else
+                            ferro_strip<2, 1, false, false>(A.packed, A.L, 1, W, nullptr, A.thresh, A.rk, ctr1,
+                                                            nullptr, 4u, true, lo + li, lane, tm, tk, tn, sS, sB,
+                                                            0, s_mask[li]);
+                    } else {
+                        for (int w = lane; w < W; w += 32)
+                            resident_word<kMode, kFerro>(A, own, oth, w, color, s_slot[li], ctr1, sS, sB, st,
+                                                         kFerro ? s_mask[li] : nullptr, wr_shift);
+                    }
                     if (st) {
                         for (int o = 16; o > 0; o >>= 1) {
                             sS += __shfl_down_sync(0xffffffffu, sS, o);
@@ -478,6 +504,7 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
                     }
                     s_mask[li][16] = t3;
                     s_mask[li][17] = t4;
+                    s_mask[li][18] = (uint32_t)nk;
                 }
             }
         }
@@ -527,6 +554,10 @@ static int launch_resident_t(const ResidentArgs& a, int sms, cudaStream_t s) {
     const int nl_max = (a.R + grid - 1) / grid;
     args.warp_lat = cs == 1 && !(ew && ew[0] == '0') && a.W <= 64 && nl_max <= kThreads / 32;
     if (args.warp_lat) threads = 32 * nl_max;
+    // L = 64 (one word per colour row): the lane-per-2-row-strip code of the
+    // sweep kernels; PTMH_RESIDENT_STRIP=0 keeps the per-word code (A/B)
+    const char* es = getenv("PTMH_RESIDENT_STRIP");
+    args.strip = args.warp_lat && a.ferro && a.W == 64 && a.WR == 1 && !(es && es[0] == '0');
     void* kargs[] = {&args};
     if (cs == 1) {
         PTMH_CUDA(cudaLaunchCooperativeKernel((const void*)cb_resident_kernel<kMode, kFerro, kThreads, false>, grid,
