@@ -46,3 +46,16 @@ def test_product_package_does_not_import_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "liboracle" not in txt, f
+
+
+def test_sync_block_size():
+    """ptmh_cb_sync_words (host arithmetic only): ticket, CTAs out, one
+    counter per lattice, and the persistent kernel's band counters (at most
+    L^2 / 16384 per lattice where the persistent path applies)."""
+    from paper_2512_03825_b200 import _lib
+    f = _lib.LIB.ptmh_cb_sync_words
+    assert f(256, 1024) == 2 + 256 + 256 * 64
+    assert f(512, 4096) == 2 + 512 + 512 * 1024
+    assert f(3, 1536) == 2 + 3 + 3 * (1536 * 1536 // 16384)
+    assert f(8, 64) == 2 + 8  # no persistent path below L = 1024
+    assert f(0, 1024) == 2
