@@ -3,6 +3,11 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--config c3|c1|c2|c4|c5]
 
+--gpus N without a torchrun environment re-launches this script under
+``python -m torch.distributed.run --nproc-per-node N`` (one rank per GPU,
+127.0.0.1 rendezvous) after checking that N GPUs are visible; under torchrun
+WORLD_SIZE must equal N.  Either mismatch exits non-zero with a message.
+
 Workload (default, BASELINE.json configs[2], the config the metric's target is
 quoted on): 2D Ising 1024^2, 256 replicas, linear ladder 1+3i/R, J=1, B=0,
 exchange every 10 sweeps.  A step = one exchange interval = 10 checkerboard
@@ -185,6 +190,37 @@ def host_cores():
         return os.cpu_count() or 1
 
 
+# ----------------------------------------------------------------- launcher --
+def _free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def _visible_gpus() -> int:
+    import torch
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+def _launch_ranks(args) -> int:
+    """Re-run this script as args.gpus ranks under torchrun (one per GPU);
+    returns the exit code.  Refuses (exit 2) when fewer GPUs are visible."""
+    if args.impl == "ours":
+        have = _visible_gpus()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, this host has {have}",
+                  file=sys.stderr, flush=True)
+            return 2
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # the init log shows the rank count
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)]
+    cmd += [a for a in sys.argv[1:] if a != "--spawn"]
+    return subprocess.run(cmd, env=env).returncode
+
+
 # --------------------------------------------------------------------- main --
 def main():
     ap = argparse.ArgumentParser()
@@ -198,8 +234,19 @@ def main():
     ap.add_argument("--no-exact", action="store_true", help="skip the exact-chain side measurement")
     ap.add_argument("--sharded", action="store_true",
                     help="use the multi-GPU coordinator (NCCL all_gather) even at one rank")
+    ap.add_argument("--spawn", action="store_true",
+                    help="launch the ranks under torchrun even for --gpus 1 (tests the launcher)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus < 1:
+        print("bench.py: --gpus must be >= 1", file=sys.stderr)
+        sys.exit(2)
+    if "WORLD_SIZE" not in os.environ and (args.gpus > 1 or args.spawn):
+        sys.exit(_launch_ranks(args))
+    if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']} ranks were launched",
+              file=sys.stderr, flush=True)
+        sys.exit(2)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -212,23 +259,30 @@ def main():
               "attempts_per_step": attempts_per_step, "J": 1.0, "B": 0.0,
               "ladder": "geometric 4^(i/(R-1))" if args.config == "c1" else "linear 1+3i/R",
               "sweep": "checkerboard, 1-bit multispin", "l2": "flushed between steps (256 MiB write)",
+              "chain": "checkerboard Metropolis (Mode F, DESIGN.md 3): a different Markov chain from the "
+                       "reference's random-site chain, statistically equal to it; the like-for-like, "
+                       "bit-exact reference chain is the exact_chain entry",
               "parallelism": f"rows sharded over {world} GPU(s), energies all-gathered"}
     metric = "spin-flip attempts/sec"
 
     if args.impl == "reference":
         if rank != 0:
             return
+        world = max(world, args.gpus)
         config = dict(config, sweep="reference random-site chain (kernels.py:62-113), int8 spins",
                       parallelism=f"{host_cores()} host threads over replica blocks "
                                   "(executor.py:227-245)", l2="n/a (CPU)")
         threads = host_cores()
         per_slot = max(1000, int(2.5e7 // R))  # ~1 s of 8-core work per step
-        for _ in range(args.warmup):
-            cpu_reference_rate(min(L, 256), R, per_slot // 10, threads)
+        # each step: every slot of the timed shape advances per_slot attempts
+        # of the reference chain (a bounded sample of the config's step)
+        config = dict(config, attempts_per_step=R * per_slot,
+                      config_attempts_per_step=attempts_per_step)
+        for _ in range(args.warmup):  # warm-up on the timed shape
+            cpu_reference_rate(L, R, max(100, per_slot // 10), threads)
         times = []
-        spins_L = L
         for _ in range(args.steps):
-            rate, n, dt = cpu_reference_rate(spins_L, R, per_slot, threads)
+            rate, n, dt = cpu_reference_rate(L, R, per_slot, threads)
             times.append(dt)
         tot = sum(times)
         val = args.steps * R * per_slot / tot
@@ -347,6 +401,8 @@ def main():
             step_ms.append(s0.elapsed_time(s1))
             if probe:
                 sweep_ms.extend(a.elapsed_time(b) for a, b in ev)
+    from paper_2512_03825_b200 import _lib
+    launched = _lib.cb_last_launch()  # this thread's last sweep launch (a timed step's)
     total_ms = sum(step_ms)
     if sharded:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -362,16 +418,12 @@ def main():
     elif persistent:  # one launch per interval: all 2*every half-sweeps
         launch_ms = statistics.mean(sweep_ms)
         bytes_per_launch = ALG_BYTES_PER_ATTEMPT * local_rows * L * L * every
-        # rows per thread as the launcher picks them (csrc/checkerboard.cu)
-        kpt = 128 if (128 % (L // 64) == 0 or local_rows * L * L >= (1 << 27)) else 256  # threads per item
-        slots = (3 * 256 // kpt) * torch.cuda.get_device_properties(dev).multi_processor_count
-        items = lambda k: local_rows * (L * L // (kpt * 64 * k))  # noqa: E731
-        krows = 32 if items(32) >= 8 * slots else next((k for k in (16, 8, 4) if items(k) >= slots), 2)
-        kernel_name = f"cb_sweeps_persistent<{krows},{kpt}>"
+        # the kernel the launcher picked for the timed steps (ptmh_cb_last_launch)
+        kernel_name = launched["name"]
     else:
         launch_ms = statistics.mean(sweep_ms) / (2.0 * every)  # two colour launches per sweep
         bytes_per_launch = ALG_BYTES_PER_ATTEMPT * local_rows * L * L / 2
-        kernel_name = "cb_half_sweep_ferro<16,0|1>" if L >= 1024 else "cb_half_sweep_ferro<8,0|1>"
+        kernel_name = launched["name"]
     achieved = bytes_per_launch / (launch_ms / 1e3) / 1e9
     peak, peak_kind = _peaks()
     traffic = _traffic(args.config) if not sharded and not resident else None
@@ -494,6 +546,10 @@ def main():
                          f"({n:.3g} attempts, {dt:.1f} s; reference chain kernels.py:62-113 "
                          f"in C, {threads} threads)"}
 
+    issue = _issue(args.config) if not resident and not sharded else None
+    issue_frac = None
+    if issue and issue.get("ipc_active"):  # ncu IPC of the same kernel / 4 issue slots per SM per cycle
+        issue_frac = float(issue["ipc_active"][0]) / float(issue.get("ipc_peak", 4.0))
     if rank == 0:
         line = {"metric": metric, "value": value, "unit": "attempts/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
@@ -504,8 +560,10 @@ def main():
                              "frac": achieved / peak, "traffic": traffic,
                              "kernel": kernel_name, "launch_ms": launch_ms,
                              "alg_bytes_per_launch": bytes_per_launch, "peak_kind": peak_kind,
-                             "note": "issue-bound (Philox + bit-sliced logic), see DESIGN.md 5",
-                             "issue_from_ncu": _issue(args.config) if not resident else None,
+                             "note": "the bound is instruction issue (Philox + bit-sliced logic), not HBM: "
+                                     "see issue_frac and DESIGN.md 5",
+                             "issue_frac": issue_frac,
+                             "issue_from_ncu": issue,
                              "traffic_note": "ncu dram read+write bytes per launch of the same kernel "
                                              "(profiles/ncu_sweep_summary.json); below the algorithmic "
                                              "bytes when the packed state stays in L2 across the "

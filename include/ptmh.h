@@ -76,6 +76,35 @@ int ptmh_host_swap_chunk(int64_t *slot_to_row, double *energies,
                          int64_t round_index, int64_t first, int64_t pair_lo,
                          int64_t pair_hi, int64_t *accepted);
 
+/* The reference's per-replica public ops on the device (host buffers).
+ *
+ * rng.py:64-96 RngStream.uniform / stream_uniform: out[t] = the uniform
+ * (w >> 11) * 2^-53 of Philox4x64-10 word 0 at (seed, stream, position + t),
+ * t = 0 .. n-1.  An RngStream then advances its position by n. */
+int ptmh_host_uniforms(uint64_t seed, uint64_t stream, uint64_t position,
+                       int64_t n, double *out);
+
+/* tempering.py:68-86 execute_swap_round, decisions only: pair k = (pair_i[k],
+ * pair_j[k]) indexes betas / energies (n entries) and draws
+ * SwapRng.pair_uniform(round_index, k) = stream stream_base + k at position
+ * round_index (rng.py:113-116); accept[k] = (u < swap_probability).  The
+ * caller swaps its replicas' lattices and energies.  near_ties: decisions a
+ * last-ulp exp difference could flip (expected 0). */
+int ptmh_host_swap_pairs(const int64_t *pair_i, const int64_t *pair_j,
+                         int64_t npairs, const double *betas,
+                         const double *energies, int64_t n, uint64_t seed,
+                         int64_t stream_base, int64_t round_index,
+                         uint8_t *accept, int64_t *near_ties);
+
+/* mh.py:73-88 mh_step, nsteps times, on one replica: lattice (L, L) int8,
+ * cached energy and spin sum, RngStream (seed, stream, *position).  Each step
+ * consumes two draws (site, acceptance), exactly as advance_block does for a
+ * slot whose stream id is `stream` (kernels.py:62-113). */
+int ptmh_host_mh_steps(int8_t *spins, int64_t L, double beta, double J,
+                       double B, double *energy, int64_t *spin_sum,
+                       uint64_t seed, uint64_t stream, uint64_t *position,
+                       int64_t nsteps);
+
 /* Checkerboard interval on host lattices (Mode F): the
  * plugin call bench.py times end to end.  Copies the int8 lattices
  * (rows, L, L) in, runs n_sweeps checkerboard sweeps starting at global
@@ -107,6 +136,18 @@ int ptmh_fill_lattices_parallel(int8_t *spins, int64_t rows, int64_t L,
                                 int64_t up_count, uint64_t seed, uint64_t stream0,
                                 uint64_t pos0, void *workspace, int64_t ws_bytes,
                                 void *stream);
+
+/* The sweep kernel the calling thread's last ptmh_cb_sweeps / _sync call
+ * launched: info[0] = kind (0 none, 1 cb_sweeps_persistent<rows, threads>,
+ * 2 cb_half_sweep_ferro<rows>, 3 cb_half_sweep_fast, 4 cb_half_sweep_generic),
+ * info[1] = rows per thread, [2] = threads per item / CTA, [3] = blocks per
+ * item (group), [4] = band dependencies, [5] = grid (persistent only). */
+int ptmh_cb_last_launch(int32_t *info);
+
+/* rng.py:64-67 stream_uniform for positions position .. position+n-1 of one
+ * stream, into device memory. */
+int ptmh_uniforms(uint64_t seed, uint64_t stream_id, uint64_t position,
+                  int64_t n, double *out, void *stream);
 
 /* stats[2r] = sum(s), stats[2r+1] = sum(s*(down+right)) of each int8 lattice
  * (the integer accumulators of kernels.py:48-59). */

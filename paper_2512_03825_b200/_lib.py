@@ -39,7 +39,13 @@ def _load():
         "ptmh_host_swap_chunk": ([P, P, P, P, i64, u64, i64, i64, i64, i64, i64, P], i32),
         "ptmh_host_cb_interval": ([P, i64, i64, P, P, f64, f64, u64, i64, i64, i64, P, P, P],
                                   i32),
+        # the reference's per-replica public ops (rng.py, mh.py, tempering.py)
+        "ptmh_host_uniforms": ([u64, u64, u64, i64, P], i32),
+        "ptmh_host_swap_pairs": ([P, P, i64, P, P, i64, u64, i64, i64, P, P], i32),
+        "ptmh_host_mh_steps": ([P, i64, f64, f64, f64, P, P, u64, u64, P, i64], i32),
         # device-resident ABI
+        "ptmh_uniforms": ([u64, u64, u64, i64, P, P], i32),
+        "ptmh_cb_last_launch": ([P], i32),
         "ptmh_fill_lattices": ([P, i64, i64, i64, u64, u64, u64, P], i32),
         "ptmh_row_stats": ([P, i64, i64, P, P], i32),
         "ptmh_fill_workspace_bytes": ([i64, i64], i64),
@@ -98,3 +104,14 @@ def check(rc: int, what: str) -> None:
 
 def call(name: str, *args) -> None:
     check(getattr(LIB, name)(*args), name)
+
+
+def cb_last_launch() -> dict:
+    """The sweep kernel this thread's last sweep call launched (ptmh_cb_last_launch)."""
+    v = (ctypes.c_int32 * 6)()
+    call("ptmh_cb_last_launch", v)
+    kinds = {0: None, 1: "cb_sweeps_persistent<{r},{t}>", 2: "cb_half_sweep_ferro<{r},0|1>",
+             3: "cb_half_sweep_fast<{r}>", 4: "cb_half_sweep_generic"}
+    k = kinds.get(v[0])
+    return {"kind": v[0], "rows": v[1], "threads": v[2], "group": v[3], "bands": bool(v[4]),
+            "grid": v[5], "name": k.format(r=v[1], t=v[2]) if k else None}

@@ -108,11 +108,12 @@ static int device_workspace(Workspace** out) {
 }
 
 static int ws_prepare(Workspace& w) {
-    if (w.dirty) {  // the previous call failed with work in flight: its copies may still use the buffers
-        for (auto& st : w.s)
-            if (st) cudaStreamSynchronize(st);
-        for (auto& st : w.cs)
-            if (st) cudaStreamSynchronize(st);
+    if (w.dirty) {
+        // the previous call failed with work in flight: its copies and kernels
+        // (also those on the exact chain's draw/commit side streams, exact.cu)
+        // may still use the buffers -- drain the whole device
+        cudaDeviceSynchronize();
+        cudaGetLastError();
     }
     w.dirty = true;  // cleared by the call's final synchronize
     for (auto& st : w.s)
@@ -484,6 +485,19 @@ int ptmh_cb_observe(const int64_t* stats_all, const int64_t* slot_to_row, int64_
     return launch_cb_observe(stats_all, slot_to_row, R, L, J, B, obs_e, obs_m, ncols, col, as_stream(stream));
 }
 
+int ptmh_cb_last_launch(int32_t* info) {
+    PTMH_CHECK_ARG(info, "cb_last_launch out");
+    const CbLaunchInfo c = cb_last_launch();
+    const int32_t v[6] = {c.kind, c.rows, c.threads, c.group, c.bands, c.grid};
+    std::memcpy(info, v, sizeof(v));
+    return PTMH_OK;
+}
+
+int ptmh_uniforms(uint64_t seed, uint64_t stream_id, uint64_t position, int64_t n, double* out, void* stream) {
+    PTMH_CHECK_ARG(n >= 0, "uniforms count");
+    return launch_uniforms(seed, stream_id, position, n, out, as_stream(stream));
+}
+
 // --------------------------------------------------------------- host ABI --
 int ptmh_host_fill_lattice(int8_t* out, int64_t n, int64_t up_count, uint64_t seed, uint64_t stream,
                            uint64_t position, uint64_t* new_position) {
@@ -645,6 +659,114 @@ int ptmh_host_swap_chunk(int64_t* slot_to_row, double* energies, int64_t* spin_s
     PTMH_CUDA(cudaStreamSynchronize(s));
     g_ws.dirty = false;
     if (accepted) *accepted = cnt[0];
+    return PTMH_OK;
+}
+
+// ---- the reference's per-replica public ops (rng.py:64-116, mh.py:73-88,
+// tempering.py:68-86) on the device; the Python layer (rng.py, mh.py,
+// tempering.py in this package) keeps the reference's objects on the host.
+int ptmh_host_uniforms(uint64_t seed, uint64_t stream, uint64_t position, int64_t n, double* out) {
+    PTMH_CHECK_ARG(n >= 0 && (n == 0 || out), "uniforms count");
+    if (n == 0) return PTMH_OK;
+    Workspace* wsp = nullptr;
+    PTMH_TRY(device_workspace(&wsp));
+    Workspace& g_ws = *wsp;
+    std::lock_guard<std::mutex> lk(g_ws.mu);
+    PTMH_TRY(ws_prepare(g_ws));
+    cudaStream_t s = g_ws.s[1];
+    double* d = nullptr;
+    PTMH_TRY(ws_get(g_ws, 20, (size_t)n, &d));
+    PTMH_TRY(launch_uniforms(seed, stream, position, n, d, s));
+    PTMH_CUDA(cudaMemcpyAsync(out, d, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+    PTMH_CUDA(cudaStreamSynchronize(s));
+    g_ws.dirty = false;
+    return PTMH_OK;
+}
+
+int ptmh_host_swap_pairs(const int64_t* pair_i, const int64_t* pair_j, int64_t npairs, const double* betas,
+                         const double* energies, int64_t n, uint64_t seed, int64_t stream_base,
+                         int64_t round_index, uint8_t* accept, int64_t* near_ties) {
+    PTMH_CHECK_ARG(npairs >= 0 && n >= 0 && stream_base >= 0 && round_index >= 0, "swap_pairs shape");
+    for (int64_t k = 0; k < npairs; ++k)
+        PTMH_CHECK_ARG(pair_i[k] >= 0 && pair_i[k] < n && pair_j[k] >= 0 && pair_j[k] < n,
+                       "swap_pairs index out of range");
+    if (near_ties) *near_ties = 0;
+    if (npairs == 0) return PTMH_OK;
+    Workspace* wsp = nullptr;
+    PTMH_TRY(device_workspace(&wsp));
+    Workspace& g_ws = *wsp;
+    std::lock_guard<std::mutex> lk(g_ws.mu);
+    PTMH_TRY(ws_prepare(g_ws));
+    cudaStream_t s = g_ws.s[1];
+    int64_t *d_i, *d_j, *d_cnt;
+    double *d_b, *d_e;
+    uint8_t* d_acc;
+    PTMH_TRY(ws_get(g_ws, 21, (size_t)npairs, &d_i));
+    PTMH_TRY(ws_get(g_ws, 22, (size_t)npairs, &d_j));
+    PTMH_TRY(ws_get(g_ws, 23, (size_t)n, &d_b));
+    PTMH_TRY(ws_get(g_ws, 24, (size_t)n, &d_e));
+    PTMH_TRY(ws_get(g_ws, 25, (size_t)npairs, &d_acc));
+    PTMH_TRY(ws_get(g_ws, 26, 1, &d_cnt));
+    PTMH_CUDA(cudaMemcpyAsync(d_i, pair_i, npairs * 8, cudaMemcpyHostToDevice, s));
+    PTMH_CUDA(cudaMemcpyAsync(d_j, pair_j, npairs * 8, cudaMemcpyHostToDevice, s));
+    PTMH_CUDA(cudaMemcpyAsync(d_b, betas, n * 8, cudaMemcpyHostToDevice, s));
+    PTMH_CUDA(cudaMemcpyAsync(d_e, energies, n * 8, cudaMemcpyHostToDevice, s));
+    PTMH_CUDA(cudaMemsetAsync(d_cnt, 0, 8, s));
+    PTMH_TRY(launch_swap_pairs(d_i, d_j, npairs, d_b, d_e, seed, stream_base, round_index, d_acc, d_cnt, s));
+    int64_t ties = 0;
+    PTMH_CUDA(cudaMemcpyAsync(accept, d_acc, (size_t)npairs, cudaMemcpyDeviceToHost, s));
+    PTMH_CUDA(cudaMemcpyAsync(&ties, d_cnt, 8, cudaMemcpyDeviceToHost, s));
+    PTMH_CUDA(cudaStreamSynchronize(s));
+    g_ws.dirty = false;
+    if (near_ties) *near_ties = ties;
+    return PTMH_OK;
+}
+
+int ptmh_host_mh_steps(int8_t* spins, int64_t L, double beta, double J, double B, double* energy,
+                       int64_t* spin_sum, uint64_t seed, uint64_t stream, uint64_t* position,
+                       int64_t nsteps) {
+    PTMH_CHECK_ARG(L >= 2 && nsteps >= 0 && energy && spin_sum && position, "mh_steps shape");
+    if (nsteps == 0) return PTMH_OK;
+    std::vector<double> tbl, dcls;
+    exact_tables(&beta, 1, J, B, tbl, dcls);
+    const int int_energy = integral(J) && integral(B) && std::fabs(J) <= 1e6 && std::fabs(B) <= 1e6 &&
+                           integral(*energy);
+    Workspace* wsp = nullptr;
+    PTMH_TRY(device_workspace(&wsp));
+    Workspace& g_ws = *wsp;
+    std::lock_guard<std::mutex> lk(g_ws.mu);
+    PTMH_TRY(ws_prepare(g_ws));
+    cudaStream_t s = g_ws.s[1];
+    const size_t nsite = (size_t)(L * L);
+    // one pinned block each way: lattice, table, (row 0, e, sum, pos, iters)
+    const size_t small = 5 * 8, tb = 20 * 8, bytes = small + tb + nsite;
+    uint8_t* pin = nullptr;
+    PTMH_TRY(ws_pinned(g_ws, bytes, &pin));
+    int64_t* hs = reinterpret_cast<int64_t*>(pin);
+    hs[0] = 0;
+    std::memcpy(&hs[1], energy, 8);
+    hs[2] = *spin_sum;
+    std::memcpy(&hs[3], position, 8);
+    hs[4] = 0;
+    std::memcpy(pin + small, tbl.data(), 10 * 8);
+    std::memcpy(pin + small + 80, dcls.data(), 10 * 8);
+    std::memcpy(pin + small + tb, spins, nsite);
+    uint8_t* d = nullptr;
+    PTMH_TRY(ws_get(g_ws, 27, bytes, &d));
+    PTMH_CUDA(cudaMemcpyAsync(d, pin, bytes, cudaMemcpyHostToDevice, s));
+    int64_t* ds = reinterpret_cast<int64_t*>(d);
+    AdvanceArgs a{reinterpret_cast<int8_t*>(d + small + tb), L, ds, 0, 1,
+                  reinterpret_cast<const double*>(d + small), reinterpret_cast<const double*>(d + small + 80),
+                  int_energy, reinterpret_cast<double*>(ds + 1), ds + 2, reinterpret_cast<uint64_t*>(ds + 3),
+                  ds + 4, seed, 0, nsteps, nullptr, nullptr, 0, 0, nullptr, nullptr, stream};
+    PTMH_TRY(launch_advance(a, s));
+    PTMH_CUDA(cudaMemcpyAsync(pin, d, bytes, cudaMemcpyDeviceToHost, s));
+    PTMH_CUDA(cudaStreamSynchronize(s));
+    g_ws.dirty = false;
+    std::memcpy(energy, &hs[1], 8);
+    *spin_sum = hs[2];
+    std::memcpy(position, &hs[3], 8);
+    std::memcpy(spins, pin + small + tb, nsite);
     return PTMH_OK;
 }
 

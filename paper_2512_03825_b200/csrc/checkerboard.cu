@@ -718,10 +718,16 @@ bool cb_sweeps_persistent_applies(int64_t L, uint32_t always_mask, int64_t n_swe
     return ferro && n_sweeps > 0 && L >= 1024 && L % 512 == 0;
 }
 
+// what the calling thread's last launch_cb_sweeps chose (ptmh_cb_last_launch:
+// tests assert the headline path, bench.py names the kernel it timed)
+static thread_local CbLaunchInfo g_last_launch = {};
+CbLaunchInfo cb_last_launch() { return g_last_launch; }
+
 int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* row_to_slot,
                      const uint32_t* thresh, uint32_t always_mask, uint64_t seed, int64_t first_sweep,
                      int64_t n_sweeps, int64_t* stats, cudaStream_t s, uint32_t* sync) {
     if (rows == 0 || n_sweeps == 0) return PTMH_OK;
+    g_last_launch = CbLaunchInfo{};
     const ClassPlan plan = make_plan(always_mask);
     const RoundKeys32 rk = make_round_keys32(seed);
     const int64_t W = cb_words(L);
@@ -816,6 +822,7 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
         // phases measure the same or 0.3 % better (fewer polls per item)
         const char* eb = getenv("PTMH_PERSIST_BANDS");  // "0" / "1" pins it (A/B and tests)
         const bool bands = kpt % WR == 0 && (eb ? eb[0] == '1' : rows * L * L < (1LL << 28));
+        g_last_launch = CbLaunchInfo{1, krows, kpt, (int)group, bands ? 1 : 0, (int)grid};
 #define PTMH_PERSIST(K, T)                                                                                    \
     cb_sweeps_persistent<K, T><<<grid, T, persistent_smem(K, T), s>>>(packed, rows, (int)L, WR, W, row_to_slot, \
                                                                       thresh, rk, c0, np, stats, 4u, sync,    \
@@ -844,6 +851,7 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
             if (fast && ferro) {  // long rows (L >= 1024): amortise the per-thread setup over 16
                 const int WR = (int)(L / 64);
                 const bool r16 = L >= 1024;
+                g_last_launch = CbLaunchInfo{2, r16 ? 16 : kFastRows, 256, 1, 0, 0};
                 const int64_t threads = rows * (L / (r16 ? 16 : kFastRows)) * WR;
                 const unsigned g = ceil_div(threads, 256);
 #define PTMH_FERRO(R, C, S) \
@@ -865,11 +873,13 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
             } else if (fast) {
                 const int WR = (int)(L / 64);
                 const int64_t threads = rows * (L / kFastRows) * WR;
+                g_last_launch = CbLaunchInfo{3, kFastRows, 256, 1, 0, 0};
                 cb_half_sweep_fast<kFastRows><<<ceil_div(threads, 256), 256, 0, s>>>(
                     packed, rows, (int)L, WR, W, row_to_slot, thresh, plan, rk, ctr1, color,
                     stats);
             } else {
                 const int64_t threads = rows * W;
+                g_last_launch = CbLaunchInfo{4, 1, 256, 1, 0, 0};
                 cb_half_sweep_generic<<<ceil_div(threads, 256), 256, 0, s>>>(
                     packed, rows, (int)L, W, row_to_slot, thresh, plan, rk, ctr1, color, stats);
             }

@@ -133,7 +133,7 @@ __global__ void advance_kernel(AdvanceArgs A) {
     double e = A.energies[slot];
     long long ssum = A.spin_sums[slot];
     const uint64_t pos0 = A.positions[slot];
-    const uint64_t st = (uint64_t)slot;
+    const uint64_t st = (uint64_t)slot + A.stream_offset;
     const double nsd = (double)n_sites;
 
     for (int64_t w0 = 0; w0 < A.nsteps; w0 += 32) {
@@ -1339,6 +1339,20 @@ int launch_bits_unpack(const uint32_t* bits, int64_t rows, int64_t L, int8_t* sp
 }
 
 // ------------------------------------------------------------------- swap --
+// The swap rule's saturating logistic (kernels.py:127-135, tempering.py:53-65)
+// in the reference's split form, every operation rounded as numba does.
+__device__ __forceinline__ double swap_logistic(double x) {
+    if (x >= 0.0) return __ddiv_rn(1.0, __dadd_rn(1.0, exp(-x)));
+    const double ex = exp(x);
+    return __ddiv_rn(ex, __dadd_rn(1.0, ex));
+}
+
+// device exp and host libm may differ in the last ulp: a decision such a
+// difference could flip is counted (expected: none; every parity test asserts 0)
+__device__ __forceinline__ bool near_tie(double u, double prob) {
+    return fabs(u - prob) <= 4.0 * 2.220446049250313e-16 * fmax(prob, 2.2250738585072014e-308);
+}
+
 __global__ void swap_kernel(int64_t* __restrict__ slot_to_row, double* __restrict__ energies,
                             int64_t* __restrict__ spin_sums, const double* __restrict__ betas,
                             int64_t R, uint64_t seed, int64_t stream_base, int64_t round_index,
@@ -1359,16 +1373,8 @@ __global__ void swap_kernel(int64_t* __restrict__ slot_to_row, double* __restric
         const int64_t i = first + 2 * p, j = i + 1;
         const double u = stream_uniform(seed, (uint64_t)(stream_base + p), (uint64_t)round_index);
         const double x = __dmul_rn(__dsub_rn(betas[i], betas[j]), __dsub_rn(energies[i], energies[j]));
-        double prob;
-        if (x >= 0.0) {
-            prob = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-x)));
-        } else {
-            const double ex = exp(x);
-            prob = __ddiv_rn(ex, __dadd_rn(1.0, ex));
-        }
-        // device exp and host libm may differ in the last ulp: count decisions
-        // that such a difference could flip (expected: none)
-        if (fabs(u - prob) <= 4.0 * 2.220446049250313e-16 * fmax(prob, 2.2250738585072014e-308)) ++ties;
+        const double prob = swap_logistic(x);
+        if (near_tie(u, prob)) ++ties;
         if (u < prob) {
             const int64_t tr = slot_to_row[i]; slot_to_row[i] = slot_to_row[j]; slot_to_row[j] = tr;
             const double te = energies[i]; energies[i] = energies[j]; energies[j] = te;
@@ -1388,6 +1394,33 @@ __global__ void swap_kernel(int64_t* __restrict__ slot_to_row, double* __restric
         __syncthreads();
         for (int64_t k = threadIdx.x; k < R; k += blockDim.x) row_to_slot[slot_to_row[k]] = (int32_t)k;
     }
+}
+
+// RngStream.uniform / stream_uniform (rng.py:64-96): out[t] = uniform at
+// position pos0 + t of one stream.
+__global__ void uniforms_kernel(uint64_t seed, uint64_t stream, uint64_t pos0, int64_t n, double* out) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+        out[t] = stream_uniform(seed, stream, pos0 + (uint64_t)t);
+}
+
+// execute_swap_round's decisions (tempering.py:68-86) for an explicit pair
+// list: pair k = (pi[k], pj[k]) uses SwapRng.pair_uniform(round, k), i.e.
+// stream stream_base + k at position round_index (rng.py:113-116).
+__global__ void swap_pairs_kernel(const int64_t* __restrict__ pi, const int64_t* __restrict__ pj, int64_t npairs,
+                                  const double* __restrict__ betas, const double* __restrict__ energies,
+                                  uint64_t seed, int64_t stream_base, int64_t round_index,
+                                  uint8_t* __restrict__ accept, int64_t* near_ties) {
+    int ties = 0;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < npairs;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = pi[k], j = pj[k];
+        const double u = stream_uniform(seed, (uint64_t)(stream_base + k), (uint64_t)round_index);
+        const double x = __dmul_rn(__dsub_rn(betas[i], betas[j]), __dsub_rn(energies[i], energies[j]));
+        const double prob = swap_logistic(x);
+        if (near_tie(u, prob)) ++ties;
+        accept[k] = u < prob ? 1 : 0;
+    }
+    if (ties && near_ties) atomicAdd((unsigned long long*)near_ties, (unsigned long long)ties);
 }
 
 // ------------------------------------------------------------ launchers --
@@ -1419,6 +1452,23 @@ int launch_advance(const AdvanceArgs& a, cudaStream_t s) {
     if (n <= 0 || a.nsteps <= 0) return PTMH_OK;
     const int warps = 4;
     advance_kernel<<<ceil_div(n, warps), 32 * warps, 0, s>>>(a);
+    PTMH_LAUNCH_CHECK();
+    return PTMH_OK;
+}
+
+int launch_uniforms(uint64_t seed, uint64_t stream, uint64_t pos0, int64_t n, double* out, cudaStream_t s) {
+    if (n <= 0) return PTMH_OK;
+    uniforms_kernel<<<std::min<int64_t>(ceil_div(n, 256), 4096), 256, 0, s>>>(seed, stream, pos0, n, out);
+    PTMH_LAUNCH_CHECK();
+    return PTMH_OK;
+}
+
+int launch_swap_pairs(const int64_t* pi, const int64_t* pj, int64_t npairs, const double* betas,
+                      const double* energies, uint64_t seed, int64_t stream_base, int64_t round_index,
+                      uint8_t* accept, int64_t* near_ties, cudaStream_t s) {
+    if (npairs <= 0) return PTMH_OK;
+    swap_pairs_kernel<<<std::min<int64_t>(ceil_div(npairs, 256), 1024), 256, 0, s>>>(
+        pi, pj, npairs, betas, energies, seed, stream_base, round_index, accept, near_ties);
     PTMH_LAUNCH_CHECK();
     return PTMH_OK;
 }

@@ -28,6 +28,8 @@ struct AdvanceArgs {
     int record;
     int8_t* states;
     uint32_t* bits;  // bit-packed lattices (row-major bits, ceil(L*L/32) words per row) or null
+    uint64_t stream_offset;  // advance_kernel only: slot k draws from stream k + stream_offset
+                             // (a lone replica's RngStream id, mh.py:73-88); 0 = the reference
 };
 
 // exact.cu (n = sites per lattice row)
@@ -51,6 +53,13 @@ int launch_advance_2phase(const AdvanceArgs& a, void* ws, int64_t ws_bytes, cuda
 int64_t advance_ws_bytes(int64_t nslots, int64_t nsteps);
 int launch_bits_pack(const int8_t* spins, int64_t rows, int64_t L, uint32_t* bits, cudaStream_t s);
 int launch_bits_unpack(const uint32_t* bits, int64_t rows, int64_t L, int8_t* spins, cudaStream_t s);
+// n consecutive uniforms of one stream (rng.py:64-67, RngStream.uniform)
+int launch_uniforms(uint64_t seed, uint64_t stream, uint64_t pos0, int64_t n, double* out, cudaStream_t s);
+// reference swap rule for an explicit pair list (tempering.py:68-86): pair k
+// draws from stream stream_base + k at position round_index; accept[k] = 0/1
+int launch_swap_pairs(const int64_t* pi, const int64_t* pj, int64_t npairs, const double* betas,
+                      const double* energies, uint64_t seed, int64_t stream_base, int64_t round_index,
+                      uint8_t* accept, int64_t* near_ties, cudaStream_t s);
 int launch_swap(int64_t* slot_to_row, double* energies, int64_t* spin_sums, const double* betas,
                 int64_t R, uint64_t seed, int64_t stream_base, int64_t round_index, int64_t first,
                 int64_t pair_lo, int64_t pair_hi, int64_t* accepted, int64_t* near_ties,
@@ -62,6 +71,12 @@ int64_t cb_words(int64_t L);
 int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* row_to_slot,
                      const uint32_t* thresh, uint32_t always_mask, uint64_t seed, int64_t first_sweep,
                      int64_t n_sweeps, int64_t* stats, cudaStream_t s, uint32_t* sync = nullptr);
+// kind: 0 none, 1 cb_sweeps_persistent<rows, threads>, 2 cb_half_sweep_ferro<rows>,
+// 3 cb_half_sweep_fast, 4 cb_half_sweep_generic
+struct CbLaunchInfo {
+    int kind, rows, threads, group, bands, grid;
+};
+CbLaunchInfo cb_last_launch();
 bool cb_sweeps_persistent_applies(int64_t L, uint32_t always_mask, int64_t n_sweeps);
 int launch_cb_pack(const int8_t* spins, int64_t rows, int64_t L, uint32_t* packed, cudaStream_t s);
 int launch_cb_unpack(const uint32_t* packed, int64_t rows, int64_t L, int8_t* spins, cudaStream_t s);

@@ -141,6 +141,16 @@ def resident_sharded(drv: "ShardedCheckerboard", peers: PeerBuffers, first_sweep
     eng = drv.eng
     lo, hi = drv.bounds[drv.rank]
     before = eng.counters.clone()
+    cols = None
+    if obs_e is not None and record_every > 0:
+        # the columns recorded in this segment: each slot's entry is written
+        # by the rank holding the slot at that sweep; zero them here so that
+        # the other ranks contribute exact zeros to the combine below
+        c0, c1 = first_sweep // record_every, (first_sweep + n_sweeps) // record_every
+        if c1 > c0:
+            cols = (c0, c1)
+            obs_e[:, c0:c1].zero_()
+            obs_m[:, c0:c1].zero_()
     eng.run_resident_sharded(first_sweep, n_sweeps, total_sweeps, swap_every, drv.rank, drv.world,
                              peers.pub_peers, peers.flag_peers, peers.slot_stats,
                              record_every=record_every, obs_e=obs_e, obs_m=obs_m)
@@ -154,12 +164,10 @@ def resident_sharded(drv: "ShardedCheckerboard", peers: PeerBuffers, first_sweep
     delta = eng.counters - before  # this segment's counts on this rank
     dist.all_reduce(delta, group=drv.group)
     eng.counters.copy_(before + delta)
-    if obs_e is not None and record_every > 0:
-        # the columns recorded in this segment; each slot's entry was
-        # written by the rank holding it, the others hold zeros
-        c0, c1 = first_sweep // record_every, (first_sweep + n_sweeps) // record_every
-        if c1 > c0:
-            for o in (obs_e, obs_m):
-                part = o[:, c0:c1].contiguous()
-                dist.all_reduce(part, group=drv.group)
-                o[:, c0:c1].copy_(part)
+    if cols is not None:
+        # one writer per entry, zeros elsewhere: an integer sum of the float64
+        # bit patterns reproduces the writer's value exactly (signed zeros too)
+        for o in (obs_e, obs_m):
+            part = o[:, cols[0]:cols[1]].contiguous().view(torch.int64)
+            dist.all_reduce(part, group=drv.group)
+            o[:, cols[0]:cols[1]].copy_(part.view(torch.float64))

@@ -15,6 +15,13 @@ Extensions (all defaulted so reference configs run unchanged):
   default is the reference's build_ladder.
 * ``device``: CUDA device index.  ``workers`` is validated and recorded
   but the GPU replaces the thread pool.
+* ``devices``: the GPUs of a multi-GPU checkerboard run, one process per
+  device (torchrun).  Rank r of the default process
+  group runs on ``devices[r]`` and owns the lattice rows
+  ``assign_replicas(replicas, len(devices))[r]``; exchanges all-gather the
+  per-lattice (S, Bond) pairs (NCCL) or, on the resident path, go through
+  NVLink peer memory.  Every rank returns the same RunRecord.  With one
+  device and no process group, run() opens a world-1 NCCL group itself.
 * ``return_final_state``: also return the final lattices (by row) and
   slot_to_row, for parity checks.
 """
@@ -58,6 +65,7 @@ class SimulationConfig:
     temperatures: tuple | None = None
     record_every: int = 1
     device: int | None = None
+    devices: tuple | None = None
     return_final_state: bool = False
     # checkerboard: "sweep" (launches per interval), "resident" (1 launch/run);
     # exact: "sweep" (launches per interval), "auto"/"resident": rounds inside
@@ -93,6 +101,21 @@ class SimulationConfig:
             raise ConfigurationError(f"kernel must be one of {KERNELS}, got {self.kernel!r}")
         if self.record_every < 1:
             raise ConfigurationError(f"record_every must be >= 1, got {self.record_every}")
+        if self.devices is not None:
+            devs = list(self.devices)
+            if (not devs or any(not isinstance(d, (int, np.integer)) or isinstance(d, bool) or d < 0
+                                for d in devs) or len(set(devs)) != len(devs)):
+                raise ConfigurationError(
+                    f"devices must be distinct non-negative device indices, got {self.devices!r}")
+            if self.device is not None:
+                raise ConfigurationError("set either device or devices, not both")
+            if len(devs) > 1 and self.sweep_mode != "checkerboard":
+                raise ConfigurationError(
+                    "the exact chain runs on one device; multi-GPU runs need sweep_mode='checkerboard'")
+            if len(devs) > 8:
+                raise ConfigurationError("at most 8 devices (one NVLink node)")
+            if self.record_mode == "full_states" and len(devs) > 1:
+                raise ConfigurationError("full_states recording is single-device")
         if self.sweep_mode == "checkerboard":
             n = self.side * self.side
             if self.side % 2:
@@ -172,11 +195,12 @@ def _resident_wins(L: int, swap_every_sweeps: int) -> bool:
 class _StateStream:
     """full_states recording for the checkerboard chain: each sample is
     unpacked on the device in slot order into one of two staging buffers and
-    copied asynchronously into a pinned host array (R, n_samples, L, L), so
-    the copy of sample c overlaps the sweeps towards sample c+1."""
+    copied asynchronously into its own contiguous block of a pinned host array
+    (n_samples, R, L, L), so the copy of sample c overlaps the sweeps towards
+    sample c+1; result() returns the reference's (R, n_samples, L, L) layout."""
 
     def __init__(self, R: int, n: int, L: int, dev):
-        self.host = torch.empty((R, n, L, L), dtype=torch.int8, pin_memory=True)
+        self.host = torch.empty((n, R, L, L), dtype=torch.int8, pin_memory=True)
         self.stage = [torch.empty((R, L, L), dtype=torch.int8, device=dev) for _ in range(2)]
         self.done = [torch.cuda.Event(), torch.cuda.Event()]
         self.copy = torch.cuda.Stream(dev)
@@ -188,13 +212,13 @@ class _StateStream:
         eng.snapshot_by_slot(self.stage[b])
         self.copy.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(self.copy):
-            self.host[:, col].copy_(self.stage[b], non_blocking=True)
+            self.host[col].copy_(self.stage[b], non_blocking=True)
             self.done[b].record(self.copy)
         self.k += 1
 
     def result(self) -> np.ndarray:
         self.copy.synchronize()
-        return self.host.numpy()
+        return np.ascontiguousarray(self.host.numpy().transpose(1, 0, 2, 3))
 
 
 def _sync(dev):
@@ -217,7 +241,7 @@ def _run_exact(config: SimulationConfig) -> RunRecord:
     t_start = time.perf_counter()
     R, L, N, I = config.replicas, config.side, config.iterations, config.swap_interval
     rec_flag = RECORD_MODES.index(config.record_mode)
-    dev = require_cuda(config.device)
+    dev = require_cuda(config.devices[0] if config.devices is not None else config.device)
     temps = config.ladder()
     eng = None
     errors: list[BaseException] = []
@@ -288,25 +312,80 @@ def _run_exact(config: SimulationConfig) -> RunRecord:
         slot_to_row=eng.slot_to_row.cpu().numpy() if (valid and config.return_final_state) else None)
 
 
+def _process_group(config: SimulationConfig) -> bool:
+    """The process group a ``devices`` run shards over; opens a world-1 NCCL
+    group when there is none and one device is named (returns True then, so
+    the caller closes it).  Raises ConfigurationError before any work when
+    the launch does not match ``devices``."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    n = len(config.devices)
+    if dist.is_available() and dist.is_initialized():
+        if dist.get_world_size() != n:
+            raise ConfigurationError(
+                f"devices names {n} GPU(s) but the process group has {dist.get_world_size()} rank(s)")
+        return False
+    if n != 1:
+        raise ConfigurationError(
+            f"devices={tuple(config.devices)!r}: a multi-GPU run is one process per device; launch it "
+            f"with torchrun --nproc-per-node {n} (or init the process group) and call run() on every rank")
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1,
+                            device_id=torch.device("cuda", int(config.devices[0])))
+    return True
+
+
 def _run_checkerboard(config: SimulationConfig) -> RunRecord:
-    from .engine import CheckerboardEngine, require_cuda
+    from .engine import require_cuda
+
+    sharded = config.devices is not None
+    own_group = _process_group(config) if sharded else False
+    try:
+        if sharded:
+            import torch.distributed as dist
+            dev = require_cuda(config.devices[dist.get_rank()])
+        else:
+            dev = require_cuda(config.device)
+        return _checkerboard_on(config, dev, sharded)
+    finally:
+        if own_group:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+def _checkerboard_on(config: SimulationConfig, dev, sharded: bool) -> RunRecord:
+    from .engine import CheckerboardEngine
 
     t_start = time.perf_counter()
     R, L = config.replicas, config.side
     n_sites = L * L
     sweeps, every_sw = config.iterations // n_sites, config.swap_interval // n_sites
     record = config.record_mode != "none"
-    dev = require_cuda(config.device)
     temps = config.ladder()
     errors: list[BaseException] = []
+    drv = peers = None
     with torch.cuda.device(dev):
         t0 = time.perf_counter()
-        eng = CheckerboardEngine(L, R, temps, config.seed, config.params.J, config.params.B,
-                                 config.init_up_fraction, dev)
-        eng.init_state()
+        if sharded:
+            from .distributed import ShardedCheckerboard
+            drv = ShardedCheckerboard(L, R, temps, config.seed, config.params.J, config.params.B,
+                                      config.init_up_fraction, device=dev)
+            eng = drv.eng
+            drv.init_state()
+        else:
+            eng = CheckerboardEngine(L, R, temps, config.seed, config.params.J, config.params.B,
+                                     config.init_up_fraction, dev)
+            eng.init_state()
         n_samples = sweeps // config.record_every if record else 0
-        obs_e = torch.empty((R, n_samples), dtype=torch.float64, device=dev) if record else None
-        obs_m = torch.empty((R, n_samples), dtype=torch.float64, device=dev) if record else None
+        obs_e = torch.zeros((R, n_samples), dtype=torch.float64, device=dev) if record else None
+        obs_m = torch.zeros((R, n_samples), dtype=torch.float64, device=dev) if record else None
         full = config.record_mode == "full_states"
         states = _StateStream(R, n_samples, L, dev) if full else None
         _sync(dev)
@@ -321,10 +400,16 @@ def _run_checkerboard(config: SimulationConfig) -> RunRecord:
                                      (config.kernel == "auto" and _resident_wins(L, every_sw)))
         try:
             if use_resident:
-                # the whole run in one persistent launch; the schedule is replayed
-                # on the host only for the bookkeeping fields
-                eng.run_resident(0, sweeps, sweeps, every_sw,
-                                 config.record_every if record else 0, obs_e, obs_m)
+                # the whole run in one persistent launch (per rank; across
+                # ranks the rounds go through peer memory); the schedule is
+                # replayed on the host only for the bookkeeping fields
+                rec_every = config.record_every if record else 0
+                if sharded:
+                    from .distributed import PeerBuffers, resident_sharded
+                    peers = PeerBuffers(R, dev)
+                    resident_sharded(drv, peers, 0, sweeps, sweeps, every_sw, rec_every, obs_e, obs_m)
+                else:
+                    eng.run_resident(0, sweeps, sweeps, every_sw, rec_every, obs_e, obs_m)
                 for target, ri in plan:
                     if ri is None:
                         continue
@@ -333,6 +418,7 @@ def _run_checkerboard(config: SimulationConfig) -> RunRecord:
                     rounds += 1
                     attempted += max(0, (R - ri % 2) // 2)
                 plan = []
+            gathered = -1  # sweep count at which every lattice's (S, Bond) was last all-gathered
             for target, ri in plan:
                 while done < target:
                     if record:
@@ -342,6 +428,9 @@ def _run_checkerboard(config: SimulationConfig) -> RunRecord:
                     eng.sweeps(done, nxt - done)
                     done = nxt
                     if record and done % config.record_every == 0:
+                        if sharded and gathered != done:
+                            drv.gather_stats()
+                            gathered = done
                         eng.observe(obs_e, obs_m, done // config.record_every - 1)
                         if full:
                             states.push(eng, done // config.record_every - 1)
@@ -350,23 +439,49 @@ def _run_checkerboard(config: SimulationConfig) -> RunRecord:
                 if snaps is not None:
                     snaps[ri, :] = done * n_sites
                 rounds += 1
+                if sharded and gathered != done:
+                    drv.gather_stats()
+                    gathered = done
                 attempted += eng.exchange(ri)
             _sync(dev)
         except BaseException as exc:  # noqa: BLE001
             errors.append(exc)
+        finally:
+            if peers is not None:
+                peers.close()
         exec_seconds = time.perf_counter() - t1
 
     valid = not errors
     accepted, near = eng.swap_counts() if valid else (0, 0)
+    final = None
+    if valid and config.return_final_state:
+        final = _gather_lattices(drv) if sharded else eng.final_spins()
     return RunRecord(
         config=config, temperatures=temps,
         energies=obs_e.cpu().numpy() if (valid and record) else None,
         magnetizations=obs_m.cpu().numpy() if (valid and record) else None,
         states=states.result() if (valid and full) else None, swap_rounds=rounds,
         swaps_attempted=attempted, swaps_accepted=accepted,
+        # Mode F draws are addressed by (slot, sweep, colour, site) and never
+        # advance a stream position; the init phase's Fisher-Yates is the only
+        # positional consumer (L^2 - 1 draws of stream r, kernels.py:26-45)
         rng_positions=np.full(R, n_sites - 1, dtype=np.int64),
         round_entry_iterations=snaps, init_seconds=init_seconds, exec_seconds=exec_seconds,
         total_seconds=time.perf_counter() - t_start, valid=valid,
         error=None if valid else repr(errors[0]), sweep_mode="checkerboard", swap_near_ties=near,
-        final_spins=eng.final_spins() if (valid and config.return_final_state) else None,
+        final_spins=final,
         slot_to_row=eng.slot_to_row.cpu().numpy() if (valid and config.return_final_state) else None)
+
+
+def _gather_lattices(drv) -> np.ndarray:
+    """Every rank's int8 lattices, in row order, on every rank."""
+    import torch.distributed as dist
+
+    eng = drv.eng
+    loc = eng.spins_int8()
+    pad = torch.zeros((drv.maxc, eng.L, eng.L), dtype=torch.int8, device=loc.device)
+    pad[: loc.shape[0]].copy_(loc)
+    out = torch.empty((drv.world * drv.maxc, eng.L, eng.L), dtype=torch.int8, device=loc.device)
+    dist.all_gather_into_tensor(out, pad, group=drv.group)
+    parts = [out[g * drv.maxc: g * drv.maxc + (h - l)] for g, (l, h) in enumerate(drv.bounds)]
+    return torch.cat(parts).cpu().numpy()

@@ -1,11 +1,14 @@
 """Temperature ladder, pairing schedule and swap rule (isingpt tempering.py).
 
-Host-side definitions.  The device exchange kernel (csrc/exact.cu
-swap_kernel) evaluates the same rule for every pair of a round.
+``build_ladder``, ``pairing`` and ``swap_probability`` are the reference's
+host-side definitions.  The sampling loop's exchange is the device kernel
+csrc/exact.cu swap_kernel; ``execute_swap_round`` (the per-replica API)
+decides its pairs with the same device rule (swap_pairs_kernel).
 """
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass
 
@@ -56,3 +59,35 @@ def swap_probability(beta_i: float, beta_j: float, energy_i: float, energy_j: fl
         return 1.0 / (1.0 + math.exp(-x))
     ex = math.exp(x)
     return ex / (1.0 + ex)
+
+
+def execute_swap_round(replicas, swap_round: SwapRound, swap_rng) -> int:
+    """Decide every pair of ``swap_round`` independently; returns the accepted
+    count (tempering.py:68-86).
+
+    Pair k draws ``swap_rng.pair_uniform(round_index, k)``; an accepted pair
+    exchanges the two replicas' lattices and cached energies, while
+    temperatures and streams stay with their slots.  The decisions are made
+    on the device (``ptmh_host_swap_pairs``) by the exchange kernels' rule.
+    """
+    from . import _lib
+
+    pairs = swap_round.pairs
+    if not pairs:
+        return 0
+    pi = np.ascontiguousarray([i for i, _ in pairs], dtype=np.int64)
+    pj = np.ascontiguousarray([j for _, j in pairs], dtype=np.int64)
+    betas = np.ascontiguousarray([r.beta for r in replicas], dtype=np.float64)
+    energies = np.ascontiguousarray([r.energy for r in replicas], dtype=np.float64)
+    accept = np.zeros(len(pairs), dtype=np.uint8)
+    ties = ctypes.c_int64(0)
+    vp = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    _lib.call("ptmh_host_swap_pairs", vp(pi), vp(pj), len(pairs), vp(betas), vp(energies),
+              len(replicas), swap_rng.master_seed, swap_rng.replica_count,
+              int(swap_round.round_index), vp(accept), ctypes.byref(ties))
+    for (i, j), ok in zip(pairs, accept):
+        if ok:
+            a, b = replicas[i], replicas[j]
+            a.lattice, b.lattice = b.lattice, a.lattice
+            a.energy, b.energy = b.energy, a.energy
+    return int(accept.sum())

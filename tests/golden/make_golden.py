@@ -202,8 +202,103 @@ def cli_vectors():
         json.dump({"cases": out, "seeds": seeds}, f, indent=1)
 
 
+def api_vectors():
+    """isingpt.__all__ and the call signature of every public name, for the
+    drop-in API test (tests/test_public_api.py)."""
+    import inspect
+    import json
+    sigs = {}
+    for name in isingpt.__all__:
+        obj = getattr(isingpt, name)
+        try:
+            sig = inspect.signature(obj)
+        except (TypeError, ValueError):
+            sigs[name] = None
+            continue
+        sigs[name] = [[p.name, str(p.kind), None if p.default is inspect.Parameter.empty
+                       else repr(p.default)] for p in sig.parameters.values()]
+    with open(os.path.join(OUT, "api.json"), "w") as f:
+        json.dump({"all": list(isingpt.__all__), "signatures": sigs}, f, indent=1)
+
+
+def public_op_vectors():
+    """The reference's per-replica public ops (rng.py, mh.py, tempering.py,
+    analysis.py) on small cases, for the GPU-backed restatements."""
+    from isingpt import analysis, mh, tempering
+    from isingpt.rng import RngStream, SwapRng
+    out = {}
+    params = IsingParams(J=1.0, B=0.0)
+    # RngStream / SwapRng
+    st = RngStream(42, 3, 5)
+    out["rng_uniforms"] = np.array([st.uniform() for _ in range(16)])
+    out["rng_choose"] = np.array([st.choose(1000) for _ in range(16)], dtype=np.int64)
+    out["rng_position"] = np.array([st.position], dtype=np.int64)
+    sw = SwapRng(2 ** 63 + 11, 7)
+    out["swap_uniforms"] = np.array([[sw.pair_uniform(r, p) for p in range(4)] for r in range(5)])
+    # make_replica + mh_step loops (two couplings, one with a field)
+    for tag, L, T, seed, idx, prm in (("a", 6, 2.0, 99, 0, params), ("b", 5, 1.5, 7, 3, IsingParams(J=1.0, B=0.5)),
+                                      ("c", 8, 3.0, 2 ** 40 + 1, 11, IsingParams(J=-0.7, B=0.3))):
+        rep = mh.make_replica(L, 0.5, T, seed, idx, prm)
+        out[f"rep_{tag}_init"] = rep.lattice.spins.copy()
+        out[f"rep_{tag}_init_pos"] = np.array([rep.rng.position], dtype=np.int64)
+        out[f"rep_{tag}_init_e"] = np.array([rep.energy])
+        acc, es = [], []
+        for _ in range(300):
+            acc.append(mh.mh_step(rep, prm))
+            es.append(rep.energy)
+        out[f"rep_{tag}_acc"] = np.array(acc, dtype=np.uint8)
+        out[f"rep_{tag}_e"] = np.array(es)
+        out[f"rep_{tag}_final"] = rep.lattice.spins.copy()
+        out[f"rep_{tag}_pos"] = np.array([rep.rng.position], dtype=np.int64)
+    # the PT composition of test_executor.py:80-104 (R=4, L=4, N=60, I=10)
+    R, L, N, I = 5, 4, 120, 10
+    temps = tempering.build_ladder(R)
+    reps = [mh.make_replica(L, 0.5, float(temps[i]), 5, i, params) for i in range(R)]
+    swap_rng = SwapRng(5, R)
+    E = np.zeros((R, N))
+    accs = []
+    rnd = 0
+    for it in range(N):
+        for i, rep in enumerate(reps):
+            mh.mh_step(rep, params)
+            E[i, it] = rep.energy
+        if (it + 1) % I == 0 and it + 1 < N:
+            accs.append(tempering.execute_swap_round(reps, tempering.pairing(rnd, R), swap_rng))
+            rnd += 1
+    out["pt_E"] = E
+    out["pt_acc"] = np.array(accs, dtype=np.int64)
+    out["pt_final"] = np.stack([r.lattice.spins for r in reps])
+    # analysis
+    rs = np.random.default_rng(5)
+    series = np.concatenate([np.linspace(0.0, 1.0, 400), 0.8 + 0.01 * rs.standard_normal(1600)])
+    out["conv_series"] = series
+    out["conv_result"] = np.array([
+        -1 if (v := analysis.convergence_iteration(series, analysis.ConvergenceCriterion(window=w, tolerance=t)))
+        is None else v for w, t in ((100, 0.02), (50, 0.005), (200, 0.05), (10, 1e-6))], dtype=np.int64)
+    pts = np.array([[8, 120.0], [16, 530.0], [32, 2100.0], [64, 8800.0]])
+    fit = analysis.fit_power_law(pts)
+    out["fit_pts"] = pts
+    out["fit"] = np.array([fit.exponent, fit.prefactor, fit.r_squared])
+    states = (rs.integers(0, 2, size=(3, 5, 3, 3)) * 2 - 1).astype(np.int8)
+    out["enc_states"] = states
+    out["enc_codes"] = analysis.encode_configurations(states)
+    for side, T, prm, tag in ((2, 2.0, params, "2"), (3, 2.5, IsingParams(J=1.0, B=0.5), "3"),
+                              (4, 1.7, IsingParams(J=-0.5, B=0.2), "4")):
+        out[f"boltz_{tag}"] = analysis.exact_boltzmann_distribution(side, T, prm)
+    rec = run(SimulationConfig(side=6, replicas=3, iterations=4000, swap_interval=100, workers=1, seed=3))
+    out["eq_mag_m"] = rec.magnetizations
+    out["eq_mag_05"] = analysis.equilibrium_magnetization(rec)
+    out["eq_mag_0"] = analysis.equilibrium_magnetization(rec, 0.0)
+    out["eq_mag_09"] = analysis.equilibrium_magnetization(rec, 0.9)
+    np.savez_compressed(os.path.join(OUT, "public_ops.npz"), **out)
+
+
 if __name__ == "__main__":
     kernels.warm_kernels()
+    if len(sys.argv) > 1:  # e.g. `make_golden.py api_vectors public_op_vectors`
+        for name in sys.argv[1:]:
+            globals()[name]()
+        sys.exit(0)
     cli_vectors()
     philox_vectors()
     kernel_vectors()

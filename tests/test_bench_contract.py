@@ -26,3 +26,21 @@ def test_reference_arm_line():
     assert cb["value"] == line["value"] and cb["kind"] == "port" and cb["cores"] >= 1 and cb["sample"]
     e2e = line["e2e"]
     assert e2e["value"] == line["value"] and e2e["h2d_bytes_per_step"] == 0 and e2e["d2h_bytes_per_step"] == 0
+
+
+def test_gpus_flag_refuses_missing_gpus():
+    """--gpus N without torchrun self-launches N ranks, after checking that N
+    GPUs are visible: this CPU container has none, so it must refuse loudly."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert out.returncode != 0
+    assert "--gpus 2 needs 2 visible GPUs" in out.stderr
+    assert not out.stdout.strip()
+
+
+def test_gpus_flag_must_match_launched_world():
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "1", "--steps", "1"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT,
+                         env=dict(os.environ, RANK="0", WORLD_SIZE="2", LOCAL_RANK="0"))
+    assert out.returncode != 0 and "WORLD_SIZE=2" in out.stderr

@@ -13,6 +13,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.parametrize("config,extra", [("c3", []), ("c1", []),
+                                          # the --gpus launcher: re-run under torchrun (one rank here)
+                                          ("c3", ["--gpus", "1", "--spawn"]),
                                           # the multi-GPU code paths at one rank: NCCL all-gather per
                                           # interval (C3), peer-memory resident rounds (C5)
                                           ("c3", ["--sharded"]), ("c5", ["--sharded"])])
@@ -30,8 +32,10 @@ def test_our_arm_line(config, extra):
     rf = line["roofline"]
     assert rf["bound"] == "hbm" and rf["unit"] == "GB/s" and 0 < rf["frac"] < 1
     assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-9
+    if "--spawn" not in extra:
+        assert line["roofline"]["kernel"] is not None
     cb = line["cpu_baseline"]
-    if extra:  # the coordinator path (N > 1 under torchrun) leaves the CPU baseline to the N = 1 run
+    if "--sharded" in extra:  # the coordinator path (N > 1 under torchrun) leaves the CPU baseline to the N = 1 run
         assert cb is None
     else:
         assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] > 0
@@ -40,3 +44,11 @@ def test_our_arm_line(config, extra):
     assert line["gpu_launches"] >= line["steps"]
     assert line["clocks"]["sm_mhz"] is not None
     assert "l2" in line["config"] and line["config"]["workload"].startswith("2D Ising")
+
+
+def test_gpus_beyond_visible_refused():
+    import torch
+    n = torch.cuda.device_count() + 1
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(n), "--steps", "2"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode != 0 and f"--gpus {n} needs {n} visible GPUs" in out.stderr
