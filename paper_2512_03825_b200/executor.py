@@ -11,6 +11,9 @@ Extensions (all defaulted so reference configs run unchanged):
   where ``iterations`` and ``swap_interval`` must be whole sweeps (multiples
   of side**2) and observables are recorded per sweep (every
   ``record_every`` sweeps), shape (R, sweeps // record_every).
+* ``record_every`` (exact chain, record_mode="observables"): keep every
+  k-th column of the reference's per-attempt series -- column c is the
+  reference's column (c+1)k - 1, shape (R, iterations // k).
 * ``temperatures``: explicit ladder (e.g. tempering.geometric_ladder);
   default is the reference's build_ladder.
 * ``device``: CUDA device index.  ``workers`` is validated and recorded
@@ -116,6 +119,11 @@ class SimulationConfig:
                 raise ConfigurationError("at most 8 devices (one NVLink node)")
             if self.record_mode == "full_states" and len(devs) > 1:
                 raise ConfigurationError("full_states recording is single-device")
+        if self.sweep_mode == "exact" and self.record_every > 1:
+            if self.record_mode != "observables":
+                raise ConfigurationError("record_every > 1 subsamples record_mode='observables' only")
+            if self.record_every > self.iterations:
+                raise ConfigurationError("record_every exceeds the number of iterations")
         if self.sweep_mode == "checkerboard":
             n = self.side * self.side
             if self.side % 2:
@@ -254,12 +262,24 @@ def _run_exact(config: SimulationConfig) -> RunRecord:
         eng = ExactEngine(L, R, temps, config.seed, config.params.J, config.params.B,
                           config.init_up_fraction, dev)
         eng.init_state()
+        k = config.record_every
+        sub = rec_flag == 1 and k > 1  # subsampled observables: column c = state after (c+1)k iterations
         if rec_flag >= 1:
-            obs_e = torch.empty((R, N), dtype=torch.float64, device=dev)
-            obs_m = torch.empty((R, N), dtype=torch.float64, device=dev)
+            ncol = N // k if sub else N
+            obs_e = torch.empty((R, ncol), dtype=torch.float64, device=dev)
+            obs_m = torch.empty((R, ncol), dtype=torch.float64, device=dev)
         if rec_flag == 2:
             states = torch.empty((R, N, L, L), dtype=torch.int8, device=dev)
-        eng.advance(0, 1, obs_e, obs_m, rec_flag, states)  # iteration 0 (executor.py:218-220)
+        if sub:
+            eng.advance(0, 1)  # iteration 0 (executor.py:218-220)
+        else:
+            eng.advance(0, 1, obs_e, obs_m, rec_flag, states)
+
+        def sample(done: int) -> None:
+            # the reference's column done-1 (kernels.py:103-105): E and sum(s)/L^2 by slot
+            if done % k == 0:
+                obs_e[:, done // k - 1].copy_(eng.energies)
+                obs_m[:, done // k - 1].copy_(eng.spin_sums.to(torch.float64) / float(L * L))
         _sync(dev)
         init_seconds = time.perf_counter() - t0
 
@@ -269,7 +289,20 @@ def _run_exact(config: SimulationConfig) -> RunRecord:
         snaps = np.zeros((n_rounds, R), dtype=np.int64) if rec_flag >= 1 and n_rounds else None
         completed = 1
         try:
-            if config.kernel != "sweep" and eng.resident_ok(rec_flag):
+            if sub:
+                for target, ri in plan:
+                    while completed < target:
+                        nxt = min(target, (completed // k + 1) * k)
+                        eng.advance(completed, nxt - completed)
+                        completed = nxt
+                        sample(completed)
+                    if ri is None:
+                        continue
+                    if snaps is not None:
+                        snaps[ri, :] = completed
+                    rounds += 1
+                    attempted += eng.exchange(ri)
+            elif config.kernel != "sweep" and eng.resident_ok(rec_flag):
                 # few small lattices (the reference's C1): the whole run with its
                 # rounds in chunked launches (csrc/exact.cu, exact_resident_kernel)
                 eng.run_resident(1, N - 1, I, N, obs_e, obs_m)

@@ -7,7 +7,7 @@
   count must equal the oracle's chain (oracle.cb_sweep_mt restates
   or_cb_sweep over host threads; tests/test_oracle_mt.py pins the two).
 * C4 -- the bench's C4 launch (512 lattices of 4096^2: the parallel init's
-  multi-batch path, then cb_sweeps_persistent<32,128> with two-block items
+  multi-batch path, then cb_sweeps_persistent<32,128> with multi-block items
   and lattice-wide phases, asserted) on the GPU; a sample of the lattices is
   checked against the oracle's init and sweeps (the lattices are independent
   between exchange rounds, so each sampled lattice's chain is complete).
@@ -95,7 +95,9 @@ def test_c4_launch_on_sampled_lattices_equals_oracle():
 
     eng.sweeps(0, n_sweeps)
     launch = _lib.cb_last_launch()
-    assert launch["name"] == "cb_sweeps_persistent<32,128>" and launch["group"] == 2 \
+    # the bench's C4 configuration (same shape, so the same launcher choice):
+    # 32-row strips, multi-block items, lattice-wide phases
+    assert launch["name"] == "cb_sweeps_persistent<32,128>" and launch["group"] >= 2 \
         and not launch["bands"], launch
     thr, always = oracle.cb_tables(1.0 / temps, J, B)
     r2s = rows.copy()  # no exchange yet: row r holds slot r
