@@ -270,6 +270,7 @@ def main():
             return
         world = max(world, args.gpus)
         config = dict(config, sweep="reference random-site chain (kernels.py:62-113), int8 spins",
+                      chain="the reference's random-site Metropolis chain (its C restatement, oracle/)",
                       parallelism=f"{host_cores()} host threads over replica blocks "
                                   "(executor.py:227-245)", l2="n/a (CPU)")
         threads = host_cores()

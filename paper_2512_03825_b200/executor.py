@@ -144,7 +144,18 @@ class SimulationConfig:
 
 @dataclass
 class RunRecord:
-    """Everything one run produced (executor.py:70-88, plus extensions)."""
+    """Everything one run produced (executor.py:70-88, plus extensions).
+
+    Checkerboard records (``sweep_mode="checkerboard"``): ``rng_positions``
+    is the init phase's stream consumption (L^2 - 1 per slot; Mode F draws
+    are addressed by slot, sweep, colour and site, so no position advances
+    after init), and ``round_entry_iterations[k]`` is the iteration count
+    (sweeps x L^2) every slot had completed when round k was decided -- the
+    reference's barrier audit (executor.py:228-229,253-256).  On the
+    resident path the rounds run inside one launch behind a grid barrier and
+    the row is the schedule's value; the barrier itself is what every
+    resident parity test checks.
+    """
 
     config: SimulationConfig
     temperatures: np.ndarray

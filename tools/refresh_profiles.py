@@ -1,6 +1,6 @@
 """Copy a gpurun bench/ncu batch (gpurun_out/) into profiles/ and refresh the
 numbers quoted in DESIGN.md section 5 (tools/ only).
-    python tools/refresh_profiles.py"""
+    python tools/refresh_profiles.py [round prefix, default r2]"""
 import collections
 import csv
 import json
@@ -11,6 +11,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 G, P = os.path.join(ROOT, "gpurun_out"), os.path.join(ROOT, "profiles")
+RND = sys.argv[1] if len(sys.argv) > 1 else "r2"
 
 
 def last_line(path):
@@ -19,9 +20,9 @@ def last_line(path):
 
 
 for c in ("c1", "c2", "c3", "c4", "c5"):
-    with open(os.path.join(P, f"r1_bench_{c}.json"), "w") as f:
+    with open(os.path.join(P, f"{RND}_bench_{c}.json"), "w") as f:
         f.write(last_line(os.path.join(G, f"bench_{c}.log")) + "\n")
-with open(os.path.join(P, "r1_bench_reference_c3.json"), "w") as f:
+with open(os.path.join(P, f"{RND}_bench_reference_c3.json"), "w") as f:
     f.write(last_line(os.path.join(G, "bench_ref_c3.log")) + "\n")
 
 # launch list: all launches, then the timed steps' share
@@ -50,12 +51,12 @@ out = ["# ncu --metrics gpu__time_duration.sum --clock-control none -c 400: pyth
        f"{'launches':>8} {'total_us':>11} {'share':>6} {'avg_us':>9}  kernel"]
 for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
     out.append(f"{n:8d} {t / 1e3:11.1f} {100 * t / tot:5.1f}% {t / n / 1e3:9.2f}  {k}")
-open(os.path.join(P, "r1_launches_bench_c3.txt"), "w").write("\n".join(out) + "\n")
+open(os.path.join(P, f"{RND}_launches_bench_c3.txt"), "w").write("\n".join(out) + "\n")
 
 # ncu capture of the persistent kernel
 subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), os.path.join(G, "persist_c3.ncu-rep"),
-                "--json", os.path.join(P, "r1_ncu_full_persistent_c3.json")], capture_output=True, check=True)
-p = json.load(open(os.path.join(P, "r1_ncu_full_persistent_c3.json")))[0]
+                "--json", os.path.join(P, f"{RND}_ncu_full_persistent_c3.json")], capture_output=True, check=True)
+p = json.load(open(os.path.join(P, f"{RND}_ncu_full_persistent_c3.json")))[0]
 d = json.load(open(os.path.join(P, "ncu_sweep_summary.json")))
 words = 256 * 1024 * 1024 * 10 / 32
 d["c3"].update({"dram_bytes_per_launch": p["dram_read"] + p["dram_write"],
@@ -70,11 +71,11 @@ json.dump(d, open(os.path.join(P, "ncu_sweep_summary.json"), "w"), indent=1)
 # DESIGN.md section 5 table
 f = {}
 for c in ("c1", "c2", "c3", "c4", "c5"):
-    b = json.load(open(os.path.join(P, f"r1_bench_{c}.json")))
+    b = json.load(open(os.path.join(P, f"{RND}_bench_{c}.json")))
     f[c] = ("%.3g" % b["value"], "%.3g" % b["ms_per_step"], "%.3g" % b["e2e"]["value"],
             "%.3g" % b["exact_chain"]["value"] if b.get("exact_chain") else "—", "%.3g" % b["cpu_baseline"]["value"])
     print(c, f[c], "frac %.3f" % b["roofline"]["frac"], b["clocks"]["sm_mhz"], b["clocks"]["reasons"])
-ref = json.load(open(os.path.join(P, "r1_bench_reference_c3.json")))
+ref = json.load(open(os.path.join(P, f"{RND}_bench_reference_c3.json")))
 s = open(os.path.join(ROOT, "DESIGN.md")).read()
 a, e = s.index("## 5. Measured performance"), s.index("**The C3 hot kernel**")
 sec = s[a:e].split("\n")
