@@ -22,6 +22,33 @@ import torch.distributed as dist
 from .executor import assign_replicas
 
 
+def _host_staged(group) -> bool:
+    """gloo moves host tensors: CUDA tensors are staged through host memory
+    (the CPU tests and multi-process tests on one GPU); NCCL moves them
+    directly (NVLink)."""
+    return dist.get_backend(group) == "gloo"
+
+
+def all_gather_into(out: torch.Tensor, inp: torch.Tensor, group=None) -> None:
+    """dist.all_gather_into_tensor for any backend."""
+    if out.is_cuda and _host_staged(group):
+        o = out.cpu()
+        dist.all_gather_into_tensor(o, inp.cpu(), group=group)
+        out.copy_(o)
+    else:
+        dist.all_gather_into_tensor(out, inp, group=group)
+
+
+def all_reduce_sum(t: torch.Tensor, group=None) -> None:
+    """dist.all_reduce (sum) for any backend."""
+    if t.is_cuda and _host_staged(group):
+        h = t.cpu()
+        dist.all_reduce(h, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, group=group)
+
+
 class ShardedCheckerboard:
     """Checkerboard PT over the ranks of ``group``.
 
@@ -58,10 +85,10 @@ class ShardedCheckerboard:
             # stats, from a separate send buffer (no aliasing of input and
             # output, which only world-1 runs could test here)
             self._send.copy_(self.eng.local_stats)
-            dist.all_gather_into_tensor(self.eng.stats, self._send, group=self.group)
+            all_gather_into(self.eng.stats, self._send, self.group)
             return
         self._send[: hi - lo].copy_(self.eng.local_stats)
-        dist.all_gather_into_tensor(self._recv, self._send, group=self.group)
+        all_gather_into(self._recv, self._send, self.group)
         for g, (l, h) in enumerate(self.bounds):
             if h > l:
                 self.eng.stats[l:h].copy_(self._recv[g * self.maxc: g * self.maxc + (h - l)])
@@ -157,17 +184,17 @@ def resident_sharded(drv: "ShardedCheckerboard", peers: PeerBuffers, first_sweep
     loc = torch.zeros(drv.maxc, dtype=torch.int32, device=eng.stats.device)
     loc[: hi - lo].copy_(eng.row_to_slot[lo:hi])
     allr = torch.empty(drv.world * drv.maxc, dtype=torch.int32, device=loc.device)
-    dist.all_gather_into_tensor(allr, loc, group=drv.group)
+    all_gather_into(allr, loc, drv.group)
     for g, (l, h) in enumerate(drv.bounds):
         eng.row_to_slot[l:h].copy_(allr[g * drv.maxc: g * drv.maxc + (h - l)])
     eng.slot_to_row[eng.row_to_slot.long()] = torch.arange(eng.R, dtype=torch.int64, device=loc.device)
     delta = eng.counters - before  # this segment's counts on this rank
-    dist.all_reduce(delta, group=drv.group)
+    all_reduce_sum(delta, drv.group)
     eng.counters.copy_(before + delta)
     if cols is not None:
         # one writer per entry, zeros elsewhere: an integer sum of the float64
         # bit patterns reproduces the writer's value exactly (signed zeros too)
         for o in (obs_e, obs_m):
             part = o[:, cols[0]:cols[1]].contiguous().view(torch.int64)
-            dist.all_reduce(part, group=drv.group)
+            all_reduce_sum(part, drv.group)
             o[:, cols[0]:cols[1]].copy_(part.view(torch.float64))

@@ -519,13 +519,13 @@ def _checkerboard_on(config: SimulationConfig, dev, sharded: bool) -> RunRecord:
 
 def _gather_lattices(drv) -> np.ndarray:
     """Every rank's int8 lattices, in row order, on every rank."""
-    import torch.distributed as dist
+    from .distributed import all_gather_into
 
     eng = drv.eng
     loc = eng.spins_int8()
     pad = torch.zeros((drv.maxc, eng.L, eng.L), dtype=torch.int8, device=loc.device)
     pad[: loc.shape[0]].copy_(loc)
     out = torch.empty((drv.world * drv.maxc, eng.L, eng.L), dtype=torch.int8, device=loc.device)
-    dist.all_gather_into_tensor(out, pad, group=drv.group)
+    all_gather_into(out, pad, drv.group)
     parts = [out[g * drv.maxc: g * drv.maxc + (h - l)] for g, (l, h) in enumerate(drv.bounds)]
     return torch.cat(parts).cpu().numpy()
