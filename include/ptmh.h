@@ -278,6 +278,26 @@ int ptmh_cb_run_resident(uint32_t *packed, int64_t R, int64_t L,
                          int64_t total_sweeps, int64_t swap_every,
                          int64_t record_every, int *buf_out, void *stream);
 
+/* ptmh_cb_run_resident with a workspace of ptmh_cb_resident_ws_bytes(R,
+ * n_rounds) bytes (n_rounds: the segment's exchange rounds).  Where every
+ * lattice has its own warp (small lattices, e.g. C5's 64^2 x 4096, C1), the
+ * rounds are then decided pair by pair -- each lattice publishes its
+ * (S, Bond) for its slot and waits only for its partner slot's -- instead of
+ * behind a grid barrier (csrc/resident.cu, cb_resident_p2p_kernel); the
+ * workspace holds the segment's swap draws.  Same chain, same results. */
+int64_t ptmh_cb_resident_ws_bytes(int64_t R, int64_t n_rounds);
+int ptmh_cb_run_resident_ws(uint32_t *packed, int64_t R, int64_t L,
+                            int64_t *slot_to_row2, int32_t *row_to_slot2,
+                            int buf, const uint32_t *thresh,
+                            uint32_t always_mask, uint64_t seed, double J,
+                            double B, const double *betas, int64_t *stats,
+                            int64_t *slot_stats, int64_t *counters,
+                            double *obs_e, double *obs_m, int64_t ncols,
+                            int64_t first_sweep, int64_t n_sweeps,
+                            int64_t total_sweeps, int64_t swap_every,
+                            int64_t record_every, int *buf_out, void *ws,
+                            int64_t ws_bytes, void *stream);
+
 /* ptmh_cb_run_resident over `world` GPUs (one process each): this rank owns
  * the `rows` lattices of global rows row_lo .. row_lo + rows - 1; slots,
  * betas, thresholds, observables and slot_to_row2 (2, R_total) range over

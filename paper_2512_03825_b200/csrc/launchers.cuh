@@ -124,8 +124,15 @@ struct ResidentArgs {
     int64_t* pub_peer[8];    // slot_stats (2, R_total, 2) of every rank (peer pointers), [rank] = own
     uint32_t* flag_peer[8];  // flags (world) of every rank, [rank] = own
     int max_ctas;            // 0 = fill the GPU (tests cap it to co-run virtual ranks on one GPU)
+    // Point-to-point rounds (cb_resident_p2p_kernel): the swap draws of this
+    // segment's rounds, u_table[(round - u_round0) * u_stride + pair]
+    // (filled by swap_draws_kernel before the launch); null = grid-barrier rounds
+    const double* u_table;
+    int64_t u_round0, u_stride;
 };
 int launch_cb_resident(const ResidentArgs& a, bool fast, cudaStream_t s, int* grid_out);
+// workspace of the point-to-point rounds: the swap draws of n_rounds rounds
+int64_t resident_ws_bytes(int64_t R, int64_t n_rounds);
 void fill_class_plan(uint32_t always_mask, int* n_up, int* k, int* sf, int* cls, int* ferro);
 
 }  // namespace ptmh

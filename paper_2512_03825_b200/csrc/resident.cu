@@ -513,6 +513,195 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
     }
 }
 
+// ------------------------------------------- point-to-point exchange rounds --
+// The same run as cb_resident_kernel for warp-owned lattices on one GPU, with
+// the exchange rounds decided pairwise instead of behind a grid barrier.  At
+// a round the lattice's warp publishes its (S, Bond) for its slot k as ONE
+// 64-bit word -- (S, Bond, round stamp) packed, so the value and its flag
+// arrive together and no fence is needed -- into a 4-deep ring indexed by
+// round, then polls the partner slot's word until it carries this round's
+// stamp and decides the pair with the reference rule (both sides compute the
+// same decision).  A warp therefore waits only for its partner, never for
+// the slowest lattice of the grid, and while it waits the SM runs the other
+// lattices' sweeps.
+//
+// Deadlock-free: every CTA is resident (cooperative launch), each warp owns
+// one lattice, and the round-r publish of every slot depends only on round
+// r-1 decisions, which depend on round r-1 publishes (induction on r).
+// The ring is safe at depth 3: the next write to entry (r mod D, k) happens
+// at round r+D, after its writer passed round r+D-1, which (chasing the
+// pairings of rounds r+1 .. r+2, which alternate between the two neighbours)
+// happens after the round-r reader of entry k decided; depth 4 is used.
+// Stamps carry a valid bit, and the launcher zeroes the ring first, so an
+// entry left by an earlier launch never matches.
+// The swap draws (stream R+p, position = round; rng.py:113-116) come from a
+// table the launcher fills before the launch (swap_draws_kernel): a
+// Philox4x64-10 chain per round and lattice stays off the warps' path.
+constexpr int kRing = 4;
+
+__device__ __forceinline__ uint64_t p2p_pack(int64_t S, int64_t Bd, int64_t round) {
+    const uint64_t st = (uint64_t)((round & 0x7fff) | 0x8000);
+    return st | (((uint64_t)S & 0xffffffull) << 16) | (((uint64_t)Bd & 0xffffffull) << 40);
+}
+__device__ __forceinline__ int64_t p2p_field(uint64_t v, int shift) {
+    return (int64_t)(((int64_t)(v << (40 - shift))) >> 40);  // sign-extended 24-bit field at `shift`
+}
+__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void swap_draws_kernel(uint64_t seed, int64_t R, int64_t round0, int64_t n_rounds, int64_t stride,
+                                  double* __restrict__ out) {
+    const int64_t n = n_rounds * stride;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = t / stride, p = t - r * stride;
+        out[t] = stream_uniform(seed, (uint64_t)(R + p), (uint64_t)(round0 + r));
+    }
+}
+
+template <int kMode, bool kFerro, int kThreads>
+__global__ void __launch_bounds__(kThreads) cb_resident_p2p_kernel(ResidentArgs A) {
+    constexpr int kWarps = kThreads / 32;
+    __shared__ uint32_t s_mask[kWarps][19];  // the warp's lattice: TM[8], TC[8], t3, t4, slot
+    __shared__ int s_slot[kWarps];
+    constexpr bool kStrip = kFerro && kMode == kGatherRows;
+    __shared__ uint32_t s_tie[kStrip ? kWarps : 1][3][2][32];
+    const int lane = threadIdx.x & 31, wq = (int)threadIdx.x >> 5;
+    const int R = A.R, W = A.W;
+    const int lo = (int)((int64_t)R * blockIdx.x / gridDim.x);
+    const int hi = (int)((int64_t)R * (blockIdx.x + 1) / gridDim.x);
+    if (wq >= hi - lo) return;  // no block-wide barrier below: spare warps leave
+    const int row = lo + wq;
+    const int wr_shift = (A.WR > 0 && (A.WR & (A.WR - 1)) == 0) ? __ffs(A.WR) - 1 : -1;
+    uint32_t* const c0 = A.packed + (int64_t)row * 2 * W;
+    uint64_t* const ring = reinterpret_cast<uint64_t*>(A.slot_stats);  // kRing x R words
+    if (lane == 0) resident_set_slot<kFerro>(A, wq, A.r2s[A.buf][row], s_slot, s_mask);
+    __syncwarp();
+    int k = s_slot[wq];
+    int rounds = 0;
+    for (int64_t t = A.first_sweep; t < A.first_sweep + A.n_sweeps; ++t) {
+        const int64_t done = t + 1;
+        const bool rec = A.record_every > 0 && done % A.record_every == 0;
+        const bool exch = A.swap_every > 0 && done % A.swap_every == 0 && done < A.total_sweeps;
+        const bool last = t + 1 == A.first_sweep + A.n_sweeps;
+        const bool need_stats = rec || exch || last;
+        int sS = 0, sB = 0;
+        for (int color = 0; color < 2; ++color) {
+            const uint32_t ctr1 = (uint32_t)(2 * t + color);
+            const bool st = color == 1 && need_stats;
+            uint32_t* own = color ? c0 + W : c0;
+            const uint32_t* oth = color ? c0 : c0 + W;
+            if (kStrip && A.strip) {
+                uint32_t(&tm)[2][32] = s_tie[kStrip ? wq : 0][0];
+                uint32_t(&tk)[2][32] = s_tie[kStrip ? wq : 0][1];
+                uint32_t(&tn)[2][32] = s_tie[kStrip ? wq : 0][2];
+                if (color == 0)
+                    ferro_strip<2, 0, false, false>(A.packed, A.L, 1, W, nullptr, A.thresh, A.rk, ctr1, nullptr, 4u,
+                                                    true, row, lane, tm, tk, tn, sS, sB, 0, s_mask[wq]);
+                else if (st)
+                    ferro_strip<2, 1, true, false>(A.packed, A.L, 1, W, nullptr, A.thresh, A.rk, ctr1, nullptr, 4u,
+                                                   true, row, lane, tm, tk, tn, sS, sB, 0, s_mask[wq]);
+                else
+                    ferro_strip<2, 1, false, false>(A.packed, A.L, 1, W, nullptr, A.thresh, A.rk, ctr1, nullptr, 4u,
+                                                    true, row, lane, tm, tk, tn, sS, sB, 0, s_mask[wq]);
+            } else {
+                for (int w = lane; w < W; w += 32)
+                    resident_word<kMode, kFerro>(A, own, oth, w, color, k, ctr1, sS, sB, st,
+                                                 kFerro ? s_mask[wq] : nullptr, wr_shift);
+            }
+            __syncwarp();  // the colour's words are stored before the other colour reads them
+        }
+        if (!need_stats) continue;
+        for (int o = 16; o > 0; o >>= 1) {
+            sS += __shfl_down_sync(0xffffffffu, sS, o);
+            sB += __shfl_down_sync(0xffffffffu, sB, o);
+        }
+        int nk = k;
+        if (lane == 0) {
+            const int64_t S = sS, Bd = sB;
+            if (last) {
+                A.stats[2 * row] = S;
+                A.stats[2 * row + 1] = Bd;
+            }
+            if (rec) {  // by slot, before the round (executor.py order)
+                const int64_t col = done / A.record_every - 1;
+                A.obs_e[(int64_t)k * A.ncols + col] = __dsub_rn(__dmul_rn(A.B, (double)S), __dmul_rn(A.J, (double)Bd));
+                A.obs_m[(int64_t)k * A.ncols + col] = __ddiv_rn((double)S, (double)A.L * A.L);
+            }
+            if (exch) {
+                const int64_t round = done / A.swap_every - 1;
+                const int first = (int)(round % 2);
+                const int n_pairs = (R - first) / 2;
+                uint64_t* slot_word = ring + (round % kRing) * (int64_t)R;
+                st_relaxed_u64(slot_word + k, p2p_pack(S, Bd, round));
+                if (k >= first && (k - first) / 2 < n_pairs) {
+                    const int p = (k - first) / 2, i = first + 2 * p, j = i + 1, other = k == i ? j : i;
+                    // everything that does not need the partner's energy, while its word travels
+                    const double u = A.u_table[(round - A.u_round0) * A.u_stride + p];
+                    const double bd = __dsub_rn(A.betas[i], A.betas[j]);
+                    const uint32_t ot3 = kFerro ? __ldg(A.thresh + other * 10 + 8) : 0u;
+                    const uint32_t ot4 = kFerro ? __ldg(A.thresh + other * 10 + 9) : 0u;
+                    const uint64_t want = (uint64_t)((round & 0x7fff) | 0x8000);
+                    uint64_t v = ld_relaxed_u64(slot_word + other);
+                    while ((v & 0xffffull) != want) {
+                        __nanosleep(64);
+                        v = ld_relaxed_u64(slot_word + other);
+                    }
+                    const int64_t So = p2p_field(v, 16), Bo = p2p_field(v, 40);
+                    const int64_t Si = k == i ? S : So, Bi = k == i ? Bd : Bo;
+                    const int64_t Sj = k == i ? So : S, Bj = k == i ? Bo : Bd;
+                    const double Ei = __dsub_rn(__dmul_rn(A.B, (double)Si), __dmul_rn(A.J, (double)Bi));
+                    const double Ej = __dsub_rn(__dmul_rn(A.B, (double)Sj), __dmul_rn(A.J, (double)Bj));
+                    const double x = __dmul_rn(bd, __dsub_rn(Ei, Ej));
+                    double prob;
+                    if (x >= 0.0) {
+                        prob = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-x)));
+                    } else {
+                        const double ex = exp(x);
+                        prob = __ddiv_rn(ex, __dadd_rn(1.0, ex));
+                    }
+                    const bool acc = u < prob;
+                    if (k == i) {
+                        if (acc) atomicAdd((unsigned long long*)&A.counters[0], 1ull);
+                        if (fabs(u - prob) <= 4.0 * 2.220446049250313e-16 * fmax(prob, 2.2250738585072014e-308))
+                            atomicAdd((unsigned long long*)&A.counters[1], 1ull);
+                    }
+                    if (acc) {
+                        nk = other;
+                        s_slot[wq] = nk;
+                        if (kFerro) {
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                const uint32_t ta = (ot3 >> (31 - q)) & 1u, tb = (ot4 >> (31 - q)) & 1u;
+                                s_mask[wq][q] = tb - ta;
+                                s_mask[wq][8 + q] = 0u - ta;
+                            }
+                            s_mask[wq][16] = ot3;
+                            s_mask[wq][17] = ot4;
+                            s_mask[wq][18] = (uint32_t)nk;
+                        }
+                    }
+                }
+            }
+        }
+        if (exch) ++rounds;
+        k = __shfl_sync(0xffffffffu, nk, 0);
+        __syncwarp();  // s_mask of the new slot before the next sweep
+    }
+    // the permutation is an output only: the final mapping, in the buffer the
+    // grid-barrier kernel would leave it in (buf flips once per round)
+    if (lane == 0) {
+        const int fb = A.buf ^ (rounds & 1);
+        A.r2s[fb][row] = k;
+        A.s2r[fb][k] = row;
+    }
+}
+
 template <int kMode, bool kFerro, int kThreads>
 static int launch_resident_t(const ResidentArgs& a, int sms, cudaStream_t s) {
     int per_sm = 0;
@@ -559,6 +748,16 @@ static int launch_resident_t(const ResidentArgs& a, int sms, cudaStream_t s) {
     const char* es = getenv("PTMH_RESIDENT_STRIP");
     args.strip = args.warp_lat && a.ferro && a.W == 64 && a.WR == 1 && !(es && es[0] == '0');
     void* kargs[] = {&args};
+    // point-to-point rounds (cb_resident_p2p_kernel): warp-owned lattices, one
+    // per warp, one GPU, a swap-draw table; PTMH_RESIDENT_P2P=0 turns it off
+    const char* ep = getenv("PTMH_RESIDENT_P2P");
+    if (cs == 1 && args.warp_lat && a.world == 1 && a.u_table && nl_max <= threads / 32 && a.L <= 1024 &&
+        !(ep && ep[0] == '0')) {
+        if (a.swap_every > 0) PTMH_CUDA(cudaMemsetAsync(a.slot_stats, 0, (size_t)kRing * a.R * 8, s));
+        PTMH_CUDA(cudaLaunchCooperativeKernel((const void*)cb_resident_p2p_kernel<kMode, kFerro, kThreads>, grid,
+                                              threads, kargs, 0, s));
+        return PTMH_OK;
+    }
     if (cs == 1) {
         PTMH_CUDA(cudaLaunchCooperativeKernel((const void*)cb_resident_kernel<kMode, kFerro, kThreads, false>, grid,
                                               threads, kargs, 0, s));
@@ -601,9 +800,20 @@ static int launch_resident_sized(const ResidentArgs& a, cudaStream_t s) {
     return launch_resident_t<kMode, kFerro, 256>(a, sms, s);
 }
 
+int64_t resident_ws_bytes(int64_t R, int64_t n_rounds) { return std::max<int64_t>(1, n_rounds) * (R / 2 + 1) * 8; }
+
 int launch_cb_resident(const ResidentArgs& a_in, bool fast, cudaStream_t s, int* grid_out) {
     (void)grid_out;
     ResidentArgs a = a_in;
+    if (a.u_table && a.swap_every > 0) {  // this segment's swap draws, for the point-to-point rounds
+        // rounds fire at done = (r + 1) * swap_every, first_sweep < done <= the
+        // segment's end, strictly below total_sweeps (executor.py:111-125)
+        const int64_t last = std::min(a.first_sweep + a.n_sweeps, a.total_sweeps - 1);
+        const int64_t n = a.u_stride * std::max<int64_t>(1, last / a.swap_every - a.u_round0);
+        swap_draws_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, s>>>(
+            a.seed, a.R, a.u_round0, n / a.u_stride, a.u_stride, const_cast<double*>(a.u_table));
+        PTMH_LAUNCH_CHECK();
+    }
     const bool segs = !fast && a.L >= 8 && 64 % a.L == 0;
     if (segs) {
         const int seg = a.L / 2;

@@ -284,11 +284,33 @@ class CheckerboardEngine(_Base):
         self._r2s2[0].copy_(self.row_to_slot)
         out = ctypes.c_int(0)
         ncols = obs_e.shape[1] if obs_e is not None else 0
-        _lib.call("ptmh_cb_run_resident", _P(self.packed), self.R, self.L, _P(self._s2r2),
-                  _P(self._r2s2), 0, _P(self.thr), self.always, self.seed, self.J, self.B,
-                  _P(self.betas), _P(self.stats), _P(self._slot_stats), _P(self.counters), _P(obs_e),
-                  _P(obs_m), ncols, first_sweep, n_sweeps, total_sweeps, swap_every, record_every,
-                  ctypes.byref(out), self._s())
+        # the segment's swap draws (point-to-point rounds where lattices are
+        # warp-owned; csrc/resident.cu), in segments of <= 4096 rounds
+        seg = n_sweeps
+        if swap_every > 0:
+            seg = max(swap_every, min(n_sweeps, 4096 * swap_every))
+        done = 0
+        while done < n_sweeps:
+            n = min(seg, n_sweeps - done)
+            t0 = first_sweep + done
+            rounds = sum(1 for d in range(t0 + 1, t0 + n + 1)
+                         if swap_every > 0 and d % swap_every == 0 and d < total_sweeps) if swap_every else 0
+            ws = None
+            if rounds:
+                need = int(_lib.LIB.ptmh_cb_resident_ws_bytes(self.R, rounds))
+                if getattr(self, "_res_ws", None) is None or self._res_ws.numel() < need:
+                    self._res_ws = torch.empty(need, dtype=torch.uint8, device=self.dev)
+                ws = self._res_ws
+            _lib.call("ptmh_cb_run_resident_ws", _P(self.packed), self.R, self.L, _P(self._s2r2),
+                      _P(self._r2s2), 0, _P(self.thr), self.always, self.seed, self.J, self.B,
+                      _P(self.betas), _P(self.stats), _P(self._slot_stats), _P(self.counters), _P(obs_e),
+                      _P(obs_m), ncols, t0, n, total_sweeps, swap_every, record_every,
+                      ctypes.byref(out), _P(ws), ws.numel() if ws is not None else 0, self._s())
+            if out.value != 0 and done + n < n_sweeps:
+                self._s2r2[0].copy_(self._s2r2[out.value])
+                self._r2s2[0].copy_(self._r2s2[out.value])
+                out.value = 0
+            done += n
         self.slot_to_row.copy_(self._s2r2[out.value])
         self.row_to_slot.copy_(self._r2s2[out.value])
 

@@ -199,8 +199,16 @@ def test_one_lattice_matches_oracle_at_1024(mods):
     (512, 3, 6, 1, 20, 1.0, 0.0, 1),    # cluster of 8 CTAs per lattice
     (2, 7, 50, 3, 5, 1.0, 0.0, 1),
     (6, 4, 25, 0, 6, 0.5, -0.5, 5),     # no exchanges
+    (8, 3, 9000, 1, 21, 1.0, 0.0, 50),  # > 4096 rounds: two segments of swap draws
+    (64, 4096, 8, 1, 22, 1.0, 0.0, 2),  # C5's shape: point-to-point rounds, 28 warp-owned lattices per CTA
 ])
-def test_resident_run_matches_oracle(mods, L, R, sweeps, every, seed, J, B, rec_every):
+@pytest.mark.parametrize("p2p", [None, "0"])
+def test_resident_run_matches_oracle(mods, monkeypatch, L, R, sweeps, every, seed, J, B, rec_every, p2p):
+    """The resident run against the oracle; warp-owned lattices decide their
+    rounds pairwise (point-to-point, default) or behind a grid barrier
+    (PTMH_RESIDENT_P2P=0)."""
+    if p2p is not None:
+        monkeypatch.setenv("PTMH_RESIDENT_P2P", p2p)
     p = mods[0]
     cfg = p.SimulationConfig(side=L, replicas=R, iterations=sweeps * L * L,
                              swap_interval=every * L * L, seed=seed,
