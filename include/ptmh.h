@@ -298,6 +298,27 @@ int ptmh_cb_run_resident_ws(uint32_t *packed, int64_t R, int64_t L,
                             int64_t record_every, int *buf_out, void *ws,
                             int64_t ws_bytes, void *stream);
 
+/* ptmh_cb_run_resident_sharded with the point-to-point rounds' workspace
+ * (ptmh_cb_resident_ws_bytes(R_total, n_rounds)): where lattices are
+ * warp-owned, every lattice stores its round word into every rank's
+ * slot_stats ring (NVLink peer stores) and waits for its partner slot's word
+ * only; flag_peers are then unused.  The rings must start zeroed for a run
+ * (ptmh_peer_alloc) and a run's rounds only grow. */
+int ptmh_cb_run_resident_sharded_ws(uint32_t *packed, int64_t rows, int64_t L,
+                                    int64_t *slot_to_row2, int32_t *row_to_slot2,
+                                    int buf, const uint32_t *thresh,
+                                    uint32_t always_mask, uint64_t seed, double J,
+                                    double B, const double *betas, int64_t *stats,
+                                    int64_t *slot_stats, int64_t *counters,
+                                    double *obs_e, double *obs_m, int64_t ncols,
+                                    int64_t first_sweep, int64_t n_sweeps,
+                                    int64_t total_sweeps, int64_t swap_every,
+                                    int64_t record_every, int *buf_out,
+                                    int64_t R_total, int rank, int world,
+                                    int64_t row_lo, int64_t *const *pub_peers,
+                                    uint32_t *const *flag_peers, int max_ctas,
+                                    void *ws, int64_t ws_bytes, void *stream);
+
 /* ptmh_cb_run_resident over `world` GPUs (one process each): this rank owns
  * the `rows` lattices of global rows row_lo .. row_lo + rows - 1; slots,
  * betas, thresholds, observables and slot_to_row2 (2, R_total) range over

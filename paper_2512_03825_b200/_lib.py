@@ -76,6 +76,9 @@ def _load():
         "ptmh_cb_resident_ws_bytes": ([i64, i64], i64),
         "ptmh_cb_run_resident_ws": ([P, i64, i64, P, P, i32, P, u32, u64, f64, f64, P, P, P, P, P,
                                      P, i64, i64, i64, i64, i64, i64, P, P, i64, P], i32),
+        "ptmh_cb_run_resident_sharded_ws": ([P, i64, i64, P, P, i32, P, u32, u64, f64, f64, P, P, P, P, P,
+                                             P, i64, i64, i64, i64, i64, i64, P, i64, i32, i32, i64, P, P,
+                                             i32, P, i64, P], i32),
         "ptmh_cb_run_resident_sharded": ([P, i64, i64, P, P, i32, P, u32, u64, f64, f64, P, P, P, P, P,
                                           P, i64, i64, i64, i64, i64, i64, P, i64, i32, i32, i64, P, P,
                                           i32, P], i32),

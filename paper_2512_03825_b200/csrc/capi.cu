@@ -394,11 +394,11 @@ static int run_resident_impl(uint32_t* packed, int64_t R, int64_t L, int64_t* sl
         if (swap_every > 0 && d % swap_every == 0 && d < total_sweeps) ++rounds;
     if (buf_out) *buf_out = buf ^ (rounds & 1);
     if (n_sweeps == 0) return PTMH_OK;
-    if (ws && world == 1 && swap_every > 0 && rounds > 0 && ws_bytes >= resident_ws_bytes(R, rounds) &&
-        R < (1LL << 24)) {
+    if (ws && swap_every > 0 && rounds > 0 && ws_bytes >= resident_ws_bytes(R_total, rounds) &&
+        R_total < (1LL << 24)) {
         a.u_table = static_cast<const double*>(ws);
         a.u_round0 = (first_sweep + swap_every) / swap_every - 1;  // the segment's first round
-        a.u_stride = R / 2 + 1;
+        a.u_stride = R_total / 2 + 1;
     }
     return launch_cb_resident(a, a.WR > 0, as_stream(stream), nullptr);
 }
@@ -426,6 +426,21 @@ int ptmh_cb_run_resident_ws(uint32_t* packed, int64_t R, int64_t L, int64_t* slo
                              stats, slot_stats, counters, obs_e, obs_m, ncols, first_sweep, n_sweeps, total_sweeps,
                              swap_every, record_every, buf_out, stream, R, 0, 1, 0, nullptr, nullptr, 0, ws,
                              ws_bytes);
+}
+
+int ptmh_cb_run_resident_sharded_ws(uint32_t* packed, int64_t rows, int64_t L, int64_t* slot_to_row2,
+                                    int32_t* row_to_slot2, int buf, const uint32_t* thresh, uint32_t always_mask,
+                                    uint64_t seed, double J, double B, const double* betas, int64_t* stats,
+                                    int64_t* slot_stats, int64_t* counters, double* obs_e, double* obs_m,
+                                    int64_t ncols, int64_t first_sweep, int64_t n_sweeps, int64_t total_sweeps,
+                                    int64_t swap_every, int64_t record_every, int* buf_out, int64_t R_total,
+                                    int rank, int world, int64_t row_lo, int64_t* const* pub_peers,
+                                    uint32_t* const* flag_peers, int max_ctas, void* ws, int64_t ws_bytes,
+                                    void* stream) {
+    return run_resident_impl(packed, rows, L, slot_to_row2, row_to_slot2, buf, thresh, always_mask, seed, J, B,
+                             betas, stats, slot_stats, counters, obs_e, obs_m, ncols, first_sweep, n_sweeps,
+                             total_sweeps, swap_every, record_every, buf_out, stream, R_total, rank, world, row_lo,
+                             pub_peers, flag_peers, max_ctas, ws, ws_bytes);
 }
 
 int ptmh_cb_run_resident_sharded(uint32_t* packed, int64_t rows, int64_t L, int64_t* slot_to_row2,

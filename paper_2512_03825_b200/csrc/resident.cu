@@ -554,6 +554,15 @@ __device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+// across GPUs (NVLink peer memory): system scope
+__device__ __forceinline__ void st_relaxed_sys_u64(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed_sys_u64(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
 
 __global__ void swap_draws_kernel(uint64_t seed, int64_t R, int64_t round0, int64_t n_rounds, int64_t stride,
                                   double* __restrict__ out) {
@@ -572,9 +581,14 @@ __global__ void __launch_bounds__(kThreads) cb_resident_p2p_kernel(ResidentArgs 
     constexpr bool kStrip = kFerro && kMode == kGatherRows;
     __shared__ uint32_t s_tie[kStrip ? kWarps : 1][3][2][32];
     const int lane = threadIdx.x & 31, wq = (int)threadIdx.x >> 5;
-    const int R = A.R, W = A.W;
-    const int lo = (int)((int64_t)R * blockIdx.x / gridDim.x);
-    const int hi = (int)((int64_t)R * (blockIdx.x + 1) / gridDim.x);
+    const int W = A.W;
+    // sharded (world > 1): this rank's A.R lattices, slots / pairs over R_total;
+    // every lattice publishes into every rank's ring (NVLink peer stores) and
+    // polls its own rank's ring
+    const bool multi = A.world > 1;
+    const int R = multi ? A.R_total : A.R;
+    const int lo = (int)((int64_t)A.R * blockIdx.x / gridDim.x);
+    const int hi = (int)((int64_t)A.R * (blockIdx.x + 1) / gridDim.x);
     if (wq >= hi - lo) return;  // no block-wide barrier below: spare warps leave
     const int row = lo + wq;
     const int wr_shift = (A.WR > 0 && (A.WR & (A.WR - 1)) == 0) ? __ffs(A.WR) - 1 : -1;
@@ -637,8 +651,15 @@ __global__ void __launch_bounds__(kThreads) cb_resident_p2p_kernel(ResidentArgs 
                 const int64_t round = done / A.swap_every - 1;
                 const int first = (int)(round % 2);
                 const int n_pairs = (R - first) / 2;
-                uint64_t* slot_word = ring + (round % kRing) * (int64_t)R;
-                st_relaxed_u64(slot_word + k, p2p_pack(S, Bd, round));
+                const int64_t ro = (round % kRing) * (int64_t)R;
+                uint64_t* slot_word = ring + ro;
+                const uint64_t mine = p2p_pack(S, Bd, round);
+                if (multi) {
+                    for (int g = 0; g < A.world; ++g)
+                        st_relaxed_sys_u64(reinterpret_cast<uint64_t*>(A.pub_peer[g]) + ro + k, mine);
+                } else {
+                    st_relaxed_u64(slot_word + k, mine);
+                }
                 if (k >= first && (k - first) / 2 < n_pairs) {
                     const int p = (k - first) / 2, i = first + 2 * p, j = i + 1, other = k == i ? j : i;
                     // everything that does not need the partner's energy, while its word travels
@@ -647,10 +668,10 @@ __global__ void __launch_bounds__(kThreads) cb_resident_p2p_kernel(ResidentArgs 
                     const uint32_t ot3 = kFerro ? __ldg(A.thresh + other * 10 + 8) : 0u;
                     const uint32_t ot4 = kFerro ? __ldg(A.thresh + other * 10 + 9) : 0u;
                     const uint64_t want = (uint64_t)((round & 0x7fff) | 0x8000);
-                    uint64_t v = ld_relaxed_u64(slot_word + other);
+                    uint64_t v = multi ? ld_relaxed_sys_u64(slot_word + other) : ld_relaxed_u64(slot_word + other);
                     while ((v & 0xffffull) != want) {
                         __nanosleep(64);
-                        v = ld_relaxed_u64(slot_word + other);
+                        v = multi ? ld_relaxed_sys_u64(slot_word + other) : ld_relaxed_u64(slot_word + other);
                     }
                     const int64_t So = p2p_field(v, 16), Bo = p2p_field(v, 40);
                     const int64_t Si = k == i ? S : So, Bi = k == i ? Bd : Bo;
@@ -698,7 +719,7 @@ __global__ void __launch_bounds__(kThreads) cb_resident_p2p_kernel(ResidentArgs 
     if (lane == 0) {
         const int fb = A.buf ^ (rounds & 1);
         A.r2s[fb][row] = k;
-        A.s2r[fb][k] = row;
+        A.s2r[fb][k] = A.row_lo + row;
     }
 }
 
@@ -751,9 +772,14 @@ static int launch_resident_t(const ResidentArgs& a, int sms, cudaStream_t s) {
     // point-to-point rounds (cb_resident_p2p_kernel): warp-owned lattices, one
     // per warp, one GPU, a swap-draw table; PTMH_RESIDENT_P2P=0 turns it off
     const char* ep = getenv("PTMH_RESIDENT_P2P");
-    if (cs == 1 && args.warp_lat && a.world == 1 && a.u_table && nl_max <= threads / 32 && a.L <= 1024 &&
+    if (cs == 1 && args.warp_lat && a.u_table && nl_max <= threads / 32 && a.L <= 1024 &&
         !(ep && ep[0] == '0')) {
-        if (a.swap_every > 0) PTMH_CUDA(cudaMemsetAsync(a.slot_stats, 0, (size_t)kRing * a.R * 8, s));
+        // one GPU: zero the ring (entries of an earlier launch could carry a
+        // matching stamp).  Across GPUs other ranks may already be storing
+        // into it: a run's ring starts zeroed (ptmh_peer_alloc) and its round
+        // indices only grow, so an older entry never matches
+        if (a.swap_every > 0 && a.world == 1)
+            PTMH_CUDA(cudaMemsetAsync(a.slot_stats, 0, (size_t)kRing * a.R * 8, s));
         PTMH_CUDA(cudaLaunchCooperativeKernel((const void*)cb_resident_p2p_kernel<kMode, kFerro, kThreads>, grid,
                                               threads, kargs, 0, s));
         return PTMH_OK;
@@ -811,7 +837,8 @@ int launch_cb_resident(const ResidentArgs& a_in, bool fast, cudaStream_t s, int*
         const int64_t last = std::min(a.first_sweep + a.n_sweeps, a.total_sweeps - 1);
         const int64_t n = a.u_stride * std::max<int64_t>(1, last / a.swap_every - a.u_round0);
         swap_draws_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, s>>>(
-            a.seed, a.R, a.u_round0, n / a.u_stride, a.u_stride, const_cast<double*>(a.u_table));
+            a.seed, a.world > 1 ? a.R_total : a.R, a.u_round0, n / a.u_stride, a.u_stride,
+            const_cast<double*>(a.u_table));
         PTMH_LAUNCH_CHECK();
     }
     const bool segs = !fast && a.L >= 8 && 64 % a.L == 0;

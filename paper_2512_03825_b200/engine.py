@@ -335,13 +335,21 @@ class CheckerboardEngine(_Base):
         flags = (ctypes.c_void_p * world)(*[int(x) for x in flag_peers])
         # (everything runs on the current stream: co-running ranks on one GPU
         # in the tests each use their own)
-        _lib.call("ptmh_cb_run_resident_sharded", _P(self.packed), self.rows, self.L, _P(self._s2r2_g),
+        # the point-to-point rounds' swap draws (csrc/resident.cu), when lattices are warp-owned
+        rounds = sum(1 for d in range(first_sweep + 1, first_sweep + n_sweeps + 1)
+                     if d % swap_every == 0 and d < total_sweeps) if swap_every > 0 else 0
+        need = int(_lib.LIB.ptmh_cb_resident_ws_bytes(self.R, rounds)) if rounds else 0
+        if need and (getattr(self, "_res_ws", None) is None or self._res_ws.numel() < need):
+            self._res_ws = torch.empty(need, dtype=torch.uint8, device=self.dev)
+        ws = self._res_ws if need else None
+        _lib.call("ptmh_cb_run_resident_sharded_ws", _P(self.packed), self.rows, self.L, _P(self._s2r2_g),
                   _P(self._r2s2_loc), 0, _P(self.thr), self.always, self.seed, self.J, self.B,
                   _P(self.betas), _P(self.local_stats),
                   slot_stats if isinstance(slot_stats, int) else _P(slot_stats), _P(self.counters), _P(obs_e),
                   _P(obs_m), ncols, first_sweep, n_sweeps, total_sweeps, swap_every, record_every,
                   ctypes.byref(out), self.R, rank, world, self.row_lo, ctypes.cast(pubs, ctypes.c_void_p),
-                  ctypes.cast(flags, ctypes.c_void_p), max_ctas, self._s())
+                  ctypes.cast(flags, ctypes.c_void_p), max_ctas, _P(ws), ws.numel() if ws is not None else 0,
+                  self._s())
         self.row_to_slot[self.row_lo:self.row_hi].copy_(self._r2s2_loc[out.value, :self.rows])
         self.slot_to_row.copy_(self._s2r2_g[out.value])
 

@@ -432,11 +432,16 @@ def _random_sharded_cases(n):
 
 @pytest.mark.parametrize("L,R,G,total,every,rec", [(64, 24, 2, 30, 1, 1), (64, 37, 3, 20, 2, 2),
                                                    (16, 40, 4, 25, 1, 5)] + _random_sharded_cases(6))
-def test_resident_sharded_virtual_ranks(mods, L, R, G, total, every, rec):
-    """The multi-GPU resident kernel (rounds exchanged through peer memory
-    and flags, no collective) with G ranks co-running on ONE GPU, each on its
-    own stream and a share of the SMs: after combining the ranks' parts it is
-    the single-GPU resident run, bit for bit."""
+@pytest.mark.parametrize("p2p", [None, "0"])
+def test_resident_sharded_virtual_ranks(mods, monkeypatch, L, R, G, total, every, rec, p2p):
+    """The multi-GPU resident kernel (rounds exchanged through peer memory, no
+    collective: pairwise round words where lattices are warp-owned, else
+    flags + grid barriers; PTMH_RESIDENT_P2P=0 forces the latter) with G ranks
+    co-running on ONE GPU, each on its own stream and a share of the SMs:
+    after combining the ranks' parts it is the single-GPU resident run, bit
+    for bit."""
+    if p2p is not None:
+        monkeypatch.setenv("PTMH_RESIDENT_P2P", p2p)
     p, engine, _, _ = mods
     from paper_2512_03825_b200.executor import assign_replicas
     temps, seed = p.build_ladder(R), 31
