@@ -114,6 +114,7 @@ struct ResidentArgs {
     uint32_t seg_lo, seg_even;  // L in {8, 16, 32}: bit 0 of each row segment, even-row segments
     int warp_lat;               // launcher-set: each warp owns whole lattices (no CTA barrier per colour)
     int strip;                  // launcher-set: warp-owned 64^2 ferro lattices use the strip code
+    int p2p;                    // launcher-set: cluster-owned lattices decide rounds pairwise (u_table)
     // Sharded across GPUs (world > 1): R above counts this rank's lattices
     // (global rows row_lo ..), slots and pairs range over R_total.  Each
     // round's (S, Bond) by slot goes to every rank's pub buffer (peer memory

@@ -189,6 +189,35 @@ __device__ __forceinline__ void resident_word(const ResidentArgs& A, uint32_t* o
 
 constexpr int kMaxLatPerBlock = 64;
 
+constexpr int kRing = 4;
+
+__device__ __forceinline__ uint64_t p2p_pack(int64_t S, int64_t Bd, int64_t round) {
+    const uint64_t st = (uint64_t)((round & 0x7fff) | 0x8000);
+    return st | (((uint64_t)S & 0xffffffull) << 16) | (((uint64_t)Bd & 0xffffffull) << 40);
+}
+__device__ __forceinline__ int64_t p2p_field(uint64_t v, int shift) {
+    return (int64_t)(((int64_t)(v << (40 - shift))) >> 40);  // sign-extended 24-bit field at `shift`
+}
+__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+// across GPUs (NVLink peer memory): system scope
+__device__ __forceinline__ void st_relaxed_sys_u64(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed_sys_u64(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+
+
 // lattice li of this block now holds `slot`: cache its slot and (ferro) the
 // threshold-plane select coefficients in shared memory
 template <bool kFerro>
@@ -223,9 +252,12 @@ __device__ __forceinline__ void resident_set_slot(const ResidentArgs& A, int li,
 // decides the exchange for its cluster's lattices redundantly (same inputs,
 // same rule); rank 0 alone writes the outputs.
 template <int kMode, bool kFerro, int kThreads, bool kCl>
-__global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
+__global__ void __launch_bounds__(kThreads, kThreads <= 256 ? 2 : 1) cb_resident_kernel(ResidentArgs A) {
     __shared__ int s_slot[kMaxLatPerBlock];
     __shared__ int s_S[kMaxLatPerBlock], s_B[kMaxLatPerBlock];
+    // point-to-point rounds on clusters: (S, Bond) accumulate in rank 0's
+    // buffer [t & 1], zeroed two sweeps after it was last read
+    __shared__ int s_Sc[kCl ? 2 : 1][kCl ? kMaxLatPerBlock : 1], s_Bc[kCl ? 2 : 1][kCl ? kMaxLatPerBlock : 1];
     __shared__ double s_u[kMaxLatPerBlock];
     __shared__ double s_bd[kMaxLatPerBlock];       // beta_i - beta_j of the slot's pair (this round)
     __shared__ uint32_t s_pt[kMaxLatPerBlock][2];  // thresholds t3, t4 of the partner slot (ferro)
@@ -273,11 +305,22 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
         cluster.sync();
     else
         __syncthreads();
+    const bool p2p = kCl && A.p2p;
+    int p2p_rounds = 0;
     for (int64_t t = A.first_sweep; t < A.first_sweep + A.n_sweeps; ++t) {
         const int64_t done = t + 1;
         const bool rec = A.record_every > 0 && done % A.record_every == 0;
         const bool exch = A.swap_every > 0 && done % A.swap_every == 0 && done < A.total_sweeps;
         const bool need_stats = rec || exch || t + 1 == A.first_sweep + A.n_sweeps;
+        if (p2p) {  // this sweep's accumulators (the colour-0 barrier orders this before the adds)
+            s_S0 = cluster.map_shared_rank(&s_Sc[t & 1][0], 0);
+            s_B0 = cluster.map_shared_rank(&s_Bc[t & 1][0], 0);
+            if (owner)
+                for (int i = threadIdx.x; i < nl; i += blockDim.x) {
+                    s_Sc[t & 1][i] = 0;
+                    s_Bc[t & 1][i] = 0;
+                }
+        }
         if (!kCl && A.warp_lat) {
             // warp-owned lattices: warp q sweeps lattices q, q + nwarps, ...
             // whole (both colours, lanes striding over the words), so the
@@ -374,6 +417,86 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
                 __syncthreads();
         }
         if (!need_stats) continue;
+        if (p2p) {
+            // Point-to-point round (cb_resident_p2p_kernel's scheme for
+            // cluster-owned lattices): rank 0 publishes each lattice's round
+            // word; every CTA of the cluster polls the partner slot's word and
+            // decides the pair redundantly (same inputs, same rule), so only
+            // the partner is waited for, not the grid.
+            const int64_t round = exch ? done / A.swap_every - 1 : 0;
+            const int first = (int)(round % 2);
+            const int n_pairs = (R - first) / 2;
+            uint64_t* ring = reinterpret_cast<uint64_t*>(A.slot_stats) + (round % kRing) * (int64_t)R;
+            for (int i = threadIdx.x; i < nl; i += blockDim.x) {
+                const int64_t S = s_S0[i], Bd = s_B0[i];  // rank 0's sums (complete after the colour-1 barrier)
+                const int k = s_slot[i];
+                if (!owner) continue;
+                if (t + 1 == A.first_sweep + A.n_sweeps) {
+                    A.stats[2 * (lo + i)] = S;
+                    A.stats[2 * (lo + i) + 1] = Bd;
+                }
+                if (rec) {
+                    const int64_t col = done / A.record_every - 1;
+                    A.obs_e[(int64_t)k * A.ncols + col] =
+                        __dsub_rn(__dmul_rn(A.B, (double)S), __dmul_rn(A.J, (double)Bd));
+                    A.obs_m[(int64_t)k * A.ncols + col] = __ddiv_rn((double)S, (double)A.L * A.L);
+                }
+                if (exch) st_relaxed_u64(ring + k, p2p_pack(S, Bd, round));
+            }
+            if (!exch) continue;
+            ++p2p_rounds;
+            for (int i = threadIdx.x; i < nl; i += blockDim.x) {
+                const int k = s_slot[i];
+                if (k < first || (k - first) / 2 >= n_pairs) continue;
+                const int p = (k - first) / 2, si = first + 2 * p, sj = si + 1, other = k == si ? sj : si;
+                const double u = A.u_table[(round - A.u_round0) * A.u_stride + p];
+                const double bd = __dsub_rn(A.betas[si], A.betas[sj]);
+                const uint32_t ot3 = kFerro ? __ldg(A.thresh + other * 10 + 8) : 0u;
+                const uint32_t ot4 = kFerro ? __ldg(A.thresh + other * 10 + 9) : 0u;
+                const int64_t S = s_S0[i], Bd = s_B0[i];
+                const uint64_t want = (uint64_t)((round & 0x7fff) | 0x8000);
+                uint64_t v = ld_relaxed_u64(ring + other);
+                while ((v & 0xffffull) != want) {
+                    __nanosleep(64);
+                    v = ld_relaxed_u64(ring + other);
+                }
+                const int64_t So = p2p_field(v, 16), Bo = p2p_field(v, 40);
+                const double Ei = __dsub_rn(__dmul_rn(A.B, (double)(k == si ? S : So)),
+                                            __dmul_rn(A.J, (double)(k == si ? Bd : Bo)));
+                const double Ej = __dsub_rn(__dmul_rn(A.B, (double)(k == si ? So : S)),
+                                            __dmul_rn(A.J, (double)(k == si ? Bo : Bd)));
+                const double x = __dmul_rn(bd, __dsub_rn(Ei, Ej));
+                double prob;
+                if (x >= 0.0) {
+                    prob = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-x)));
+                } else {
+                    const double ex = exp(x);
+                    prob = __ddiv_rn(ex, __dadd_rn(1.0, ex));
+                }
+                const bool acc = u < prob;
+                if (k == si && owner) {
+                    if (acc) atomicAdd((unsigned long long*)&A.counters[0], 1ull);
+                    if (fabs(u - prob) <= 4.0 * 2.220446049250313e-16 * fmax(prob, 2.2250738585072014e-308))
+                        atomicAdd((unsigned long long*)&A.counters[1], 1ull);
+                }
+                if (acc) {
+                    s_slot[i] = other;
+                    if (kFerro) {
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const uint32_t ta = (ot3 >> (31 - q)) & 1u, tb = (ot4 >> (31 - q)) & 1u;
+                            s_mask[i][q] = tb - ta;
+                            s_mask[i][8 + q] = 0u - ta;
+                        }
+                        s_mask[i][16] = ot3;
+                        s_mask[i][17] = ot4;
+                        s_mask[i][18] = (uint32_t)other;
+                    }
+                }
+            }
+            __syncthreads();  // next sweep reads s_slot / s_mask
+            continue;
+        }
         // publish (S, Bond); zero the accumulators for the next stats sweep
         // (the colour-0 barrier separates this from the next accumulation)
         const int64_t round = exch ? done / A.swap_every - 1 : 0;
@@ -511,6 +634,13 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
         buf ^= 1;
         __syncthreads();  // next sweep reads s_slot / s_mask
     }
+    if (p2p && owner) {  // the final mapping, where the grid-barrier rounds would leave it
+        const int fb = A.buf ^ (p2p_rounds & 1);
+        for (int i = threadIdx.x; i < nl; i += blockDim.x) {
+            A.r2s[fb][lo + i] = s_slot[i];
+            A.s2r[fb][s_slot[i]] = A.row_lo + lo + i;
+        }
+    }
 }
 
 // ------------------------------------------- point-to-point exchange rounds --
@@ -537,33 +667,6 @@ __global__ void __launch_bounds__(kThreads) cb_resident_kernel(ResidentArgs A) {
 // The swap draws (stream R+p, position = round; rng.py:113-116) come from a
 // table the launcher fills before the launch (swap_draws_kernel): a
 // Philox4x64-10 chain per round and lattice stays off the warps' path.
-constexpr int kRing = 4;
-
-__device__ __forceinline__ uint64_t p2p_pack(int64_t S, int64_t Bd, int64_t round) {
-    const uint64_t st = (uint64_t)((round & 0x7fff) | 0x8000);
-    return st | (((uint64_t)S & 0xffffffull) << 16) | (((uint64_t)Bd & 0xffffffull) << 40);
-}
-__device__ __forceinline__ int64_t p2p_field(uint64_t v, int shift) {
-    return (int64_t)(((int64_t)(v << (40 - shift))) >> 40);  // sign-extended 24-bit field at `shift`
-}
-__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
-    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
-    uint64_t v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-// across GPUs (NVLink peer memory): system scope
-__device__ __forceinline__ void st_relaxed_sys_u64(uint64_t* p, uint64_t v) {
-    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ uint64_t ld_relaxed_sys_u64(const uint64_t* p) {
-    uint64_t v;
-    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
 __global__ void swap_draws_kernel(uint64_t seed, int64_t R, int64_t round0, int64_t n_rounds, int64_t stride,
                                   double* __restrict__ out) {
     const int64_t n = n_rounds * stride;
@@ -789,6 +892,10 @@ static int launch_resident_t(const ResidentArgs& a, int sms, cudaStream_t s) {
                                               threads, kargs, 0, s));
         return PTMH_OK;
     }
+    if (a.u_table && a.world == 1 && a.L <= 1024 && !(ep && ep[0] == '0')) {
+        args.p2p = 1;  // cluster-owned lattices: point-to-point rounds
+        if (a.swap_every > 0) PTMH_CUDA(cudaMemsetAsync(a.slot_stats, 0, (size_t)kRing * a.R * 8, s));
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3((unsigned)threads);
@@ -802,7 +909,11 @@ static int launch_resident_t(const ResidentArgs& a, int sms, cudaStream_t s) {
     attr[1].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    PTMH_CUDA(cudaLaunchKernelExC(&cfg, (const void*)cb_resident_kernel<kMode, kFerro, kThreads, true>, kargs));
+    // cluster CTAs of <= 256 threads (C2): the 256-thread build (<= 128
+    // registers, two CTAs per SM) instead of the 64-register 1024-thread one
+    const void* fn = threads <= 256 ? (const void*)cb_resident_kernel<kMode, kFerro, 256, true>
+                                    : (const void*)cb_resident_kernel<kMode, kFerro, kThreads, true>;
+    PTMH_CUDA(cudaLaunchKernelExC(&cfg, fn, kargs));
     return PTMH_OK;
 }
 
