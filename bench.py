@@ -415,7 +415,7 @@ def main():
         sweep_ms = [m for m in sweep_ms if m > 0]
         launch_ms = statistics.mean(sweep_ms)
         bytes_per_launch = ALG_BYTES_PER_ATTEMPT * local_rows * L * L * every * ips
-        kernel_name = "cb_resident_kernel<fast,ferro>"
+        kernel_name = launched["name"]
     elif persistent:  # one launch per interval: all 2*every half-sweeps
         launch_ms = statistics.mean(sweep_ms)
         bytes_per_launch = ALG_BYTES_PER_ATTEMPT * local_rows * L * L * every

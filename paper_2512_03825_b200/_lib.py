@@ -117,7 +117,10 @@ def cb_last_launch() -> dict:
     v = (ctypes.c_int32 * 6)()
     call("ptmh_cb_last_launch", v)
     kinds = {0: None, 1: "cb_sweeps_persistent<{r},{t}>", 2: "cb_half_sweep_ferro<{r},0|1>",
-             3: "cb_half_sweep_fast<{r}>", 4: "cb_half_sweep_generic"}
+             3: "cb_half_sweep_fast<{r}>", 4: "cb_half_sweep_generic",
+             5: "cb_resident_kernel (clusters of {r}, grid-barrier rounds)",
+             6: "cb_resident_p2p_kernel (warp-owned lattices, point-to-point rounds)",
+             7: "cb_resident_kernel (clusters of {r}, point-to-point rounds)"}
     k = kinds.get(v[0])
     return {"kind": v[0], "rows": v[1], "threads": v[2], "group": v[3], "bands": bool(v[4]),
             "grid": v[5], "name": k.format(r=v[1], t=v[2]) if k else None}

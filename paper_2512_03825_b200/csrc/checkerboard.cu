@@ -722,6 +722,7 @@ bool cb_sweeps_persistent_applies(int64_t L, uint32_t always_mask, int64_t n_swe
 // tests assert the headline path, bench.py names the kernel it timed)
 static thread_local CbLaunchInfo g_last_launch = {};
 CbLaunchInfo cb_last_launch() { return g_last_launch; }
+void cb_set_last_launch(const CbLaunchInfo& info) { g_last_launch = info; }
 
 int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* row_to_slot,
                      const uint32_t* thresh, uint32_t always_mask, uint64_t seed, int64_t first_sweep,

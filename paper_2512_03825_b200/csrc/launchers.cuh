@@ -72,11 +72,15 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
                      const uint32_t* thresh, uint32_t always_mask, uint64_t seed, int64_t first_sweep,
                      int64_t n_sweeps, int64_t* stats, cudaStream_t s, uint32_t* sync = nullptr);
 // kind: 0 none, 1 cb_sweeps_persistent<rows, threads>, 2 cb_half_sweep_ferro<rows>,
-// 3 cb_half_sweep_fast, 4 cb_half_sweep_generic
+// 3 cb_half_sweep_fast, 4 cb_half_sweep_generic; resident runs (resident.cu):
+// 5 cb_resident_kernel (grid-barrier rounds; rows = cluster size),
+// 6 cb_resident_p2p_kernel (warp-owned lattices), 7 cb_resident_kernel on
+// clusters with point-to-point rounds
 struct CbLaunchInfo {
     int kind, rows, threads, group, bands, grid;
 };
 CbLaunchInfo cb_last_launch();
+void cb_set_last_launch(const CbLaunchInfo& info);
 bool cb_sweeps_persistent_applies(int64_t L, uint32_t always_mask, int64_t n_sweeps);
 int launch_cb_pack(const int8_t* spins, int64_t rows, int64_t L, uint32_t* packed, cudaStream_t s);
 int launch_cb_unpack(const uint32_t* packed, int64_t rows, int64_t L, int8_t* spins, cudaStream_t s);

@@ -885,11 +885,13 @@ static int launch_resident_t(const ResidentArgs& a, int sms, cudaStream_t s) {
             PTMH_CUDA(cudaMemsetAsync(a.slot_stats, 0, (size_t)kRing * a.R * 8, s));
         PTMH_CUDA(cudaLaunchCooperativeKernel((const void*)cb_resident_p2p_kernel<kMode, kFerro, kThreads>, grid,
                                               threads, kargs, 0, s));
+        cb_set_last_launch(CbLaunchInfo{6, 1, threads, 1, 0, grid});
         return PTMH_OK;
     }
     if (cs == 1) {
         PTMH_CUDA(cudaLaunchCooperativeKernel((const void*)cb_resident_kernel<kMode, kFerro, kThreads, false>, grid,
                                               threads, kargs, 0, s));
+        cb_set_last_launch(CbLaunchInfo{5, 1, threads, 1, 0, grid});
         return PTMH_OK;
     }
     if (a.u_table && a.world == 1 && a.L <= 1024 && !(ep && ep[0] == '0')) {
@@ -914,6 +916,7 @@ static int launch_resident_t(const ResidentArgs& a, int sms, cudaStream_t s) {
     const void* fn = threads <= 256 ? (const void*)cb_resident_kernel<kMode, kFerro, 256, true>
                                     : (const void*)cb_resident_kernel<kMode, kFerro, kThreads, true>;
     PTMH_CUDA(cudaLaunchKernelExC(&cfg, fn, kargs));
+    cb_set_last_launch(CbLaunchInfo{args.p2p ? 7 : 5, cs, threads, 1, 0, grid});
     return PTMH_OK;
 }
 
