@@ -11,3 +11,8 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
 ncu --set full --clock-control none --import-source on -k regex:cb_sweeps_persistent -c 1 \
     -o gpurun_out/persist_c3 -f python tools/prof_sweep.py c3 10 > gpurun_out/ncu_full.log 2>&1
 tail -n 1 gpurun_out/bench_*.log
+# the resident kernels (C5: warp-owned lattices, C2: clusters), 20 sweeps with a round every sweep
+ncu --set full --clock-control none --import-source on -k regex:cb_resident -c 1 -o gpurun_out/res_c5 -f \
+    python tools/prof_resident.py c5 1 > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:cb_resident -c 1 -o gpurun_out/res_c2 -f \
+    python tools/prof_resident.py c2 1 > /dev/null 2>&1
