@@ -4,14 +4,16 @@
         --swap-interval I --workers W --seed S --J J --B B --init-up F
         --preset desk|paper-small|paper-full --sweep KIND --axis a,b,c
         --reps K --out DIR --record none|observables|full --config FILE.json
-        --sweep-mode exact|checkerboard --record-every K --device D]
+        --sweep-mode exact|checkerboard --record-every K --device D | --devices 0,1,...]
 
 Same flags, precedence (flags > JSON config > preset), presets, sweep kinds,
 seed derivation, output files and exit codes as `isingpt` (ref:cli.py:1-411):
 timings.csv, observables.csv / observables-<point>-rep<k>.csv, states*.npz
 and summary.json, exit 0 / 1 (usage) / 2 (a failed row).  The three flags
 after --config are extensions: the chain (the reference's, default, or the
-checkerboard sweep), the checkerboard sampling stride and the GPU.
+checkerboard sweep), the checkerboard sampling stride and the GPU; --devices
+runs every point on several GPUs, one process per GPU (launch the CLI under
+torchrun --nproc-per-node len(devices); rank 0 writes the output files).
 """
 
 from __future__ import annotations
@@ -45,7 +47,7 @@ DEFAULT_AXES = {"single": (), "worker_scaling": (1, 2, 4, 8),
                 "replica_scaling": (16, 32, 64, 128), "swap_sweep": (0, 100, 1000, 10000),
                 "size_sweep": (8, 12, 16, 24, 32)}
 SETTINGS = ("size", "replicas", "iters", "swap_interval", "workers", "seed", "J", "B", "init_up")
-EXTENSIONS = ("sweep_mode", "record_every", "device")
+EXTENSIONS = ("sweep_mode", "record_every", "device", "devices")
 FILE_KEYS = SETTINGS + ("preset", "sweep", "axis", "reps", "out", "record") + EXTENSIONS
 TIMINGS_COLUMNS = ("sweep_point", "rep", "workers", "replicas", "L", "iters", "swap_interval",
                    "seed", "init_s", "exec_s", "total_s", "swaps_attempted", "swaps_accepted",
@@ -122,7 +124,19 @@ def _parser() -> _ArgParser:
     p.add_argument("--record", choices=sorted(RECORD_CHOICES))
     p.add_argument("--config")
     p.add_argument("--sweep-mode", choices=SWEEP_MODES, dest="sweep_mode")
+    p.add_argument("--devices")
     return p
+
+
+def _devices(v) -> tuple | None:
+    """--devices 0,1,2 (or a JSON list) -> (0, 1, 2)."""
+    if v is None:
+        return None
+    try:
+        items = v.split(",") if isinstance(v, str) else list(v)
+        return tuple(int(x) for x in items if str(x).strip() != "")
+    except (TypeError, ValueError) as exc:
+        raise UsageError(f"devices must be comma-separated GPU indices, got {v!r}") from exc
 
 
 def derive_seed(master_seed: int, point_id: str, rep: int) -> int:
@@ -195,7 +209,7 @@ def parse_config(argv: list[str] | None = None) -> SweepSpec:
             init_up_fraction=float(setting["init_up"]), record_mode=RECORD_CHOICES[record],
             sweep_mode=_pick(ns, cfg, "sweep_mode", "exact"),
             record_every=int(_pick(ns, cfg, "record_every", 1)),
-            device=_pick(ns, cfg, "device"))
+            device=_pick(ns, cfg, "device"), devices=_devices(_pick(ns, cfg, "devices")))
         base.validate()
     except (ConfigurationError, ValueError) as exc:
         raise UsageError(str(exc)) from exc
@@ -268,10 +282,39 @@ def _summary(spec: SweepSpec, rows: list[TimingRow]) -> dict:
     return {"sweep": spec.kind, "baseline": baseline, "points": pts}
 
 
+def _join_devices(spec: SweepSpec) -> int:
+    """--devices with several GPUs: this process is one rank of a torchrun
+    launch (RANK / LOCAL_RANK / WORLD_SIZE from the environment); joins the
+    NCCL process group every run() of the sweep shards over.  Returns the
+    rank (0 without --devices or with one device)."""
+    devs = spec.base.devices
+    if devs is None or len(devs) == 1:
+        return 0
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    if not dist.is_initialized():
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        if world != len(devs):
+            raise UsageError(f"--devices names {len(devs)} GPUs: launch with torchrun --nproc-per-node "
+                             f"{len(devs)} (WORLD_SIZE is {world})")
+        rank = int(os.environ["RANK"])
+        torch.cuda.set_device(devs[rank])
+        dist.init_process_group("nccl", device_id=torch.device("cuda", devs[rank]))
+    torch.cuda.set_device(devs[dist.get_rank()])
+    return dist.get_rank()
+
+
 def run_sweep(spec: SweepSpec) -> int:
     """Every point x repetition, sequentially; failures become rows and the
-    sweep goes on; exit 2 if any row failed (ref:cli.py:314-368)."""
-    spec.out_dir.mkdir(parents=True, exist_ok=True)
+    sweep goes on; exit 2 if any row failed (ref:cli.py:314-368).  With
+    several --devices every rank runs every point; rank 0 writes the files."""
+    rank = _join_devices(spec)
+    writer = rank == 0
+    if writer:
+        spec.out_dir.mkdir(parents=True, exist_ok=True)
     from .kernels import warm_kernels
 
     warm_kernels()  # CUDA context + module load outside the timed runs
@@ -297,14 +340,17 @@ def run_sweep(spec: SweepSpec) -> int:
                                   rec.total_seconds if rec else 0.0,
                                   rec.swaps_attempted if rec else 0,
                                   rec.swaps_accepted if rec else 0, status))
-            print(f"[b200] {point_id} rep {rep}: {status}"
-                  + (f" total {rec.total_seconds:.3f}s" if rec else ""), file=sys.stderr)
-            if rec is not None and rec.valid and spec.record_mode != "none":
+            if writer:
+                print(f"[b200] {point_id} rep {rep}: {status}"
+                      + (f" total {rec.total_seconds:.3f}s" if rec else ""), file=sys.stderr)
+            if writer and rec is not None and rec.valid and spec.record_mode != "none":
                 suffix = "" if one_file else f"-{point_id}-rep{rep}"
                 write_observables(spec.out_dir / f"observables{suffix}.csv", rec)
                 if rec.states is not None:
                     np.savez_compressed(spec.out_dir / f"states{suffix}.npz", states=rec.states,
                                         temperatures=rec.temperatures)
+    if not writer:
+        return 0 if all(r.status == "ok" for r in rows) else 2
     (spec.out_dir / "timings.csv").write_text(
         ",".join(TIMINGS_COLUMNS) + "\n" + "".join(r.to_csv() + "\n" for r in rows))
     (spec.out_dir / "summary.json").write_text(json.dumps(_summary(spec, rows), indent=2) + "\n")
@@ -318,7 +364,11 @@ def main(argv: list[str] | None = None) -> int:
         print(f"paper_2512_03825_b200: error: {exc}", file=sys.stderr)
         return 1
     t0 = time.perf_counter()
-    code = run_sweep(spec)
+    try:
+        code = run_sweep(spec)
+    except UsageError as exc:
+        print(f"paper_2512_03825_b200: error: {exc}", file=sys.stderr)
+        return 1
     print(f"[b200] sweep finished in {time.perf_counter() - t0:.1f}s, outputs in {spec.out_dir}",
           file=sys.stderr)
     return code

@@ -41,10 +41,30 @@ def test_precedence_flags_over_file_over_preset(tmp_path):
     ["--bogus"], ["--size", "1"], ["--sweep", "size_sweep", "--axis", "8,1"],
     ["--sweep", "replica_scaling", "--axis", "a,b"], ["--reps", "0"], ["--config", "/nope.json"],
     ["--sweep", "swap_sweep", "--axis", ""], ["--sweep-mode", "checkerboard", "--size", "7"],
+    ["--devices", "a,b"], ["--devices", "0,0", "--sweep-mode", "checkerboard", "--iters", "1024",
+                           "--swap-interval", "64"],
 ])
 def test_usage_errors_exit_1(argv, capsys):
     assert cli.main(argv) == 1
     assert "error" in capsys.readouterr().err
+
+
+def test_devices_flag_and_file_key(tmp_path):
+    spec = cli.parse_config(["--devices", "0,1", "--sweep-mode", "checkerboard", "--iters", "1024",
+                             "--swap-interval", "64", "--size", "8"])
+    assert spec.base.devices == (0, 1)
+    f = tmp_path / "c.json"
+    f.write_text(json.dumps({"size": 8, "iters": 1024, "swap_interval": 64, "sweep_mode": "checkerboard",
+                             "devices": [2, 3, 4]}))
+    assert cli.parse_config(["--config", str(f)]).base.devices == (2, 3, 4)
+
+
+def test_devices_without_torchrun_is_a_usage_error(tmp_path, monkeypatch, capsys):
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    argv = ["--devices", "0,1", "--sweep-mode", "checkerboard", "--iters", "1024", "--swap-interval", "64",
+            "--size", "8", "--out", str(tmp_path)]
+    assert cli.main(argv) == 1
+    assert "torchrun --nproc-per-node 2" in capsys.readouterr().err
 
 
 def test_unknown_config_key(tmp_path):
@@ -99,6 +119,15 @@ def test_cli_outputs_match_reference_cli(tmp_path, name):
     hdr = rows[0].split(",")
     keep = [i for i, c in enumerate(hdr) if c not in ("init_s", "exec_s", "total_s")]
     assert [",".join(r.split(",")[i] for i in keep) for r in rows] == case["timings_stable"]
+
+
+@pytest.mark.gpu
+def test_cli_devices_world1_equals_single_device(tmp_path):
+    argv = ["--size", "64", "--replicas", "6", "--iters", str(20 * 4096), "--swap-interval", "8192",
+            "--sweep-mode", "checkerboard", "--seed", "5"]
+    assert cli.main(argv + ["--out", str(tmp_path / "a")]) == 0
+    assert cli.main(argv + ["--devices", "0", "--out", str(tmp_path / "b")]) == 0
+    assert (tmp_path / "a" / "observables.csv").read_bytes() == (tmp_path / "b" / "observables.csv").read_bytes()
 
 
 @pytest.mark.gpu
