@@ -142,7 +142,9 @@ int ptmh_fill_lattices_parallel(int8_t *spins, int64_t rows, int64_t L,
  * 2 cb_half_sweep_ferro<rows>, 3 cb_half_sweep_fast, 4 cb_half_sweep_generic;
  * after a resident run: 5 cb_resident_kernel with grid-barrier rounds, 6
  * cb_resident_p2p_kernel, 7 cb_resident_kernel on clusters with
- * point-to-point rounds; info[1] = cluster size there),
+ * point-to-point rounds; info[1] = cluster size there; 8
+ * cb_cluster_smem_kernel, lattices in the shared memory of clusters of
+ * info[3] CTAs, info[1] = strip rows),
  * info[1] = rows per thread, [2] = threads per item / CTA, [3] = blocks per
  * item (group), [4] = band dependencies, [5] = grid (persistent only). */
 int ptmh_cb_last_launch(int32_t *info);

@@ -23,6 +23,7 @@
 #include "common.cuh"
 #include "launchers.cuh"
 #include "philox.cuh"
+#include "rounds.cuh"
 #include "strip.cuh"
 
 namespace cg = cooperative_groups;
@@ -188,35 +189,6 @@ __device__ __forceinline__ void resident_word(const ResidentArgs& A, uint32_t* o
 }
 
 constexpr int kMaxLatPerBlock = 64;
-
-constexpr int kRing = 4;
-
-__device__ __forceinline__ uint64_t p2p_pack(int64_t S, int64_t Bd, int64_t round) {
-    const uint64_t st = (uint64_t)((round & 0x7fff) | 0x8000);
-    return st | (((uint64_t)S & 0xffffffull) << 16) | (((uint64_t)Bd & 0xffffffull) << 40);
-}
-__device__ __forceinline__ int64_t p2p_field(uint64_t v, int shift) {
-    return (int64_t)(((int64_t)(v << (40 - shift))) >> 40);  // sign-extended 24-bit field at `shift`
-}
-__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
-    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
-    uint64_t v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-// across GPUs (NVLink peer memory): system scope
-__device__ __forceinline__ void st_relaxed_sys_u64(uint64_t* p, uint64_t v) {
-    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ uint64_t ld_relaxed_sys_u64(const uint64_t* p) {
-    uint64_t v;
-    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
-
 
 // lattice li of this block now holds `slot`: cache its slot and (ferro) the
 // threshold-plane select coefficients in shared memory
@@ -964,6 +936,10 @@ int launch_cb_resident(const ResidentArgs& a_in, bool fast, cudaStream_t s, int*
             a.seg_lo |= 1u << b;
             if (((b / seg) & 1) == 0) a.seg_even |= (seg == 32 ? 0xffffffffu : ((1u << seg) - 1u)) << b;
         }
+    }
+    if (fast && a.ferro) {  // cluster-owned lattices held in shared memory (resident_smem.cu)
+        const int rc = launch_cb_cluster_smem(a, s);
+        if (rc != 1) return rc;
     }
     if (fast)
         return a.ferro ? launch_resident_sized<kGatherRows, true>(a, s)

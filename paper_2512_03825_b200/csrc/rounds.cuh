@@ -1,0 +1,54 @@
+// rounds.cuh -- the point-to-point exchange-round words shared by the
+// resident kernels (resident.cu, resident_smem.cu): one 64-bit (S, Bond,
+// round stamp) word per slot in a kRing-deep ring, stored and polled with
+// relaxed accesses (gpu scope on one GPU, system scope across GPUs).
+#pragma once
+#include <cstdint>
+
+namespace ptmh {
+
+constexpr int kRing = 4;
+
+__device__ __forceinline__ uint64_t p2p_pack(int64_t S, int64_t Bd, int64_t round) {
+    const uint64_t st = (uint64_t)((round & 0x7fff) | 0x8000);
+    return st | (((uint64_t)S & 0xffffffull) << 16) | (((uint64_t)Bd & 0xffffffull) << 40);
+}
+__device__ __forceinline__ int64_t p2p_field(uint64_t v, int shift) {
+    return (int64_t)(((int64_t)(v << (40 - shift))) >> 40);  // sign-extended 24-bit field at `shift`
+}
+__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+// across GPUs (NVLink peer memory): system scope
+__device__ __forceinline__ void st_relaxed_sys_u64(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed_sys_u64(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// The reference exchange rule for one pair (kernels.py:116-148): x =
+// (beta_i - beta_j) * (E_i - E_j), p = logistic(x) evaluated on the stable
+// side, accept iff u < p.  near: |u - p| within 4 ulp of p, where a last-ulp
+// difference between the device exp and glibc's could flip the decision.
+__device__ __forceinline__ bool swap_decide(double bd, double Ei, double Ej, double u, bool& near) {
+    const double x = __dmul_rn(bd, __dsub_rn(Ei, Ej));
+    double prob;
+    if (x >= 0.0) {
+        prob = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-x)));
+    } else {
+        const double ex = exp(x);
+        prob = __ddiv_rn(ex, __dadd_rn(1.0, ex));
+    }
+    near = fabs(u - prob) <= 4.0 * 2.220446049250313e-16 * fmax(prob, 2.2250738585072014e-308);
+    return u < prob;
+}
+
+}  // namespace ptmh

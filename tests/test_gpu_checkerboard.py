@@ -274,6 +274,46 @@ def test_resident_cluster_sizes(mods, monkeypatch, cluster):
     assert rec.swaps_accepted == ref.swaps_accepted
 
 
+@pytest.mark.parametrize("L,R,sweeps,every,rec_every,cfg", [
+    (256, 5, 8, 1, 2, None),         # automatic cluster size (C2's lattice)
+    (256, 64, 6, 1, 3, None),        # C2's shape: 2-CTA clusters
+    (256, 6, 7, 1, 1, "2,2,256"),
+    (256, 3, 5, 2, 5, "1,2,256"),    # whole lattice in one CTA: halos wrap onto itself
+    (256, 4, 6, 1, 2, "4,1,256"),
+    (256, 4, 6, 3, 2, "2,4,128"),
+    (256, 4, 4, 1, 1, "2,1,512"),
+    (256, 4, 4, 1, 1, "8,2,128"),
+    (128, 9, 9, 1, 3, "2,2,128"),
+    (512, 3, 4, 1, 2, "8,2,128"),
+    (512, 2, 3, 1, 3, "16,2,128"),   # non-portable cluster size
+    (192, 4, 5, 1, 1, "1,1,256"),    # L/64 = 3 words per row
+    (320, 3, 4, 2, 2, "5,2,256"),    # odd cluster size, 64-row bands
+    (256, 7, 6, 0, 2, None),         # no exchanges
+])
+def test_cluster_smem_kernel_matches_oracle(mods, monkeypatch, L, R, sweeps, every, rec_every, cfg):
+    """cb_cluster_smem_kernel (lattices in the shared memory of thread-block
+    clusters, halos over DSMEM, point-to-point rounds) against the oracle,
+    over cluster sizes, strip heights and CTA widths."""
+    if cfg is not None:
+        monkeypatch.setenv("PTMH_RESIDENT_SMEM", cfg)
+    p = mods[0]
+    from paper_2512_03825_b200 import _lib
+    seed = 1000 + L + R
+    cfg_run = p.SimulationConfig(side=L, replicas=R, iterations=sweeps * L * L, swap_interval=every * L * L,
+                                 seed=seed, sweep_mode="checkerboard", record_every=rec_every,
+                                 return_final_state=True, kernel="resident")
+    rec = p.run(cfg_run)
+    assert rec.valid, rec.error
+    assert _lib.cb_last_launch()["kind"] == 8
+    ref = oracle.run_checkerboard(L, R, sweeps, every, seed, record_every=rec_every)
+    assert np.array_equal(rec.final_spins, ref.final_spins)
+    assert np.array_equal(rec.slot_to_row, ref.slot_to_row)
+    assert np.array_equal(rec.energies, ref.energies)
+    assert np.array_equal(rec.magnetizations, ref.magnetizations)
+    assert (rec.swap_rounds, rec.swaps_attempted, rec.swaps_accepted) == \
+        (ref.swap_rounds, ref.swaps_attempted, ref.swaps_accepted)
+
+
 def test_resident_segments_compose(mods):
     """Two resident segments == one resident run == the sweep-kernel path."""
     p, engine, _, _ = mods
@@ -431,7 +471,9 @@ def _random_sharded_cases(n):
 
 
 @pytest.mark.parametrize("L,R,G,total,every,rec", [(64, 24, 2, 30, 1, 1), (64, 37, 3, 20, 2, 2),
-                                                   (16, 40, 4, 25, 1, 5)] + _random_sharded_cases(6))
+                                                   (16, 40, 4, 25, 1, 5),
+                                                   (256, 6, 2, 8, 1, 2),   # shared-memory clusters
+                                                   (128, 9, 3, 7, 2, 1)] + _random_sharded_cases(6))
 @pytest.mark.parametrize("p2p", [None, "0"])
 def test_resident_sharded_virtual_ranks(mods, monkeypatch, L, R, G, total, every, rec, p2p):
     """The multi-GPU resident kernel (rounds exchanged through peer memory, no
