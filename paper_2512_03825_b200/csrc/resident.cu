@@ -706,13 +706,23 @@ __global__ void __launch_bounds__(kThreads) cb_resident_p2p_kernel(ResidentArgs 
             __syncwarp();  // the colour's words are stored before the other colour reads them
         }
         if (!need_stats) continue;
-        for (int o = 16; o > 0; o >>= 1) {
-            sS += __shfl_down_sync(0xffffffffu, sS, o);
-            sB += __shfl_down_sync(0xffffffffu, sB, o);
-        }
+        sS = __reduce_add_sync(0xffffffffu, sS);
+        sB = __reduce_add_sync(0xffffffffu, sB);
         int nk = k;
         if (lane == 0) {
             const int64_t S = sS, Bd = sB;
+            const int64_t round = exch ? done / A.swap_every - 1 : 0;
+            uint64_t* const slot_word = ring + (round % kRing) * (int64_t)R;
+            if (exch) {  // first: the partner is waiting for it
+                const uint64_t mine = p2p_pack(S, Bd, round);
+                if (multi) {
+                    for (int g = 0; g < A.world; ++g)
+                        st_relaxed_sys_u64(reinterpret_cast<uint64_t*>(A.pub_peer[g]) + (slot_word - ring) + k,
+                                           mine);
+                } else {
+                    st_relaxed_u64(slot_word + k, mine);
+                }
+            }
             if (last) {
                 A.stats[2 * row] = S;
                 A.stats[2 * row + 1] = Bd;
@@ -722,24 +732,15 @@ __global__ void __launch_bounds__(kThreads) cb_resident_p2p_kernel(ResidentArgs 
                 A.obs_e[(int64_t)k * A.ncols + col] = __dsub_rn(__dmul_rn(A.B, (double)S), __dmul_rn(A.J, (double)Bd));
                 A.obs_m[(int64_t)k * A.ncols + col] = __ddiv_rn((double)S, (double)A.L * A.L);
             }
-            if (exch) {
-                const int64_t round = done / A.swap_every - 1;
-                const int first = (int)(round % 2);
-                const int n_pairs = (R - first) / 2;
-                const int64_t ro = (round % kRing) * (int64_t)R;
-                uint64_t* slot_word = ring + ro;
-                const uint64_t mine = p2p_pack(S, Bd, round);
-                if (multi) {
-                    for (int g = 0; g < A.world; ++g)
-                        st_relaxed_sys_u64(reinterpret_cast<uint64_t*>(A.pub_peer[g]) + ro + k, mine);
-                } else {
-                    st_relaxed_u64(slot_word + k, mine);
-                }
-                if (k >= first && (k - first) / 2 < n_pairs) {
-                    const int p = (k - first) / 2, i = first + 2 * p, j = i + 1, other = k == i ? j : i;
+            const int first = (int)(round % 2), n_pairs = (R - first) / 2;
+            if (exch && k >= first && (k - first) / 2 < n_pairs) {
+                {
                     // everything that does not need the partner's energy, while its word travels
+                    // (loaded here rather than before the sweep: held across the
+                    // strip code, the values cost the 64-register build spills)
+                    const int p = (k - first) / 2, i = first + 2 * p, other = k == i ? i + 1 : i;
                     const double u = A.u_table[(round - A.u_round0) * A.u_stride + p];
-                    const double bd = __dsub_rn(A.betas[i], A.betas[j]);
+                    const double bi = A.betas[i], bj = A.betas[i + 1];
                     const uint32_t ot3 = kFerro ? __ldg(A.thresh + other * 10 + 8) : 0u;
                     const uint32_t ot4 = kFerro ? __ldg(A.thresh + other * 10 + 9) : 0u;
                     const uint64_t want = (uint64_t)((round & 0x7fff) | 0x8000);
@@ -753,19 +754,11 @@ __global__ void __launch_bounds__(kThreads) cb_resident_p2p_kernel(ResidentArgs 
                     const int64_t Sj = k == i ? So : S, Bj = k == i ? Bo : Bd;
                     const double Ei = __dsub_rn(__dmul_rn(A.B, (double)Si), __dmul_rn(A.J, (double)Bi));
                     const double Ej = __dsub_rn(__dmul_rn(A.B, (double)Sj), __dmul_rn(A.J, (double)Bj));
-                    const double x = __dmul_rn(bd, __dsub_rn(Ei, Ej));
-                    double prob;
-                    if (x >= 0.0) {
-                        prob = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-x)));
-                    } else {
-                        const double ex = exp(x);
-                        prob = __ddiv_rn(ex, __dadd_rn(1.0, ex));
-                    }
-                    const bool acc = u < prob;
+                    bool near = false;
+                    const bool acc = swap_decide(__dsub_rn(bi, bj), Ei, Ej, u, near);
                     if (k == i) {
                         if (acc) atomicAdd((unsigned long long*)&A.counters[0], 1ull);
-                        if (fabs(u - prob) <= 4.0 * 2.220446049250313e-16 * fmax(prob, 2.2250738585072014e-308))
-                            atomicAdd((unsigned long long*)&A.counters[1], 1ull);
+                        if (near) atomicAdd((unsigned long long*)&A.counters[1], 1ull);
                     }
                     if (acc) {
                         nk = other;
