@@ -140,6 +140,7 @@ int ptmh_fill_lattices_parallel(int8_t *spins, int64_t rows, int64_t L,
 /* The sweep kernel the calling thread's last ptmh_cb_sweeps / _sync call
  * launched: info[0] = kind (0 none, 1 cb_sweeps_persistent<rows, threads>,
  * 2 cb_half_sweep_ferro<rows>, 3 cb_half_sweep_fast, 4 cb_half_sweep_generic;
+ * info[4] = 2: temporally blocked items (ptmh_cb_sweeps_ws);
  * after a resident run: 5 cb_resident_kernel with grid-barrier rounds, 6
  * cb_resident_p2p_kernel, 7 cb_resident_kernel on clusters with
  * point-to-point rounds; info[1] = cluster size there; 8
@@ -261,6 +262,21 @@ int ptmh_cb_sweeps_sync(uint32_t *packed, int64_t rows, int64_t L,
                         uint32_t always_mask, uint64_t seed,
                         int64_t first_sweep, int64_t n_sweeps, int64_t *stats,
                         uint32_t *sync, void *stream);
+
+/* ptmh_cb_sweeps_sync with a caller-owned scratch state buffer of the
+ * packed state's size (rows * 2 * ceil(L*L/64) uint32, contents irrelevant):
+ * the persistent path then runs temporally blocked -- one work item per
+ * (sweep, lattice, band), both colours of the band, out of place between
+ * packed and scratch (ping-pong), so every word is read once per sweep
+ * instead of once per colour.  The result is in `packed` afterwards (an odd
+ * sweep count ends with one device copy).  stats (rows, 2) are overwritten
+ * with the final (S, Bond), as on every other path.  Bit-identical to
+ * ptmh_cb_sweeps.  scratch == NULL is ptmh_cb_sweeps_sync. */
+int ptmh_cb_sweeps_ws(uint32_t *packed, int64_t rows, int64_t L,
+                      const int32_t *row_to_slot, const uint32_t *thresh,
+                      uint32_t always_mask, uint64_t seed, int64_t first_sweep,
+                      int64_t n_sweeps, int64_t *stats, uint32_t *sync,
+                      uint32_t *scratch, void *stream);
 
 /* Persistent single-device run segment (csrc/resident.cu): sweeps
  * first_sweep .. first_sweep+n_sweeps-1 of a run of total_sweeps sweeps,

@@ -69,6 +69,7 @@ def _load():
         "ptmh_cb_sweeps": ([P, i64, i64, P, P, u32, u64, i64, i64, P, P], i32),
         "ptmh_cb_sync_words": ([i64, i64], i64),
         "ptmh_cb_sweeps_sync": ([P, i64, i64, P, P, u32, u64, i64, i64, P, P, P], i32),
+        "ptmh_cb_sweeps_ws": ([P, i64, i64, P, P, u32, u64, i64, i64, P, P, P, P], i32),
         "ptmh_cb_row_stats": ([P, i64, i64, P, P], i32),
         "ptmh_cb_unpack_slots": ([P, P, i64, i64, P, P], i32),
         "ptmh_cb_run_resident": ([P, i64, i64, P, P, i32, P, u32, u64, f64, f64, P, P, P, P, P,
@@ -116,7 +117,7 @@ def cb_last_launch() -> dict:
     """The sweep kernel this thread's last sweep call launched (ptmh_cb_last_launch)."""
     v = (ctypes.c_int32 * 6)()
     call("ptmh_cb_last_launch", v)
-    kinds = {0: None, 1: "cb_sweeps_persistent<{r},{t}>", 2: "cb_half_sweep_ferro<{r},0|1>",
+    kinds = {0: None, 1: "cb_sweeps_persistent<{r},{t}>{tb}", 2: "cb_half_sweep_ferro<{r},0|1>",
              3: "cb_half_sweep_fast<{r}>", 4: "cb_half_sweep_generic",
              5: "cb_resident_kernel (clusters of {r}, grid-barrier rounds)",
              6: "cb_resident_p2p_kernel (warp-owned lattices, point-to-point rounds)",
@@ -124,5 +125,6 @@ def cb_last_launch() -> dict:
              8: "cb_cluster_smem_kernel<{r},{t}> (lattices in the shared memory of {g}-CTA clusters, "
                 "point-to-point rounds)"}
     k = kinds.get(v[0])
-    return {"kind": v[0], "rows": v[1], "threads": v[2], "group": v[3], "bands": bool(v[4]),
-            "grid": v[5], "name": k.format(r=v[1], t=v[2], g=v[3]) if k else None}
+    return {"kind": v[0], "rows": v[1], "threads": v[2], "group": v[3], "bands": bool(v[4]), "tb": v[4] == 2,
+            "grid": v[5], "name": k.format(r=v[1], t=v[2], g=v[3], tb=" (temporally blocked)" if v[4] == 2 else "")
+            if k else None}

@@ -333,6 +333,17 @@ int ptmh_cb_sweeps_sync(uint32_t* packed, int64_t rows, int64_t L, const int32_t
                             stats, as_stream(stream), sync);
 }
 
+int ptmh_cb_sweeps_ws(uint32_t* packed, int64_t rows, int64_t L, const int32_t* row_to_slot,
+                      const uint32_t* thresh, uint32_t always_mask, uint64_t seed, int64_t first_sweep,
+                      int64_t n_sweeps, int64_t* stats, uint32_t* sync, uint32_t* scratch, void* stream) {
+    PTMH_CHECK_ARG(L >= 2 && L % 2 == 0 && L <= 65536, "checkerboard needs even 2 <= L <= 65536");
+    PTMH_CHECK_ARG(first_sweep >= 0 && n_sweeps >= 0 && first_sweep + n_sweeps < (1LL << 31),
+                   "checkerboard sweep index must stay below 2^31");
+    PTMH_CHECK_ARG(scratch == nullptr || sync != nullptr, "the scratch buffer needs a sync block");
+    return launch_cb_sweeps(packed, rows, L, row_to_slot, thresh, always_mask, seed, first_sweep, n_sweeps,
+                            stats, as_stream(stream), sync, scratch);
+}
+
 static int run_resident_impl(uint32_t* packed, int64_t R, int64_t L, int64_t* slot_to_row2,
                              int32_t* row_to_slot2, int buf, const uint32_t* thresh, uint32_t always_mask,
                              uint64_t seed, double J, double B, const double* betas, int64_t* stats,
@@ -873,9 +884,11 @@ int ptmh_host_cb_interval(int8_t* spins, int64_t R, int64_t L, int64_t* slot_to_
     // latter (A/B, tools/ only).
     const char* ps = getenv("PTMH_PLUGIN_SYNC");
     const bool plugin_sync = !(ps && ps[0] == '0') && cb_sweeps_persistent_applies(L, always, n_sweeps);
+    uint32_t* d_scratch = nullptr;  // the temporally blocked persistent path's second state buffer
     if (plugin_sync) {
         PTMH_TRY(ws_get(g_ws, 17, (size_t)(nch * sync_words), &d_sync));
         PTMH_CUDA(cudaMemsetAsync(d_sync, 0, (size_t)(nch * sync_words) * 4, sc));
+        PTMH_TRY(ws_get(g_ws, 28, (size_t)(R * 2 * W), &d_scratch));
     }
     auto chunk = [&](int64_t c, int64_t& lo, int64_t& n) {
         lo = R * c / nch;
@@ -885,7 +898,8 @@ int ptmh_host_cb_interval(int8_t* spins, int64_t R, int64_t L, int64_t* slot_to_
         PTMH_TRY(launch_cb_pack(d_spins + lo * nsite, n, L, d_packed + lo * 2 * W, cst));
         PTMH_TRY(launch_cb_row_stats(d_packed + lo * 2 * W, n, L, d_stats + 2 * lo, cst));
         PTMH_TRY(launch_cb_sweeps(d_packed + lo * 2 * W, n, L, d_r2s + lo, d_thr, always, seed, first_sweep,
-                                  n_sweeps, d_stats + 2 * lo, cst, sync));
+                                  n_sweeps, d_stats + 2 * lo, cst, sync,
+                                  sync && d_scratch ? d_scratch + lo * 2 * W : nullptr));
         PTMH_TRY(launch_cb_unpack(d_packed + lo * 2 * W, n, L, d_spins + lo * nsite, cst));
         return PTMH_OK;
     };

@@ -250,20 +250,71 @@ __global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_half_sweep_ferro(
 // Coherence: own-colour words are read and written at L2 (.cg).  The other
 // colour is read through L1 (ld.global.nc), which is safe because (a) the
 // words an item reads are not written while it runs (their next writers
-// depend on it), and (b) every item of phase > 0 starts with an
-// ld.acquire.gpu of its dependency counters, which ptxas emits with
-// CCTL.IVALL: the SM's L1 is invalidated after the words were last written
-// and before they are read.  Phase-0 items read words no item of this launch
+// depend on it), and (b) every item of phase > 0 starts with an acquire
+// fence after its dependency polls, which ptxas emits with CCTL.IVALL: the
+// SM's L1 is invalidated after the words were last written and before they
+// are read.  Phase-0 items read words no item of this launch
 // has written yet.
-__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+__device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
     uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+
+// acquire side of the relaxed polls (ptxas: MEMBAR + CCTL.IVALL, the L1
+// invalidation the .nc reads of the other colour rely on)
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
 // release-add (MEMBAR + RED: no L1 invalidate, no return value to wait for)
 __device__ __forceinline__ void red_release_gpu_add(uint32_t* p, uint32_t v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Temporally blocked items (tb): the colour-0 word (row r, column k) of the
+// next sweep of lattice lat, computed from the current state `in` exactly as
+// ferro_strip computes it (same classes, random numbers and tie rule; ties
+// resolved in place).  An item recomputes the two colour-0 rows just outside
+// its band with it: their owners may be rewriting them concurrently.
+__device__ __forceinline__ uint32_t ferro_word0(const uint32_t* __restrict__ in, int L, int WR, int64_t W,
+                                                int64_t lat, int r, int k, const uint32_t* __restrict__ planes,
+                                                const RoundKeys32& rk, uint32_t ctr1) {
+    const uint32_t* c0 = in + lat * 2 * W;
+    const uint32_t* c1 = c0 + W;
+    const int ru = r == 0 ? L - 1 : r - 1, rd = r == L - 1 ? 0 : r + 1;
+    const int kl = k == 0 ? WR - 1 : k - 1, kr = k == WR - 1 ? 0 : k + 1;
+    const bool even = (r & 1) == 0;  // colour 0: (r + 0) even -> site m sees m - 1
+    const uint32_t S = __ldcg(c0 + r * WR + k);
+    const uint32_t up = __ldg(c1 + ru * WR + k), dn = __ldg(c1 + rd * WR + k), mid = __ldg(c1 + r * WR + k);
+    const uint32_t adj = __ldg(c1 + r * WR + (even ? kl : kr));
+    const uint32_t hz = even ? __funnelshift_l(adj, mid, 1) : __funnelshift_r(mid, adj, 1);
+    const uint32_t a = ~(S ^ up), b = ~(S ^ dn), c = ~(S ^ mid), d = ~(S ^ hz);
+    const uint32_t s1 = a ^ b, c1m = a & b, s2 = c ^ d, c2 = c & d;
+    const uint32_t k0 = s1 ^ s2, c3 = s1 & s2;
+    const uint32_t k1 = c1m ^ c2 ^ c3, K4 = c1m & c2;
+    const uint32_t upm = (k1 & k0) | K4, K2 = k1 & ~k0;
+    uint32_t acc = ~(k1 | K4);
+    const uint32_t slot = planes[18], t3 = planes[16], t4 = planes[17];
+    const uint32_t w32 = (uint32_t)(r * WR + k);
+    const uint4 r0 = philox4x32_10(make_uint4(2u * w32, ctr1, slot, 0u), rk);
+    const uint4 r1 = philox4x32_10(make_uint4(2u * w32 + 1u, ctr1, slot, 0u), rk);
+    const uint32_t U[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+    acc |= K2 & ~U[0];
+    uint32_t bor = 0, eq = upm;
+#pragma unroll
+    for (int p = 7; p >= 0; --p) {
+        const uint32_t Tm = K4 * planes[p] + planes[8 + p];
+        bor = (~U[p] & Tm) | (~U[p] & bor) | (Tm & bor);
+        eq &= ~(U[p] ^ Tm);
+    }
+    acc |= bor & upm;
+    while (eq) {
+        const int bit = __ffs(eq) - 1;
+        eq &= eq - 1;
+        const uint32_t t24 = (((K4 >> bit) & 1u) ? t4 : t3) & 0x00ffffffu;
+        const uint4 r2 = philox4x32_10(make_uint4(w32 * 32u + (uint32_t)bit, ctr1, slot, 1u), rk);
+        if ((r2.x >> 8) < t24) acc |= 1u << bit;
+    }
+    return S ^ acc;
 }
 
 // kPT threads per CTA = per item: 128 where items cover whole lattice rows
@@ -273,7 +324,7 @@ __global__ void __launch_bounds__(kPT, PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_pe
     uint32_t* __restrict__ packed, int64_t rows, int L, int WR, int64_t W,
     const int32_t* __restrict__ row_to_slot, const uint32_t* __restrict__ thresh, const RoundKeys32 rk,
     uint32_t ctr_base, uint32_t n_phases, int64_t* __restrict__ stats, uint32_t esz,
-    uint32_t* __restrict__ sync, uint32_t group, bool bands) {
+    uint32_t* __restrict__ sync, uint32_t group, bool bands, uint32_t* __restrict__ scratch, bool tb) {
     constexpr int kWarps = kPT / 32;
     // tie scratch (3 x kRows x 32 words per warp: 48 KB at kRows = 16) in
     // dynamic shared memory; cb_sweeps_persistent_smem() bytes
@@ -283,13 +334,17 @@ __global__ void __launch_bounds__(kPT, PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_pe
     uint32_t(*tie_sn)[kRows][32] = kRows <= 16 ? tie_m + 2 * kWarps : tie_m;  // (unused at 32 rows)
     __shared__ uint32_t s_item[2];
     __shared__ uint32_t s_planes[2][20];  // the item's lattice: TM[8], TC[8], t3, t4, slot
+    __shared__ uint32_t s_halo[2][128];   // tb: colour-0 rows band_lo - 1 and band_hi (WR <= 128)
     const int warp = threadIdx.x >> 5;
     const int wr_shift = (WR & (WR - 1)) == 0 ? __ffs(WR) - 1 : -1;
     // items per lattice and phase (the host picks group so that a phase still
     // has >= 8 items per resident CTA)
     const uint32_t subs = (uint32_t)((L / kRows) * WR / kPT) / group;
     const uint32_t per_phase = (uint32_t)rows * subs;
-    const uint32_t n_items = n_phases * per_phase;
+    // tb: an item is a whole sweep of its band (both colours), so a "phase"
+    // below counts sweeps and the dependency counters count sweeps done
+    const uint32_t n_steps = tb ? n_phases / 2 : n_phases;
+    const uint32_t n_items = n_steps * per_phase;
     // Band dependencies: an item covers a band of whole strip rows when its
     // blocks span whole lattice rows (kPT % WR == 0).  Its phase-p half-sweep
     // then reads only its band and the adjacent rows of the two neighbouring
@@ -302,45 +357,72 @@ __global__ void __launch_bounds__(kPT, PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_pe
     // counter sync[2 + lat] orders whole phases.
     // (bands: kPT % WR == 0, checked by the launcher)
     uint32_t* const band = sync + 2 + rows;
-    // thread 0 schedules: it holds the next ticket (prefetched one item
-    // ahead, so the atomic's latency is off the critical path), waits for the
-    // item's dependencies, and publishes it
-    uint32_t next = threadIdx.x == 0 ? atomicAdd(&sync[0], 1u) : 0u;
+    // Thread 0 schedules: it holds the next ticket (prefetched one item
+    // ahead, so the atomic's latency is off the critical path), prepares the
+    // item's threshold planes (once per item instead of per thread) and waits
+    // for its dependencies.  It does both as soon as its own strips of the
+    // current item are done -- while the other warps finish theirs -- so that
+    // between the end barrier and the next item's start barrier it only
+    // issues the acquire fence; the release of the finished item is issued
+    // by the last warp meanwhile.  (Before: release, slot and threshold
+    // loads and three ld.acquire polls, one after the other, all between the
+    // two barriers with the CTA's other warps parked: ncu put 12 % of the warp
+    // samples there.)
+    // Dependencies are polled with RELAXED loads, all at once; one acquire
+    // fence follows once every one is satisfied (a release the loads observed
+    // synchronises with the fence; ptxas emits it with CCTL.IVALL, the L1
+    // invalidation the other-colour .nc reads rely on).
+    auto deps_ok = [&](uint32_t item) -> bool {
+        const uint32_t phase = item / per_phase;
+        if (phase == 0) return true;
+        const uint32_t lat = (item - phase * per_phase) / subs;
+        if (!bands) return ld_relaxed_gpu(&sync[2 + lat]) >= phase * subs;
+        const uint32_t sub = item - phase * per_phase - lat * subs;
+        const uint32_t* b = band + (size_t)lat * subs;
+        const uint32_t sm = sub == 0 ? subs - 1 : sub - 1, sp = sub + 1 == subs ? 0 : sub + 1;
+        const bool stats_phase = !tb && phase + 1 == n_phases;
+        const uint32_t dm = ld_relaxed_gpu(b + sm), d0 = ld_relaxed_gpu(b + sub), dp = ld_relaxed_gpu(b + sp);
+        const uint32_t db = stats_phase ? ld_relaxed_gpu(b) : phase;
+        return min(min(dm, d0), min(dp, db)) >= phase;
+    };
+    auto prepare = [&](uint32_t item, uint32_t* pl) {
+        const uint32_t lat = (item - item / per_phase * per_phase) / subs;
+        const int slot = row_to_slot[lat];
+        const uint32_t t3 = __ldg(thresh + slot * 10 + 8), t4 = __ldg(thresh + slot * 10 + 9);
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+            const uint32_t ta = (t3 >> (31 - p)) & 1u, tb3 = (t4 >> (31 - p)) & 1u;
+            pl[p] = tb3 - ta;
+            pl[8 + p] = 0u - ta;
+        }
+        pl[16] = t3;
+        pl[17] = t4;
+        pl[18] = (uint32_t)slot;
+    };
+    // thread 0's scheduling state lives in shared memory (registers are the
+    // strip code's): the next ticket, and whether its planes are in place /
+    // its dependencies were already seen satisfied
+    __shared__ uint32_t s_next, s_prepared, s_ready;
+    if (threadIdx.x == 0) {
+        s_next = atomicAdd(&sync[0], 1u);
+        s_prepared = 0;
+        s_ready = 0;
+    }
     for (int it = 0;; ++it) {
         if (threadIdx.x == 0) {
+            const uint32_t next = s_next;
             if (next < n_items) {
-                const uint32_t phase = next / per_phase;
-                const uint32_t lat = (next - phase * per_phase) / subs;
-                // the lattice's threshold planes, once per item instead of per
-                // thread (the loads overlap the dependency poll)
-                const int slot = row_to_slot[lat];
-                const uint32_t t3 = __ldg(thresh + slot * 10 + 8), t4 = __ldg(thresh + slot * 10 + 9);
-                uint32_t* pl = s_planes[it & 1];
-#pragma unroll
-                for (int p = 0; p < 8; ++p) {
-                    const uint32_t ta = (t3 >> (31 - p)) & 1u, tb = (t4 >> (31 - p)) & 1u;
-                    pl[p] = tb - ta;
-                    pl[8 + p] = 0u - ta;
+                if (!s_prepared) prepare(next, s_planes[it & 1]);
+                if (next >= per_phase) {
+                    if (!s_ready)
+                        while (!deps_ok(next)) __nanosleep(32);
+                    fence_acq_rel_gpu();
                 }
-                pl[16] = t3;
-                pl[17] = t4;
-                pl[18] = (uint32_t)slot;
-                if (phase > 0) {
-                    if (bands) {
-                        const uint32_t sub = next - phase * per_phase - lat * subs;
-                        const uint32_t* b = band + (size_t)lat * subs;
-                        const uint32_t sm = sub == 0 ? subs - 1 : sub - 1, sp = sub + 1 == subs ? 0 : sub + 1;
-                        const bool stats_phase = phase + 1 == n_phases;
-                        while (ld_acquire_gpu(b + sm) < phase || ld_acquire_gpu(b + sub) < phase ||
-                               ld_acquire_gpu(b + sp) < phase || (stats_phase && ld_acquire_gpu(b) < phase))
-                            __nanosleep(32);
-                    } else {
-                        while (ld_acquire_gpu(&sync[2 + lat]) < phase * subs) __nanosleep(32);
-                    }
-                }
+                s_next = atomicAdd(&sync[0], 1u);
             }
             s_item[it & 1] = next;  // double-buffered: the next write is past a barrier
-            if (next < n_items) next = atomicAdd(&sync[0], 1u);
+            s_prepared = 0;
+            s_ready = 0;
         }
         __syncthreads();
         const uint32_t item = s_item[it & 1];
@@ -348,8 +430,49 @@ __global__ void __launch_bounds__(kPT, PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_pe
         const uint32_t phase = item / per_phase;
         const uint32_t r = item - phase * per_phase;
         const uint32_t lat = r / subs, sub = r - lat * subs;
-        const uint32_t ctr1 = ctr_base + phase;
         int sumS = 0, sumB = 0;
+        if (tb) {
+            // ---- temporally blocked item: sweep `phase` of band `sub`, out of
+            // place.  Even sweeps of the launch read packed and write scratch,
+            // odd ones the reverse (ferro_strip kTB).  Colour 0 of the band, and
+            // the two colour-0 rows just outside it (ferro_word0, into s_halo);
+            // a CTA barrier; colour 1 of the band from the new colour 0.
+            uint32_t* const src = (phase & 1) ? scratch : packed;
+            uint32_t* const dstb = (phase & 1) ? packed : scratch;
+            const uint32_t c0 = ctr_base + 2 * phase;
+            const int band_rows = (int)(group * (kPT / WR) * kRows);
+            const int band_lo = (int)sub * band_rows, band_hi = band_lo + band_rows;
+            const uint32_t* pl = s_planes[it & 1];
+            for (uint32_t g = 0; g < group; ++g)
+                ferro_strip<kRows, 0, false, true, 1>(src, L, WR, W, row_to_slot, thresh, rk, c0, stats, esz, true,
+                                                      lat, (int)((sub * group + g) * kPT + threadIdx.x),
+                                                      tie_m[warp], tie_k4[warp], tie_sn[warp], sumS, sumB,
+                                                      wr_shift, pl, dstb);
+            for (int x = (int)threadIdx.x; x < 2 * WR; x += kPT) {
+                const int side = x >= WR, k = x - side * WR;
+                const int r = side ? (band_hi == L ? 0 : band_hi) : (band_lo == 0 ? L - 1 : band_lo - 1);
+                s_halo[side][k] = ferro_word0(src, L, WR, W, lat, r, k, pl, rk, c0);
+            }
+            __syncthreads();  // the band's colour-0 words (stored at L2) and the halo rows
+            const bool last_sweep = phase + 1 == n_steps;
+#define PTMH_TB1(ST)                                                                                           \
+    for (uint32_t g = 0; g < group; ++g)                                                                       \
+        ferro_strip<kRows, 1, ST, false, 2>(src, L, WR, W, row_to_slot, thresh, rk, c0 + 1, stats, esz, true, \
+                                            lat, (int)((sub * group + g) * kPT + threadIdx.x), tie_m[warp],   \
+                                            tie_k4[warp], tie_sn[warp], sumS, sumB, wr_shift, pl, dstb,        \
+                                            s_halo[0], s_halo[1], band_lo, band_hi)
+            if (last_sweep) {
+                PTMH_TB1(true);
+                flush_stats(stats, lat, true, sumS, sumB);  // stats zeroed by the launcher
+            } else {
+                PTMH_TB1(false);
+            }
+#undef PTMH_TB1
+            __syncthreads();  // every store of this item is issued before the release
+            if (threadIdx.x == kPT - 32) red_release_gpu_add(band + (size_t)lat * subs + sub, 1u);
+            continue;
+        }
+        const uint32_t ctr1 = ctr_base + phase;
         // (S, Bond) are only read after the launch: the last sweep's colour 0
         // resets them and its colour 1 recomputes them; earlier sweeps skip
         // the popcounts and the reduction
@@ -372,7 +495,8 @@ __global__ void __launch_bounds__(kPT, PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_pe
         }
 #undef PTMH_STRIP
         __syncthreads();  // every store of this item is issued before the release
-        if (threadIdx.x == 0) red_release_gpu_add(bands ? band + (size_t)lat * subs + sub : &sync[2 + lat], 1u);
+        if (threadIdx.x == kPT - 32)
+            red_release_gpu_add(bands ? band + (size_t)lat * subs + sub : &sync[2 + lat], 1u);
     }
     // last CTA out leaves the sync block zeroed (all of its threads clear the
     // counters: rows * subs band words)
@@ -726,7 +850,7 @@ void cb_set_last_launch(const CbLaunchInfo& info) { g_last_launch = info; }
 
 int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* row_to_slot,
                      const uint32_t* thresh, uint32_t always_mask, uint64_t seed, int64_t first_sweep,
-                     int64_t n_sweeps, int64_t* stats, cudaStream_t s, uint32_t* sync) {
+                     int64_t n_sweeps, int64_t* stats, cudaStream_t s, uint32_t* sync, uint32_t* scratch) {
     if (rows == 0 || n_sweeps == 0) return PTMH_OK;
     g_last_launch = CbLaunchInfo{};
     const ClassPlan plan = make_plan(always_mask);
@@ -815,19 +939,35 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
         while (group * 2 <= blocks && blocks % (group * 2) == 0 &&
                rows * blocks / (group * 2) >= per_slot * slots)
             group *= 2;
-        const int64_t items = 2 * n_sweeps * rows * (blocks / group);
+        const int64_t items = 2 * n_sweeps * rows * (blocks / group);  // (tb: half as many, twice as long)
         const unsigned grid = (unsigned)std::min<int64_t>(items, slots);
         const uint32_t c0 = (uint32_t)(2 * first_sweep), np = (uint32_t)(2 * n_sweeps);
         // band dependencies pay where a phase has few items per CTA slot
         // (1024^2 x 128: 3.21 -> 3.25e12); at C3 size and above lattice-wide
         // phases measure the same or 0.3 % better (fewer polls per item)
         const char* eb = getenv("PTMH_PERSIST_BANDS");  // "0" / "1" pins it (A/B and tests)
-        const bool bands = kpt % WR == 0 && (eb ? eb[0] == '1' : rows * L * L < (1LL << 28));
-        g_last_launch = CbLaunchInfo{1, krows, kpt, (int)group, bands ? 1 : 0, (int)grid};
+        // Temporal blocking (with a caller's scratch state buffer): an item is a
+        // whole sweep of its band, out of place (ping-pong buffers), so each
+        // band's words are read once per sweep instead of once per colour and
+        // an interval has half the items and dependency hand-offs.  It pays
+        // for small shards, whose interval is a chain of few, short items
+        // (one B200, 10 sweeps per launch, attempts/s, per-colour -> blocked:
+        // 1024^2 x 32 2.24 -> 2.37e12), and costs where the GPU is full
+        // (x 64 2.89 -> 2.77e12, x 128 3.22 -> 3.00e12, C3 3.40 -> 3.21e12, C4
+        // 3.54 -> 3.53e12: +7 % instructions for the recomputed halo rows and
+        // the unconditional stores, twice the state in L2; C4's DRAM bytes
+        // only drop 1.49 -> 1.44x, its 888 in-flight bands outgrow L2).
+        // PTMH_PERSIST_TB=1 / 0 forces it on / off (A/B and tests).
+        const char* etb = getenv("PTMH_PERSIST_TB");
+        const bool tb = scratch != nullptr && kpt % WR == 0 && WR <= 128 &&
+                        (etb ? etb[0] == '1' : rows * L * L <= (1LL << 25));
+        const bool bands = tb || (kpt % WR == 0 && (eb ? eb[0] == '1' : rows * L * L < (1LL << 28)));
+        g_last_launch = CbLaunchInfo{1, krows, kpt, (int)group, tb ? 2 : (bands ? 1 : 0), (int)grid};
+        if (tb) PTMH_CUDA(cudaMemsetAsync(stats, 0, (size_t)rows * 2 * sizeof(int64_t), s));
 #define PTMH_PERSIST(K, T)                                                                                    \
     cb_sweeps_persistent<K, T><<<grid, T, persistent_smem(K, T), s>>>(packed, rows, (int)L, WR, W, row_to_slot, \
                                                                       thresh, rk, c0, np, stats, 4u, sync,    \
-                                                                      (uint32_t)group, bands)
+                                                                      (uint32_t)group, bands, scratch, tb)
         if (t128) {
             if (krows == 32) PTMH_PERSIST(32, 128);
             else if (krows == 16) PTMH_PERSIST(16, 128);
@@ -843,6 +983,9 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
         }
 #undef PTMH_PERSIST
         PTMH_LAUNCH_CHECK();
+        if (tb && (n_sweeps & 1))  // an odd number of sweeps left the state in the scratch buffer
+            PTMH_CUDA(cudaMemcpyAsync(packed, scratch, (size_t)rows * 2 * W * sizeof(uint32_t),
+                                      cudaMemcpyDeviceToDevice, s));
         return PTMH_OK;
     }
     for (int64_t t = first_sweep; t < first_sweep + n_sweeps; ++t) {

@@ -70,7 +70,8 @@ int launch_swap(int64_t* slot_to_row, double* energies, int64_t* spin_sums, cons
 int64_t cb_words(int64_t L);
 int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* row_to_slot,
                      const uint32_t* thresh, uint32_t always_mask, uint64_t seed, int64_t first_sweep,
-                     int64_t n_sweeps, int64_t* stats, cudaStream_t s, uint32_t* sync = nullptr);
+                     int64_t n_sweeps, int64_t* stats, cudaStream_t s, uint32_t* sync = nullptr,
+                     uint32_t* scratch = nullptr);
 // kind: 0 none, 1 cb_sweeps_persistent<rows, threads>, 2 cb_half_sweep_ferro<rows>,
 // 3 cb_half_sweep_fast, 4 cb_half_sweep_generic; resident runs (resident.cu):
 // 5 cb_resident_kernel (grid-barrier rounds; rows = cluster size),

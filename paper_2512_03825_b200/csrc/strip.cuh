@@ -28,12 +28,36 @@ template <bool kNC>
 __device__ __forceinline__ uint32_t ld_other(const uint32_t* p) {
     return kNC ? __ldg(p) : __ldcg(p);
 }
+// kTB == 2 (the colour-1 half of a temporally blocked item): the colour-0
+// words this CTA stored before its barrier, read with ordinary (L1-allocating)
+// loads -- coherent within the CTA after bar.sync; no other SM writes them
+// while the item runs, and the item's acquire invalidated L1 after their
+// last readers elsewhere
+__device__ __forceinline__ uint32_t ld_cta(const uint32_t* p) {
+    uint32_t v;  // (explicit: a const __restrict__ pointer would be turned into the .nc path)
+    asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+template <bool kNC, int kTB>
+__device__ __forceinline__ uint32_t ld_oth(const uint32_t* p) {
+    return kTB == 2 ? ld_cta(p) : ld_other<kNC>(p);
+}
 
 // One thread's strip: word column k of lattice rows i0 .. i0+kRows-1 of
 // colour kColor.  kStats: colour 0 resets the lattice's stats, colour 1
 // recomputes them -- the thread's (S, Bond) contributions in sumS / sumB,
 // which the caller reduces (flush_stats).
-template <int kRows, int kColor, bool kStats, bool kNC>
+//
+// kTB: 0 = in place (packed is read and updated).  The temporally blocked
+// persistent path (checkerboard.cu) runs a whole sweep of a band per item,
+// out of place (ping-pong state buffers: `packed` holds sweep t-1, `out`
+// receives sweep t, every word is stored): 1 = its colour-0 half (colour 1
+// read from packed), 2 = its colour-1 half (colour 0 read from out, already
+// updated by this CTA -- at L2, so kNC must be false -- except the rows just
+// outside the band [band_lo, band_hi), which come from hup / hdn: the
+// neighbouring bands' colour-0 words, recomputed by this CTA because those
+// bands may be updating them concurrently; no stats reset in either half).
+template <int kRows, int kColor, bool kStats, bool kNC, int kTB = 0>
 __device__ __forceinline__ void ferro_strip(uint32_t* __restrict__ packed, int L, int WR, int64_t W,
                                             const int32_t* __restrict__ row_to_slot,
                                             const uint32_t* __restrict__ thresh, const RoundKeys32& rk,
@@ -42,22 +66,28 @@ __device__ __forceinline__ void ferro_strip(uint32_t* __restrict__ packed, int L
                                             uint32_t (&tie_m)[kRows][32], uint32_t (&tie_k4)[kRows][32],
                                             uint32_t (&tie_sn)[kRows][32],
                                             int& sumS, int& sumB, int wr_shift = -1,
-                                            const uint32_t* __restrict__ planes = nullptr) {
+                                            const uint32_t* __restrict__ planes = nullptr,
+                                            uint32_t* __restrict__ out = nullptr, const uint32_t* hup = nullptr,
+                                            const uint32_t* hdn = nullptr, int band_lo = 0, int band_hi = 0) {
+    static_assert(kTB == 0 || (kTB == 1 && kColor == 0) || (kTB == 2 && kColor == 1), "kTB");
     const int lane = threadIdx.x & 31;
     const int strip = wr_shift >= 0 ? rem >> wr_shift : rem / WR;
     const int k = rem - strip * WR;
     const int i0 = strip * kRows;
     const uint32_t own_base = (uint32_t)((lat * 2 + kColor) * W);
+    // where the own colour is stored (in place, or the next sweep's buffer)
+    uint32_t* const dst = kTB ? out : packed;
     int slot = 0;
     uint32_t t3 = 0, t4 = 0;
     uint32_t tie_rows = 0;  // bit rr: row rr has ties
     if (active) {
-        if (kColor == 0 && kStats && rem == 0) {  // colour-0 pass: reset, colour-1 pass recomputes
+        if (kTB == 0 && kColor == 0 && kStats && rem == 0) {  // colour-0 pass: reset, colour-1 pass recomputes
             stats[2 * lat] = 0;
             stats[2 * lat + 1] = 0;
         }
-        const uint32_t* __restrict__ other = packed + (lat * 2 + (1 - kColor)) * W;
-        uint32_t* __restrict__ own = packed + own_base;
+        const uint32_t* __restrict__ other = (kTB == 2 ? out : packed) + (lat * 2 + (1 - kColor)) * W;
+        const uint32_t* own = packed + own_base;  // (== own_dst in place)
+        uint32_t* own_dst = dst + own_base;
         // Threshold plane p of a site is bit p of t4 where K4 is set, else of
         // t3: Tm = K4 ? TB : TA with TA, TB in {0, ~0}.  Written as the
         // integer K4 * (TB - TA) - TA (TM[p] in {-1, 0, 1}, TC[p] = -TA) so
@@ -100,11 +130,13 @@ __device__ __forceinline__ void ferro_strip(uint32_t* __restrict__ packed, int L
         oup = min(oup, oup - LW);
         uint32_t o1 = o0 + uWR;
         o1 = min(o1, o1 - LW);
-        uint32_t up = ld_other<kNC>(word_at(other, oup, esz));
-        uint32_t mid = ld_other<kNC>(word_at(other, o0, esz));
-        uint32_t dn = ld_other<kNC>(word_at(other, o1, esz));
+        // kTB == 2: rows band_lo - 1 and band_hi of the other colour come from hup / hdn
+        const bool htop = kTB == 2 && i0 == band_lo, hbot = kTB == 2 && i0 + kRows == band_hi;
+        uint32_t up = htop ? hup[k] : ld_oth<kNC, kTB>(word_at(other, oup, esz));
+        uint32_t mid = ld_oth<kNC, kTB>(word_at(other, o0, esz));
+        uint32_t dn = (kRows == 1 && hbot) ? hdn[k] : ld_oth<kNC, kTB>(word_at(other, o1, esz));
         uint32_t S = __ldcg(word_at(own, o0, esz));
-        uint32_t adj = ld_other<kNC>(word_at(other, o0 + (uint32_t)((kColor & 1) ? dOdd : dEven), esz));
+        uint32_t adj = ld_oth<kNC, kTB>(word_at(other, o0 + (uint32_t)((kColor & 1) ? dOdd : dEven), esz));
         uint32_t o = o0;
 #pragma unroll 2
         for (int rr = 0; rr < kRows; ++rr) {
@@ -112,9 +144,9 @@ __device__ __forceinline__ void ferro_strip(uint32_t* __restrict__ packed, int L
             // prefetch row i+1 (own, adjacent) and row i+2 (other colour, below)
             uint32_t o2 = o1 + uWR;
             o2 = min(o2, o2 - LW);
-            const uint32_t dn_n = ld_other<kNC>(word_at(other, o2, esz));
+            const uint32_t dn_n = (hbot && rr == kRows - 2) ? hdn[k] : ld_oth<kNC, kTB>(word_at(other, o2, esz));
             const uint32_t S_n = __ldcg(word_at(own, o1, esz));
-            const uint32_t adj_n = ld_other<kNC>(word_at(other, o1 + (uint32_t)(even ? dOdd : dEven), esz));
+            const uint32_t adj_n = ld_oth<kNC, kTB>(word_at(other, o1 + (uint32_t)(even ? dOdd : dEven), esz));
             const uint32_t hz = even ? __funnelshift_l(adj, mid, 1)   // m sees m-1
                                      : __funnelshift_r(mid, adj, 1);  // m sees m+1
             const uint32_t a = ~(S ^ up), b = ~(S ^ dn), c = ~(S ^ mid), d = ~(S ^ hz);
@@ -146,7 +178,7 @@ __device__ __forceinline__ void ferro_strip(uint32_t* __restrict__ packed, int L
             if (kRows <= 16) tie_sn[rr][lane] = S ^ acc;  // the row's word as stored: the tie walk starts from it
             if (eq) tie_rows |= 1u << rr;
             const uint32_t Sn = S ^ acc;
-            if (acc) __stcg(word_at(own, o, esz), Sn);
+            if (kTB || acc) __stcg(word_at(own_dst, o, esz), Sn);
             if (kColor == 1 && kStats) {
                 // new aligned masks: a flip toggles alignment with all four neighbours
                 const int kk = __popc(a ^ acc) + __popc(b ^ acc) + __popc(c ^ acc) + __popc(d ^ acc);
@@ -179,7 +211,7 @@ __device__ __forceinline__ void ferro_strip(uint32_t* __restrict__ packed, int L
                 w32 = (uint32_t)((i0 + rr) * WR + k);
                 // (shared memory: no L2 round trip per tie row; 32-row strips
                 // keep only two scratch arrays to fit three CTAs per SM)
-                Sw = kRows <= 16 ? tie_sn[rr][lane] : __ldcg(packed + own_base + w32);
+                Sw = kRows <= 16 ? tie_sn[rr][lane] : __ldcg(dst + own_base + w32);
                 dirty = false;
             }
             if (m != 0) {
@@ -197,7 +229,7 @@ __device__ __forceinline__ void ferro_strip(uint32_t* __restrict__ packed, int L
                     Sw ^= 1u << bit;
                     dirty = true;
                 }
-                if (m == 0 && dirty) __stcg(packed + own_base + w32, Sw);
+                if (m == 0 && dirty) __stcg(dst + own_base + w32, Sw);
             }
         }
     }

@@ -220,6 +220,7 @@ class CheckerboardEngine(_Base):
         # zeroed sync block of the persistent sweep path (left zeroed by every call)
         self.persistent = True
         self._sync = torch.zeros(int(_lib.LIB.ptmh_cb_sync_words(self.rows, self.L)), dtype=torch.int32, device=d)
+        self._scratch = None  # the temporally blocked path's second state buffer (allocated on first use)
 
     @property
     def local_stats(self) -> torch.Tensor:
@@ -251,10 +252,14 @@ class CheckerboardEngine(_Base):
         rts = self.row_to_slot[self.row_lo:self.row_hi]
         if self.persistent:
             # one persistent launch for all 2n half-sweeps where the kernel
-            # supports it (csrc/checkerboard.cu, cb_sweeps_persistent)
-            _lib.call("ptmh_cb_sweeps_sync", _P(self.packed), self.rows, self.L, _P(rts), _P(self.thr),
+            # supports it (csrc/checkerboard.cu, cb_sweeps_persistent); with a
+            # scratch state buffer it runs temporally blocked (a whole sweep of
+            # a band per work item, ping-pong between packed and scratch)
+            if self._scratch is None and self.L >= 1024 and self.L % 512 == 0:
+                self._scratch = torch.empty_like(self.packed)
+            _lib.call("ptmh_cb_sweeps_ws", _P(self.packed), self.rows, self.L, _P(rts), _P(self.thr),
                       self.always, self.seed, first_sweep, n, _P(self.local_stats), _P(self._sync),
-                      self._s())
+                      _P(self._scratch), self._s())
         else:
             _lib.call("ptmh_cb_sweeps", _P(self.packed), self.rows, self.L, _P(rts), _P(self.thr),
                       self.always, self.seed, first_sweep, n, _P(self.local_stats), self._s())

@@ -396,13 +396,20 @@ def test_full_states_match_oracle(mods, L, R, sweeps, every, rec_every):
     (2048, 4, 1, 3, None, "32", "128"),  # ... on 128-thread items (the C4 launch)
     (1024, 8, 0, 2, "0", "32", None),    # 32 rows, grouped
 ])
-@pytest.mark.parametrize("bands", [None, "0", "1"])
+@pytest.mark.parametrize("tb,bands", [(None, None), ("1", None), ("0", None), ("0", "0"), ("0", "1")])
 def test_persistent_sweeps_equal_per_launch_path(mods, monkeypatch, L, R, first, nsweeps, per_slot, rows, threads,
-                                                 bands):
+                                                 tb, bands):
     """The one-launch dataflow path (cb_sweeps_persistent) and the per-launch
     half-sweep kernels give identical lattices and stats; the sync block is
-    left zeroed for the next call."""
+    left zeroed for the next call.  tb = "1": temporally blocked items (a
+    whole sweep of a band per item, ping-pong buffers; odd sweep counts end
+    with the copy back) wherever items span whole lattice rows (the default
+    for shards of <= 2^25 sites); tb = "0": per-colour items with band (or,
+    bands "0", lattice-wide) dependencies."""
     p, engine, _, _ = mods
+    from paper_2512_03825_b200 import _lib
+    if tb is not None:
+        monkeypatch.setenv("PTMH_PERSIST_TB", tb)
     if per_slot is not None:
         monkeypatch.setenv("PTMH_PERSIST_ITEMS_PER_SLOT", per_slot)
     if rows is not None:
@@ -422,6 +429,12 @@ def test_persistent_sweeps_equal_per_launch_path(mods, monkeypatch, L, R, first,
         eng.row_to_slot.copy_(torch.from_numpy(r2s.astype(np.int32)))
         eng.init_state()
         eng.sweeps(first, nsweeps)
+        if persistent and L >= 1024:  # (L = 512: the per-launch kernels either way)
+            launch = _lib.cb_last_launch()
+            assert launch["kind"] == 1
+            # 128-thread items span whole rows up to L = 8192 (256-thread ones up to 16384)
+            spans = launch["threads"] % (L // 64) == 0
+            assert launch["tb"] == (spans and (tb == "1" or (tb is None and R * L * L <= 1 << 25)))
         eng.sweeps(first + nsweeps, 1)  # a second call reuses the (re-zeroed) sync block
         torch.cuda.synchronize()
         if persistent:

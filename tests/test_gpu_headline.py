@@ -11,6 +11,8 @@
   and lattice-wide phases, asserted) on the GPU; a sample of the lattices is
   checked against the oracle's init and sweeps (the lattices are independent
   between exchange rounds, so each sampled lattice's chain is complete).
+* A rank's C3 shard at 8 GPUs (32 lattices) -- the temporally blocked
+  persistent launch (asserted), 10 and 7 sweeps, against the oracle.
 """
 
 import numpy as np
@@ -106,3 +108,35 @@ def test_c4_launch_on_sampled_lattices_equals_oracle():
     torch.cuda.synchronize()
     assert np.array_equal(sample(), ref)
     assert np.array_equal(eng.local_stats.cpu().numpy()[rows], stats)
+
+
+@pytest.mark.parametrize("n_sweeps", [10, 7])
+def test_c3_rank_shard_temporally_blocked_equals_oracle(n_sweeps):
+    """A rank's shard of C3 at 8 GPUs (32 lattices of 1024^2, the rows
+    assign_replicas gives rank 3): the persistent launch runs temporally
+    blocked there (asserted: one work item per (sweep, lattice, band), ping-
+    pong buffers; an odd sweep count ends with the copy back), against the
+    oracle's sweeps of the same rows."""
+    from paper_2512_03825_b200 import _lib, build_ladder
+    from paper_2512_03825_b200.engine import CheckerboardEngine
+
+    L, R_total, G, rank, seed = 1024, 256, 8, 3, 42
+    lo, hi = rank * R_total // G, (rank + 1) * R_total // G
+    temps = build_ladder(R_total)
+    torch.cuda.set_device(0)
+    eng = CheckerboardEngine(L, R_total, temps, seed, 1.0, 0.0, 0.5, 0, row_range=(lo, hi))
+    eng.init_state()
+    ref = np.empty((hi - lo, L, L), dtype=np.int8)
+    oracle.fill_lattices_mt(ref, L * L // 2, seed, stream0=lo)
+    assert np.array_equal(eng.final_spins(), ref)
+    stats = oracle.row_stats_mt(ref)
+    eng.sweeps(0, n_sweeps)
+    launch = _lib.cb_last_launch()
+    assert launch["kind"] == 1 and launch["tb"], launch
+    thr, always = oracle.cb_tables(1.0 / temps, 1.0, 0.0)
+    r2s = np.arange(lo, hi, dtype=np.int64)  # no exchange yet: row r holds slot r
+    for t in range(n_sweeps):
+        oracle.cb_sweep_mt(ref, r2s, thr, always, seed, t, stats)
+    torch.cuda.synchronize()
+    assert np.array_equal(eng.final_spins(), ref)
+    assert np.array_equal(eng.local_stats.cpu().numpy(), stats)
