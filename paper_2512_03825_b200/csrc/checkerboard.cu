@@ -357,21 +357,13 @@ __global__ void __launch_bounds__(kPT, PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_pe
     // counter sync[2 + lat] orders whole phases.
     // (bands: kPT % WR == 0, checked by the launcher)
     uint32_t* const band = sync + 2 + rows;
-    // Thread 0 schedules: it holds the next ticket (prefetched one item
-    // ahead, so the atomic's latency is off the critical path), prepares the
-    // item's threshold planes (once per item instead of per thread) and waits
-    // for its dependencies.  It does both as soon as its own strips of the
-    // current item are done -- while the other warps finish theirs -- so that
-    // between the end barrier and the next item's start barrier it only
-    // issues the acquire fence; the release of the finished item is issued
-    // by the last warp meanwhile.  (Before: release, slot and threshold
-    // loads and three ld.acquire polls, one after the other, all between the
-    // two barriers with the CTA's other warps parked: ncu put 12 % of the warp
-    // samples there.)
-    // Dependencies are polled with RELAXED loads, all at once; one acquire
-    // fence follows once every one is satisfied (a release the loads observed
-    // synchronises with the fence; ptxas emits it with CCTL.IVALL, the L1
-    // invalidation the other-colour .nc reads rely on).
+    // Scheduling.  Dependencies are polled with RELAXED loads, all at once;
+    // one acquire fence follows once every one is satisfied (a release the
+    // loads observed synchronises with the fence; ptxas emits it with
+    // CCTL.IVALL, the L1 invalidation the other-colour .nc reads rely on).
+    // Three ld.acquire in a row each waited for their load and invalidated L1
+    // before the next was issued.  The item's threshold planes are prepared
+    // once per item instead of per thread.
     auto deps_ok = [&](uint32_t item) -> bool {
         const uint32_t phase = item / per_phase;
         if (phase == 0) return true;
@@ -399,30 +391,34 @@ __global__ void __launch_bounds__(kPT, PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_pe
         pl[17] = t4;
         pl[18] = (uint32_t)slot;
     };
-    // thread 0's scheduling state lives in shared memory (registers are the
-    // strip code's): the next ticket, and whether its planes are in place /
-    // its dependencies were already seen satisfied
-    __shared__ uint32_t s_next, s_prepared, s_ready;
-    if (threadIdx.x == 0) {
-        s_next = atomicAdd(&sync[0], 1u);
-        s_prepared = 0;
-        s_ready = 0;
-    }
+    auto release = [&](uint32_t item) {
+        const uint32_t phase = item / per_phase;
+        const uint32_t lat = (item - phase * per_phase) / subs, sub = item - phase * per_phase - lat * subs;
+        red_release_gpu_add(bands ? band + (size_t)lat * subs + sub : &sync[2 + lat], 1u);
+    };
+    // Thread 0 schedules between the items: it holds the next ticket
+    // (prefetched one item ahead, so the atomic's latency is off the critical
+    // path), prepares its planes and waits for its dependencies while the
+    // CTA's other warps wait at the barrier; the last warp issues the
+    // finished item's release meanwhile.  (Tried, slower: preparing the next
+    // item and polling before the end barrier, C3 -1 %, 32-lattice shard
+    // -7 %; a dedicated scheduler warp per CTA talking to the four worker
+    // warps through named barriers -- 5 CTAs of 160 threads per SM -- C3
+    // -15 %, C4 -7 %.)
+    __shared__ uint32_t s_next;
+    if (threadIdx.x == 0) s_next = atomicAdd(&sync[0], 1u);
     for (int it = 0;; ++it) {
         if (threadIdx.x == 0) {
             const uint32_t next = s_next;
             if (next < n_items) {
-                if (!s_prepared) prepare(next, s_planes[it & 1]);
+                prepare(next, s_planes[it & 1]);
                 if (next >= per_phase) {
-                    if (!s_ready)
-                        while (!deps_ok(next)) __nanosleep(32);
+                    while (!deps_ok(next)) __nanosleep(32);
                     fence_acq_rel_gpu();
                 }
                 s_next = atomicAdd(&sync[0], 1u);
             }
             s_item[it & 1] = next;  // double-buffered: the next write is past a barrier
-            s_prepared = 0;
-            s_ready = 0;
         }
         __syncthreads();
         const uint32_t item = s_item[it & 1];
@@ -469,7 +465,7 @@ __global__ void __launch_bounds__(kPT, PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_pe
             }
 #undef PTMH_TB1
             __syncthreads();  // every store of this item is issued before the release
-            if (threadIdx.x == kPT - 32) red_release_gpu_add(band + (size_t)lat * subs + sub, 1u);
+            if (threadIdx.x == kPT - 32) release(item);
             continue;
         }
         const uint32_t ctr1 = ctr_base + phase;
@@ -495,8 +491,7 @@ __global__ void __launch_bounds__(kPT, PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_pe
         }
 #undef PTMH_STRIP
         __syncthreads();  // every store of this item is issued before the release
-        if (threadIdx.x == kPT - 32)
-            red_release_gpu_add(bands ? band + (size_t)lat * subs + sub : &sync[2 + lat], 1u);
+        if (threadIdx.x == kPT - 32) release(item);
     }
     // last CTA out leaves the sync block zeroed (all of its threads clear the
     // counters: rows * subs band words)
@@ -509,7 +504,7 @@ __global__ void __launch_bounds__(kPT, PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_pe
     if (s_last) {
         __threadfence();
         const int64_t n_cnt = rows + (bands ? rows * (int64_t)subs : 0);
-        for (int64_t l = threadIdx.x; l < n_cnt; l += kPT) sync[2 + l] = 0;
+        for (int64_t l = threadIdx.x; l < n_cnt; l += (int64_t)blockDim.x) sync[2 + l] = 0;
         __syncthreads();
         if (threadIdx.x == 0) {
             sync[0] = 0;
