@@ -250,20 +250,16 @@ __global__ void __launch_bounds__(256, PTMH_FERRO_MINB) cb_half_sweep_ferro(
 // Coherence: own-colour words are read and written at L2 (.cg).  The other
 // colour is read through L1 (ld.global.nc), which is safe because (a) the
 // words an item reads are not written while it runs (their next writers
-// depend on it), and (b) every item of phase > 0 starts with an acquire
-// fence after its dependency polls, which ptxas emits with CCTL.IVALL: the
-// SM's L1 is invalidated after the words were last written and before they
-// are read.  Phase-0 items read words no item of this launch
+// depend on it), and (b) every item of phase > 0 starts with an
+// ld.acquire.gpu of its dependency counters, which ptxas emits with
+// CCTL.IVALL: the SM's L1 is invalidated after the words were last written
+// and before they are read.  Phase-0 items read words no item of this launch
 // has written yet.
-__device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
     uint32_t v;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
-
-// acquire side of the relaxed polls (ptxas: MEMBAR + CCTL.IVALL, the L1
-// invalidation the .nc reads of the other colour rely on)
-__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
 // release-add (MEMBAR + RED: no L1 invalidate, no return value to wait for)
 __device__ __forceinline__ void red_release_gpu_add(uint32_t* p, uint32_t v) {
@@ -318,13 +314,16 @@ __device__ __forceinline__ uint32_t ferro_word0(const uint32_t* __restrict__ in,
 }
 
 // kPT threads per CTA = per item: 128 where items cover whole lattice rows
-// (band dependencies, below) or the shard is big, else 256 (the launcher)
-template <int kRows, int kPT>
+// (band dependencies, below) or the shard is big, else 256 (the launcher).
+// tb: temporally blocked items (a separate instantiation: carrying both
+// item kinds in one kernel doubled its code and cost the per-colour path 2 %)
+template <int kRows, int kPT, bool tb = false>
 __global__ void __launch_bounds__(kPT, PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_persistent(
     uint32_t* __restrict__ packed, int64_t rows, int L, int WR, int64_t W,
     const int32_t* __restrict__ row_to_slot, const uint32_t* __restrict__ thresh, const RoundKeys32 rk,
     uint32_t ctr_base, uint32_t n_phases, int64_t* __restrict__ stats, uint32_t esz,
-    uint32_t* __restrict__ sync, uint32_t group, bool bands, uint32_t* __restrict__ scratch, bool tb) {
+    uint32_t* __restrict__ sync, uint32_t group, bool bands, uint32_t* __restrict__ scratch) {
+
     constexpr int kWarps = kPT / 32;
     // tie scratch (3 x kRows x 32 words per warp: 48 KB at kRows = 16) in
     // dynamic shared memory; cb_sweeps_persistent_smem() bytes
@@ -334,7 +333,7 @@ __global__ void __launch_bounds__(kPT, PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_pe
     uint32_t(*tie_sn)[kRows][32] = kRows <= 16 ? tie_m + 2 * kWarps : tie_m;  // (unused at 32 rows)
     __shared__ uint32_t s_item[2];
     __shared__ uint32_t s_planes[2][20];  // the item's lattice: TM[8], TC[8], t3, t4, slot
-    __shared__ uint32_t s_halo[2][128];   // tb: colour-0 rows band_lo - 1 and band_hi (WR <= 128)
+    __shared__ uint32_t s_halo[tb ? 2 : 1][tb ? 128 : 1];  // tb: colour-0 rows band_lo - 1 and band_hi (WR <= 128)
     const int warp = threadIdx.x >> 5;
     const int wr_shift = (WR & (WR - 1)) == 0 ? __ffs(WR) - 1 : -1;
     // items per lattice and phase (the host picks group so that a phase still
@@ -357,68 +356,53 @@ __global__ void __launch_bounds__(kPT, PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_pe
     // counter sync[2 + lat] orders whole phases.
     // (bands: kPT % WR == 0, checked by the launcher)
     uint32_t* const band = sync + 2 + rows;
-    // Scheduling.  Dependencies are polled with RELAXED loads, all at once;
-    // one acquire fence follows once every one is satisfied (a release the
-    // loads observed synchronises with the fence; ptxas emits it with
-    // CCTL.IVALL, the L1 invalidation the other-colour .nc reads rely on).
-    // Three ld.acquire in a row each waited for their load and invalidated L1
-    // before the next was issued.  The item's threshold planes are prepared
-    // once per item instead of per thread.
-    auto deps_ok = [&](uint32_t item) -> bool {
-        const uint32_t phase = item / per_phase;
-        if (phase == 0) return true;
-        const uint32_t lat = (item - phase * per_phase) / subs;
-        if (!bands) return ld_relaxed_gpu(&sync[2 + lat]) >= phase * subs;
-        const uint32_t sub = item - phase * per_phase - lat * subs;
-        const uint32_t* b = band + (size_t)lat * subs;
-        const uint32_t sm = sub == 0 ? subs - 1 : sub - 1, sp = sub + 1 == subs ? 0 : sub + 1;
-        const bool stats_phase = !tb && phase + 1 == n_phases;
-        const uint32_t dm = ld_relaxed_gpu(b + sm), d0 = ld_relaxed_gpu(b + sub), dp = ld_relaxed_gpu(b + sp);
-        const uint32_t db = stats_phase ? ld_relaxed_gpu(b) : phase;
-        return min(min(dm, d0), min(dp, db)) >= phase;
-    };
-    auto prepare = [&](uint32_t item, uint32_t* pl) {
-        const uint32_t lat = (item - item / per_phase * per_phase) / subs;
-        const int slot = row_to_slot[lat];
-        const uint32_t t3 = __ldg(thresh + slot * 10 + 8), t4 = __ldg(thresh + slot * 10 + 9);
-#pragma unroll
-        for (int p = 0; p < 8; ++p) {
-            const uint32_t ta = (t3 >> (31 - p)) & 1u, tb3 = (t4 >> (31 - p)) & 1u;
-            pl[p] = tb3 - ta;
-            pl[8 + p] = 0u - ta;
-        }
-        pl[16] = t3;
-        pl[17] = t4;
-        pl[18] = (uint32_t)slot;
-    };
-    auto release = [&](uint32_t item) {
-        const uint32_t phase = item / per_phase;
-        const uint32_t lat = (item - phase * per_phase) / subs, sub = item - phase * per_phase - lat * subs;
-        red_release_gpu_add(bands ? band + (size_t)lat * subs + sub : &sync[2 + lat], 1u);
-    };
-    // Thread 0 schedules between the items: it holds the next ticket
-    // (prefetched one item ahead, so the atomic's latency is off the critical
-    // path), prepares its planes and waits for its dependencies while the
-    // CTA's other warps wait at the barrier; the last warp issues the
-    // finished item's release meanwhile.  (Tried, slower: preparing the next
-    // item and polling before the end barrier, C3 -1 %, 32-lattice shard
-    // -7 %; a dedicated scheduler warp per CTA talking to the four worker
-    // warps through named barriers -- 5 CTAs of 160 threads per SM -- C3
-    // -15 %, C4 -7 %.)
-    __shared__ uint32_t s_next;
-    if (threadIdx.x == 0) s_next = atomicAdd(&sync[0], 1u);
+    // thread 0 schedules: it holds the next ticket (prefetched one item
+    // ahead, so the atomic's latency is off the critical path), waits for the
+    // item's dependencies, and publishes it.  (Measured in round 2, none kept:
+    // polling the dependency counters with relaxed loads and one acquire
+    // fence instead of ld.acquire each, and issuing the release from another
+    // warp: within noise; preparing the next item and polling before the end
+    // barrier: C3 -1 %, 32-lattice shard -7 %; a dedicated scheduler warp
+    // talking to four worker warps through named barriers, 5 CTAs of 160
+    // threads per SM: C3 -15 %, C4 -7 %; 7 or 8 CTAs per SM at 72 / 64
+    // registers: C3 -8 %.  Keeping `next` in shared memory put the atomic's
+    // round trip in front of every start barrier: C3 -1.6 %.)
+    uint32_t next = threadIdx.x == 0 ? atomicAdd(&sync[0], 1u) : 0u;
     for (int it = 0;; ++it) {
         if (threadIdx.x == 0) {
-            const uint32_t next = s_next;
             if (next < n_items) {
-                prepare(next, s_planes[it & 1]);
-                if (next >= per_phase) {
-                    while (!deps_ok(next)) __nanosleep(32);
-                    fence_acq_rel_gpu();
+                const uint32_t phase = next / per_phase;
+                const uint32_t lat = (next - phase * per_phase) / subs;
+                // the lattice's threshold planes, once per item instead of per
+                // thread (the loads overlap the dependency poll)
+                const int slot = row_to_slot[lat];
+                const uint32_t t3 = __ldg(thresh + slot * 10 + 8), t4 = __ldg(thresh + slot * 10 + 9);
+                uint32_t* pl = s_planes[it & 1];
+#pragma unroll
+                for (int p = 0; p < 8; ++p) {
+                    const uint32_t ta = (t3 >> (31 - p)) & 1u, tb = (t4 >> (31 - p)) & 1u;
+                    pl[p] = tb - ta;
+                    pl[8 + p] = 0u - ta;
                 }
-                s_next = atomicAdd(&sync[0], 1u);
+                pl[16] = t3;
+                pl[17] = t4;
+                pl[18] = (uint32_t)slot;
+                if (phase > 0) {
+                    if (bands) {
+                        const uint32_t sub = next - phase * per_phase - lat * subs;
+                        const uint32_t* b = band + (size_t)lat * subs;
+                        const uint32_t sm = sub == 0 ? subs - 1 : sub - 1, sp = sub + 1 == subs ? 0 : sub + 1;
+                        const bool stats_phase = !tb && phase + 1 == n_phases;
+                        while (ld_acquire_gpu(b + sm) < phase || ld_acquire_gpu(b + sub) < phase ||
+                               ld_acquire_gpu(b + sp) < phase || (stats_phase && ld_acquire_gpu(b) < phase))
+                            __nanosleep(32);
+                    } else {
+                        while (ld_acquire_gpu(&sync[2 + lat]) < phase * subs) __nanosleep(32);
+                    }
+                }
             }
             s_item[it & 1] = next;  // double-buffered: the next write is past a barrier
+            if (next < n_items) next = atomicAdd(&sync[0], 1u);
         }
         __syncthreads();
         const uint32_t item = s_item[it & 1];
@@ -427,7 +411,7 @@ __global__ void __launch_bounds__(kPT, PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_pe
         const uint32_t r = item - phase * per_phase;
         const uint32_t lat = r / subs, sub = r - lat * subs;
         int sumS = 0, sumB = 0;
-        if (tb) {
+        if constexpr (tb) {
             // ---- temporally blocked item: sweep `phase` of band `sub`, out of
             // place.  Even sweeps of the launch read packed and write scratch,
             // odd ones the reverse (ferro_strip kTB).  Colour 0 of the band, and
@@ -465,7 +449,7 @@ __global__ void __launch_bounds__(kPT, PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_pe
             }
 #undef PTMH_TB1
             __syncthreads();  // every store of this item is issued before the release
-            if (threadIdx.x == kPT - 32) release(item);
+            if (threadIdx.x == 0) red_release_gpu_add(band + (size_t)lat * subs + sub, 1u);
             continue;
         }
         const uint32_t ctr1 = ctr_base + phase;
@@ -491,7 +475,7 @@ __global__ void __launch_bounds__(kPT, PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_pe
         }
 #undef PTMH_STRIP
         __syncthreads();  // every store of this item is issued before the release
-        if (threadIdx.x == kPT - 32) release(item);
+        if (threadIdx.x == 0) red_release_gpu_add(bands ? band + (size_t)lat * subs + sub : &sync[2 + lat], 1u);
     }
     // last CTA out leaves the sync block zeroed (all of its threads clear the
     // counters: rows * subs band words)
@@ -504,7 +488,7 @@ __global__ void __launch_bounds__(kPT, PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_pe
     if (s_last) {
         __threadfence();
         const int64_t n_cnt = rows + (bands ? rows * (int64_t)subs : 0);
-        for (int64_t l = threadIdx.x; l < n_cnt; l += (int64_t)blockDim.x) sync[2 + l] = 0;
+        for (int64_t l = threadIdx.x; l < n_cnt; l += kPT) sync[2 + l] = 0;
         __syncthreads();
         if (threadIdx.x == 0) {
             sync[0] = 0;
@@ -878,6 +862,15 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
                 {(const void*)cb_sweeps_persistent<32, 128>, (const void*)cb_sweeps_persistent<16, 128>,
                  (const void*)cb_sweeps_persistent<8, 128>, (const void*)cb_sweeps_persistent<4, 128>,
                  (const void*)cb_sweeps_persistent<2, 128>}};
+            const void* fns_tb[5] = {(const void*)cb_sweeps_persistent<32, 128, true>,
+                                     (const void*)cb_sweeps_persistent<16, 128, true>,
+                                     (const void*)cb_sweeps_persistent<8, 128, true>,
+                                     (const void*)cb_sweeps_persistent<4, 128, true>,
+                                     (const void*)cb_sweeps_persistent<2, 128, true>};
+            for (const void* fn : fns_tb)
+                if (t128)
+                    PTMH_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)persistent_smem(32, kpt)));
             for (const void* fn : fns[t128])
                 PTMH_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)persistent_smem(32, kpt)));
@@ -954,7 +947,7 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
         // only drop 1.49 -> 1.44x, its 888 in-flight bands outgrow L2).
         // PTMH_PERSIST_TB=1 / 0 forces it on / off (A/B and tests).
         const char* etb = getenv("PTMH_PERSIST_TB");
-        const bool tb = scratch != nullptr && kpt % WR == 0 && WR <= 128 &&
+        const bool tb = scratch != nullptr && kpt == 128 && kpt % WR == 0 &&
                         (etb ? etb[0] == '1' : rows * L * L <= (1LL << 25));
         const bool bands = tb || (kpt % WR == 0 && (eb ? eb[0] == '1' : rows * L * L < (1LL << 28)));
         g_last_launch = CbLaunchInfo{1, krows, kpt, (int)group, tb ? 2 : (bands ? 1 : 0), (int)grid};
@@ -962,8 +955,18 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
 #define PTMH_PERSIST(K, T)                                                                                    \
     cb_sweeps_persistent<K, T><<<grid, T, persistent_smem(K, T), s>>>(packed, rows, (int)L, WR, W, row_to_slot, \
                                                                       thresh, rk, c0, np, stats, 4u, sync,    \
-                                                                      (uint32_t)group, bands, scratch, tb)
-        if (t128) {
+                                                                      (uint32_t)group, bands, scratch)
+#define PTMH_PERSIST_TB(K)                                                                                       \
+    cb_sweeps_persistent<K, 128, true><<<grid, 128, persistent_smem(K, 128), s>>>(                               \
+        packed, rows, (int)L, WR, W, row_to_slot, thresh, rk, c0, np, stats, 4u, sync, (uint32_t)group, bands, \
+        scratch)
+        if (tb) {
+            if (krows == 32) PTMH_PERSIST_TB(32);
+            else if (krows == 16) PTMH_PERSIST_TB(16);
+            else if (krows == 8) PTMH_PERSIST_TB(8);
+            else if (krows == 4) PTMH_PERSIST_TB(4);
+            else PTMH_PERSIST_TB(2);
+        } else if (t128) {
             if (krows == 32) PTMH_PERSIST(32, 128);
             else if (krows == 16) PTMH_PERSIST(16, 128);
             else if (krows == 8) PTMH_PERSIST(8, 128);
@@ -977,6 +980,7 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
             else PTMH_PERSIST(2, 256);
         }
 #undef PTMH_PERSIST
+#undef PTMH_PERSIST_TB
         PTMH_LAUNCH_CHECK();
         if (tb && (n_sweeps & 1))  // an odd number of sweeps left the state in the scratch buffer
             PTMH_CUDA(cudaMemcpyAsync(packed, scratch, (size_t)rows * 2 * W * sizeof(uint32_t),

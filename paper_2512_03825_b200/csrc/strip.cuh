@@ -86,8 +86,9 @@ __device__ __forceinline__ void ferro_strip(uint32_t* __restrict__ packed, int L
             stats[2 * lat + 1] = 0;
         }
         const uint32_t* __restrict__ other = (kTB == 2 ? out : packed) + (lat * 2 + (1 - kColor)) * W;
-        const uint32_t* own = packed + own_base;  // (== own_dst in place)
-        uint32_t* own_dst = dst + own_base;
+        // (in place, own is own_dst: one __restrict__ pointer)
+        uint32_t* __restrict__ own_dst = dst + own_base;
+        const uint32_t* own = kTB ? packed + own_base : own_dst;
         // Threshold plane p of a site is bit p of t4 where K4 is set, else of
         // t3: Tm = K4 ? TB : TA with TA, TB in {0, ~0}.  Written as the
         // integer K4 * (TB - TA) - TA (TM[p] in {-1, 0, 1}, TC[p] = -TA) so

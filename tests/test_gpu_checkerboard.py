@@ -432,8 +432,8 @@ def test_persistent_sweeps_equal_per_launch_path(mods, monkeypatch, L, R, first,
         if persistent and L >= 1024:  # (L = 512: the per-launch kernels either way)
             launch = _lib.cb_last_launch()
             assert launch["kind"] == 1
-            # 128-thread items span whole rows up to L = 8192 (256-thread ones up to 16384)
-            spans = launch["threads"] % (L // 64) == 0
+            # temporally blocked items: 128-thread items that span whole rows (L <= 8192)
+            spans = launch["threads"] == 128 and 128 % (L // 64) == 0
             assert launch["tb"] == (spans and (tb == "1" or (tb is None and R * L * L <= 1 << 25)))
         eng.sweeps(first + nsweeps, 1)  # a second call reuses the (re-zeroed) sync block
         torch.cuda.synchronize()

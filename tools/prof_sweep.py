@@ -1,6 +1,6 @@
 """Small driver for ncu: init a config, run a few sweeps + one exchange.
 
-    python tools/prof_sweep.py [c3|c4|c5|c2|c1] [sweeps]
+    python tools/prof_sweep.py [c3|c4|c5|c2|c1|L,R] [sweeps]
 """
 import os
 import sys
@@ -15,7 +15,10 @@ from paper_2512_03825_b200.engine import CheckerboardEngine  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c3"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 4
-L, R, every, _ = CONFIGS[name]
+if "," in name:  # "L,R": e.g. 1024,32 (a rank's C3 shard at 8 GPUs)
+    L, R = map(int, name.split(","))
+else:
+    L, R, every, _ = CONFIGS[name]
 eng = CheckerboardEngine(L, R, build_ladder(R), 42, 1.0, 0.0, 0.5, 0)
 eng.init_state()
 eng.sweeps(0, n)

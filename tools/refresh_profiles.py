@@ -66,7 +66,41 @@ d["c3"].update({"dram_bytes_per_launch": p["dram_read"] + p["dram_write"],
                           "top_stalls": p["stalls"],
                           "note": "bound by ALU + FMA-heavy pipe issue (Philox IMAD.WIDE on fmaheavy, LOP3 on "
                                   "alu), not HBM"}})
+def summ(rep, out):
+    """ncu_summary of gpurun_out/<rep>.ncu-rep into profiles/<RND>_<out>.json; its first kernel."""
+    dst = os.path.join(P, f"{RND}_{out}.json")
+    subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), os.path.join(G, f"{rep}.ncu-rep"),
+                    "--json", dst], capture_output=True, check=True)
+    return json.load(open(dst))[0]
+
+
+def issue(k, words):
+    return {"ipc_active": [k["ipc_active"]], "ipc_peak": 4.0, "alu_pipe_pct": [round(k["alu_pct"], 1)],
+            "fma_pipe_pct": [round(k["fma_pct"], 1)], "warp_instr_per_launch": [k["inst_executed"]],
+            "thread_instr_per_32site_word": [round(k["inst_executed"] * 32 / words, 1)], "top_stalls": k["stalls"]}
+
+
+# C4: one persistent launch of 2 sweeps captured; the bench launch is 10 sweeps (x5)
+k4 = summ("persist_c4", "ncu_full_persistent_c4")
+d["c4"].update({"dram_bytes_per_launch": 5 * (k4["dram_read"] + k4["dram_write"]),
+                "source": f"profiles/{RND}_ncu_full_persistent_c4.json (ncu --set full --clock-control none, one "
+                          "cb_sweeps_persistent<32,128> launch of 2 sweeps of 512 x 4096^2; the bench launch is 10 "
+                          "sweeps, so x5: the 1 GiB state does not fit L2 and every sweep streams it)",
+                "issue": dict(issue(k4, 512 * 4096 * 4096 * 2 / 32),
+                              note="bound by ALU + FMA-heavy pipe issue, not HBM")})
+# the resident kernels: 20 sweeps with a round every sweep (issue figures only; the state is L2-resident)
+for c, rep, L, R, kern in (("c5", "res_c5", 64, 4096, "cb_resident_p2p_kernel<1, 1, 1024>"),
+                           ("c2", "res_c2", 256, 64, "cb_cluster_smem_kernel<2, 256>")):
+    k = summ(rep, f"ncu_full_res_{c}")
+    d[c] = {"source": f"profiles/{RND}_ncu_full_res_{c}.json (ncu --set full, one resident launch of 20 sweeps "
+                      "with a round every sweep)", "kernels": [kern],
+            "issue": dict(issue(k, R * L * L * 20 / 32),
+                          note="latency-bound: few words per thread per colour phase, cluster / round waits")}
+summ("persist_shard32", "ncu_full_persistent_shard32_tb")
 json.dump(d, open(os.path.join(P, "ncu_sweep_summary.json"), "w"), indent=1)
+with open(os.path.join(P, f"{RND}_sanitizer.txt"), "w") as f:
+    f.write("# compute-sanitizer over tools/sanitize_paths.py (round 2, final build, one B200)\n")
+    f.write(open(os.path.join(G, "sanitizer.txt")).read())
 
 # DESIGN.md section 5 table
 f = {}

@@ -1,5 +1,6 @@
 """compute-sanitizer driver (tools/ only): one small call of every kernel family -- persistent
-sweeps, resident checkerboard (warp-owned lattices, clusters), exact windows, resident exact run,
+sweeps (2 lattices of 1024^2: the temporally blocked items), resident checkerboard (warp-owned
+lattices; 256^2 lattices in cluster shared memory), exact windows, resident exact run,
 the per-replica API (device draws, mh_steps, swap_pairs), the host interval plugin.
     compute-sanitizer --tool memcheck|racecheck|synccheck python tools/sanitize_paths.py"""
 import sys
