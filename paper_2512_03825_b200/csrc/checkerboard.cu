@@ -939,13 +939,13 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
         // band's words are read once per sweep instead of once per colour and
         // an interval has half the items and dependency hand-offs.  It pays
         // for small shards, whose interval is a chain of few, short items
-        // (one B200, 10 sweeps per launch, attempts/s, per-colour -> blocked:
-        // 1024^2 x 32 2.24 -> 2.37e12), and costs where the GPU is full
-        // (x 64 2.89 -> 2.77e12, x 128 3.22 -> 3.00e12, C3 3.40 -> 3.21e12, C4
-        // 3.54 -> 3.53e12: +7 % instructions for the recomputed halo rows and
-        // the unconditional stores, twice the state in L2; C4's DRAM bytes
-        // only drop 1.49 -> 1.44x, its 888 in-flight bands outgrow L2).
-        // PTMH_PERSIST_TB=1 / 0 forces it on / off (A/B and tests).
+        // (one B200, attempts/s, per-colour -> blocked: 1024^2 x 16 1.75 ->
+        // 1.96e12, x 32 2.37 -> 2.39e12), and costs where the GPU is full
+        // (x 64 2.93 -> 2.80e12, 2048^2 x 8 2.34 -> 2.30e12, C4 3.74 ->
+        // 3.46e12: the recomputed halo rows and unconditional stores, twice the
+        // state in L2; C4's DRAM bytes only drop 1.49 -> 1.44x, its 888
+        // in-flight bands outgrow L2).  PTMH_PERSIST_TB=1 / 0 forces it on /
+        // off (A/B and tests).
         const char* etb = getenv("PTMH_PERSIST_TB");
         const bool tb = scratch != nullptr && kpt == 128 && kpt % WR == 0 &&
                         (etb ? etb[0] == '1' : rows * L * L <= (1LL << 25));
