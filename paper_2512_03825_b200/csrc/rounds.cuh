@@ -38,8 +38,23 @@ __device__ __forceinline__ uint64_t ld_relaxed_sys_u64(const uint64_t* p) {
 // (beta_i - beta_j) * (E_i - E_j), p = logistic(x) evaluated on the stable
 // side, accept iff u < p.  near: |u - p| within 4 ulp of p, where a last-ulp
 // difference between the device exp and glibc's could flip the decision.
+//
+// Fast path (the decision sits on a resident round's critical path: the FP64
+// exp and division are ~550 cycles): p in FP32 from the same x, |p32 - p| <
+// 1e-6, so wherever |u - p32| > 1e-5 the FP32 comparison IS the FP64 one.
+// The rest (probability ~2e-5 per pair, and every near tie, since a near tie
+// has |u - p| <= 4 ulp) takes the exact FP64 evaluation below.
 __device__ __forceinline__ bool swap_decide(double bd, double Ei, double Ej, double u, bool& near) {
     const double x = __dmul_rn(bd, __dsub_rn(Ei, Ej));
+    {
+        const float xf = (float)x;
+        const float pf = xf >= 0.0f ? __frcp_rn(1.0f + __expf(-xf)) : __fdividef(__expf(xf), 1.0f + __expf(xf));
+        const double d = __dsub_rn(u, (double)pf);
+        if (fabs(d) > 1e-5) {
+            near = false;
+            return d < 0.0;
+        }
+    }
     double prob;
     if (x >= 0.0) {
         prob = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-x)));
