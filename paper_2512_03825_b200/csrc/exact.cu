@@ -38,6 +38,7 @@
 #include "common.cuh"
 #include "launchers.cuh"
 #include "philox.cuh"
+#include "rounds.cuh"
 
 namespace ptmh {
 
@@ -1054,16 +1055,10 @@ __global__ void __launch_bounds__(kMaxThreads, 1) exact_resident_kernel(CommitAr
             for (int p = lane; p < n_pairs; p += 32) {
                 const int i = first + 2 * p, j = i + 1;
                 const double u = stream_uniform(A.seed, (uint64_t)(R + p), (uint64_t)rnd);
-                const double x = __dmul_rn(__dsub_rn(X.betas[i], X.betas[j]), __dsub_rn(s_e[i], s_e[j]));
-                double prob;
-                if (x >= 0.0) {
-                    prob = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-x)));
-                } else {
-                    const double ex = exp(x);
-                    prob = __ddiv_rn(ex, __dadd_rn(1.0, ex));
-                }
-                if (fabs(u - prob) <= 4.0 * 2.220446049250313e-16 * fmax(prob, 2.2250738585072014e-308)) ++ties;
-                if (u < prob) {
+                bool near = false;  // (rounds.cuh: FP32 fast path, exact FP64 near the decision)
+                const bool accept = swap_decide(__dsub_rn(X.betas[i], X.betas[j]), s_e[i], s_e[j], u, near);
+                if (near) ++ties;
+                if (accept) {
                     const int tr = s_s2r[i]; s_s2r[i] = s_s2r[j]; s_s2r[j] = tr;
                     const double te = s_e[i]; s_e[i] = s_e[j]; s_e[j] = te;
                     const long long ts = s_ss[i]; s_ss[i] = s_ss[j]; s_ss[j] = ts;
