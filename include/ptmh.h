@@ -90,6 +90,15 @@ int ptmh_host_uniforms(uint64_t seed, uint64_t stream, uint64_t position,
  * round_index (rng.py:113-116); accept[k] = (u < swap_probability).  The
  * caller swaps its replicas' lattices and energies.  near_ties: decisions a
  * last-ulp exp difference could flip (expected 0). */
+/* The resident kernels' exchange decision (kernels.py:116-148 rule, with an
+ * FP32 fast path and the exact FP64 evaluation within 1e-5 of the boundary)
+ * over n given (beta_i - beta_j, E_i, E_j, u) on the device: accept[t] = 1 iff
+ * u < p; near[t] = 1 where |u - p| <= 4 ulp (a last-ulp exp difference from
+ * glibc could flip it).  Device pointers; for tests of the decision. */
+int ptmh_swap_decide(const double *bd, const double *Ei, const double *Ej,
+                     const double *u, int64_t n, uint8_t *accept, uint8_t *near,
+                     void *stream);
+
 int ptmh_host_swap_pairs(const int64_t *pair_i, const int64_t *pair_j,
                          int64_t npairs, const double *betas,
                          const double *energies, int64_t n, uint64_t seed,

@@ -70,6 +70,7 @@ def _load():
         "ptmh_cb_sync_words": ([i64, i64], i64),
         "ptmh_cb_sweeps_sync": ([P, i64, i64, P, P, u32, u64, i64, i64, P, P, P], i32),
         "ptmh_cb_sweeps_ws": ([P, i64, i64, P, P, u32, u64, i64, i64, P, P, P, P], i32),
+        "ptmh_swap_decide": ([P, P, P, P, i64, P, P, P], i32),
         "ptmh_cb_row_stats": ([P, i64, i64, P, P], i32),
         "ptmh_cb_unpack_slots": ([P, P, i64, i64, P, P], i32),
         "ptmh_cb_run_resident": ([P, i64, i64, P, P, i32, P, u32, u64, f64, f64, P, P, P, P, P,

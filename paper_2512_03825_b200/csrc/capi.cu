@@ -729,6 +729,12 @@ int ptmh_host_uniforms(uint64_t seed, uint64_t stream, uint64_t position, int64_
     return PTMH_OK;
 }
 
+int ptmh_swap_decide(const double* bd, const double* Ei, const double* Ej, const double* u, int64_t n,
+                     uint8_t* accept, uint8_t* near, void* stream) {
+    PTMH_CHECK_ARG(n >= 0, "swap_decide: n >= 0");
+    return launch_swap_decide(bd, Ei, Ej, u, n, accept, near, as_stream(stream));
+}
+
 int ptmh_host_swap_pairs(const int64_t* pair_i, const int64_t* pair_j, int64_t npairs, const double* betas,
                          const double* energies, int64_t n, uint64_t seed, int64_t stream_base,
                          int64_t round_index, uint8_t* accept, int64_t* near_ties) {

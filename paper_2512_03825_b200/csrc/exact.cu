@@ -1391,6 +1391,28 @@ __global__ void swap_kernel(int64_t* __restrict__ slot_to_row, double* __restric
     }
 }
 
+// the resident kernels' pair decision (rounds.cuh, swap_decide: FP32 fast
+// path, exact FP64 within 1e-5 of the decision) over given inputs, so tests
+// can drive it with adversarial u right at the FP64 boundary
+__global__ void swap_decide_kernel(const double* __restrict__ bd, const double* __restrict__ Ei,
+                                   const double* __restrict__ Ej, const double* __restrict__ u, int64_t n,
+                                   uint8_t* __restrict__ accept, uint8_t* __restrict__ near) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        bool nr = false;
+        accept[t] = swap_decide(bd[t], Ei[t], Ej[t], u[t], nr) ? 1 : 0;
+        near[t] = nr ? 1 : 0;
+    }
+}
+
+int launch_swap_decide(const double* bd, const double* Ei, const double* Ej, const double* u, int64_t n,
+                       uint8_t* accept, uint8_t* near, cudaStream_t s) {
+    if (n <= 0) return PTMH_OK;
+    swap_decide_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, s>>>(bd, Ei, Ej, u, n, accept,
+                                                                                            near);
+    PTMH_LAUNCH_CHECK();
+    return PTMH_OK;
+}
+
 // RngStream.uniform / stream_uniform (rng.py:64-96): out[t] = uniform at
 // position pos0 + t of one stream.
 __global__ void uniforms_kernel(uint64_t seed, uint64_t stream, uint64_t pos0, int64_t n, double* out) {

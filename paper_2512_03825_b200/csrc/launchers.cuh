@@ -60,6 +60,9 @@ int launch_uniforms(uint64_t seed, uint64_t stream, uint64_t pos0, int64_t n, do
 int launch_swap_pairs(const int64_t* pi, const int64_t* pj, int64_t npairs, const double* betas,
                       const double* energies, uint64_t seed, int64_t stream_base, int64_t round_index,
                       uint8_t* accept, int64_t* near_ties, cudaStream_t s);
+// the resident rounds' pair decision (rounds.cuh swap_decide) over given inputs
+int launch_swap_decide(const double* bd, const double* Ei, const double* Ej, const double* u, int64_t n,
+                       uint8_t* accept, uint8_t* near, cudaStream_t s);
 int launch_swap(int64_t* slot_to_row, double* energies, int64_t* spin_sums, const double* betas,
                 int64_t R, uint64_t seed, int64_t stream_base, int64_t round_index, int64_t first,
                 int64_t pair_lo, int64_t pair_hi, int64_t* accepted, int64_t* near_ties,
