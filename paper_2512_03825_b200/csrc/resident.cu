@@ -437,19 +437,11 @@ __global__ void __launch_bounds__(kThreads, kThreads <= 256 ? 2 : 1) cb_resident
                                             __dmul_rn(A.J, (double)(k == si ? Bd : Bo)));
                 const double Ej = __dsub_rn(__dmul_rn(A.B, (double)(k == si ? So : S)),
                                             __dmul_rn(A.J, (double)(k == si ? Bo : Bd)));
-                const double x = __dmul_rn(bd, __dsub_rn(Ei, Ej));
-                double prob;
-                if (x >= 0.0) {
-                    prob = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-x)));
-                } else {
-                    const double ex = exp(x);
-                    prob = __ddiv_rn(ex, __dadd_rn(1.0, ex));
-                }
-                const bool acc = u < prob;
+                bool near = false;
+                const bool acc = swap_decide(bd, Ei, Ej, u, near);
                 if (k == si && owner) {
                     if (acc) atomicAdd((unsigned long long*)&A.counters[0], 1ull);
-                    if (fabs(u - prob) <= 4.0 * 2.220446049250313e-16 * fmax(prob, 2.2250738585072014e-308))
-                        atomicAdd((unsigned long long*)&A.counters[1], 1ull);
+                    if (near) atomicAdd((unsigned long long*)&A.counters[1], 1ull);
                 }
                 if (acc) {
                     s_slot[i] = other;
@@ -565,21 +557,12 @@ __global__ void __launch_bounds__(kThreads, kThreads <= 256 ? 2 : 1) cb_resident
                 const int i = first + 2 * p, j = i + 1;
                 const double Ei = __dsub_rn(__dmul_rn(A.B, (double)pub[2 * i]), __dmul_rn(A.J, (double)pub[2 * i + 1]));
                 const double Ej = __dsub_rn(__dmul_rn(A.B, (double)pub[2 * j]), __dmul_rn(A.J, (double)pub[2 * j + 1]));
-                const double u = s_u[li];
-                const double x = __dmul_rn(s_bd[li], __dsub_rn(Ei, Ej));
-                double prob;
-                if (x >= 0.0) {
-                    prob = __ddiv_rn(1.0, __dadd_rn(1.0, exp(-x)));
-                } else {
-                    const double ex = exp(x);
-                    prob = __ddiv_rn(ex, __dadd_rn(1.0, ex));
-                }
-                const bool acc = u < prob;
+                bool near = false;
+                const bool acc = swap_decide(s_bd[li], Ei, Ej, s_u[li], near);
                 if (acc) nk = (k == i) ? j : i;
                 if (k == i && owner) {
                     if (acc) atomicAdd((unsigned long long*)&A.counters[0], 1ull);
-                    if (fabs(u - prob) <= 4.0 * 2.220446049250313e-16 * fmax(prob, 2.2250738585072014e-308))
-                        atomicAdd((unsigned long long*)&A.counters[1], 1ull);
+                    if (near) atomicAdd((unsigned long long*)&A.counters[1], 1ull);
                 }
             }
             // the permutation is an output only: nothing in the launch reads it back
