@@ -206,9 +206,14 @@ def _interval_plan(iterations: int, interval: int) -> list[tuple[int, int | None
 
 
 def _resident_wins(L: int, swap_every_sweeps: int) -> bool:
-    """Persistent launch for small lattices or per-sweep exchanges, where the
-    two-launches-per-sweep path is launch-latency bound."""
-    return L <= 256 or swap_every_sweeps == 1
+    """The resident run (sweeps and rounds in one launch) below L = 1024,
+    where the one-launch-per-interval sweep kernel does not apply and the
+    per-launch sweeps are launch-latency bound, and for per-sweep exchanges.
+    Measured (one B200, attempts/s, resident vs sweep path): 512^2 x 64 every
+    10 sweeps 1.57e12 vs 9.1e11; 384^2 x 64 every 5: 1.13e12 vs 4.2e11;
+    512^2 x 256 every 10: 2.25e12 vs 2.0e12; 1024^2 x 64 every sweep: 1.73e12
+    vs 1.68e12; 1024^2 x 16 every 10: 1.06e12 vs 1.61e12."""
+    return L < 1024 or swap_every_sweeps == 1
 
 
 class _StateStream:
