@@ -369,11 +369,16 @@ static int launch_smem_t(const ResidentArgs& a, int cs, cudaStream_t s) {
     attr[1].id = cudaLaunchAttributeCooperative;
     attr[1].val.cooperative = 1;
     cfg.attrs = attr;
-    // PTMH_SMEM_NOCOOP=1: launch without the cooperative attribute (every
-    // cluster is still resident when the GPU is otherwise idle; ncu replays
-    // cooperative cluster launches with dynamic shared memory as failures)
+    // Without the cooperative attribute under Nsight Compute (which sets
+    // NV_COMPUTE_PROFILER_PERFWORKS_DIR / NV_NSIGHT_INJECTION_PORT_BASE in the
+    // target) or with PTMH_SMEM_NOCOOP=1: ncu fails cooperative cluster
+    // launches with dynamic shared memory (LaunchFailed).  Every cluster is
+    // still resident at once: the launcher checked that they all fit, and a
+    // profiled kernel runs alone.
     const char* nc = getenv("PTMH_SMEM_NOCOOP");
-    cfg.numAttrs = (nc && nc[0] == '1') ? 1 : 2;
+    const bool profiled = getenv("NV_COMPUTE_PROFILER_PERFWORKS_DIR") != nullptr ||
+                          getenv("NV_NSIGHT_INJECTION_PORT_BASE") != nullptr;
+    cfg.numAttrs = ((nc && nc[0] == '1') || profiled) ? 1 : 2;
     int ncl = 0;
     if (cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg) != cudaSuccess) {
         cudaGetLastError();
