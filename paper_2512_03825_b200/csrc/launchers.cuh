@@ -80,7 +80,8 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
 // 5 cb_resident_kernel (grid-barrier rounds; rows = cluster size),
 // 6 cb_resident_p2p_kernel (warp-owned lattices), 7 cb_resident_kernel on
 // clusters with point-to-point rounds, 8 cb_cluster_smem_kernel (rows = strip
-// rows, group = cluster size; resident_smem.cu)
+// rows, group = cluster size; resident_smem.cu), 9 cb_resident_reg64_kernel
+// (64^2 lattices in registers; resident_reg.cu)
 struct CbLaunchInfo {
     int kind, rows, threads, group, bands, grid;
 };
@@ -144,6 +145,9 @@ int launch_cb_resident(const ResidentArgs& a, bool fast, cudaStream_t s, int* gr
 // resident_smem.cu: ferro lattices held in the shared memory of a cluster of
 // CTAs each (point-to-point rounds); returns 1 when it does not apply
 int launch_cb_cluster_smem(const ResidentArgs& a, cudaStream_t s);
+// resident_reg.cu: 64^2 ferro lattices held in registers, one warp each
+// (grid CTAs of `threads`); returns 1 when it does not apply
+int launch_cb_resident_reg64(const ResidentArgs& a, int grid, int threads, cudaStream_t s);
 // workspace of the point-to-point rounds: the swap draws of n_rounds rounds
 int64_t resident_ws_bytes(int64_t R, int64_t n_rounds);
 void fill_class_plan(uint32_t always_mask, int* n_up, int* k, int* sf, int* cls, int* ferro);

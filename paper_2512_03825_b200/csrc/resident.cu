@@ -820,6 +820,10 @@ static int launch_resident_t(const ResidentArgs& a, int sms, cudaStream_t s) {
     const char* es = getenv("PTMH_RESIDENT_STRIP");
     args.strip = args.warp_lat && a.ferro && a.W == 64 && a.WR == 1 && !(es && es[0] == '0');
     void* kargs[] = {&args};
+    if (args.strip) {  // 64^2 ferro lattices: held in registers (resident_reg.cu)
+        const int rc = launch_cb_resident_reg64(args, grid, threads, s);
+        if (rc != 1) return rc;
+    }
     // point-to-point rounds (cb_resident_p2p_kernel): warp-owned lattices, one
     // per warp, one GPU, a swap-draw table; PTMH_RESIDENT_P2P=0 turns it off
     const char* ep = getenv("PTMH_RESIDENT_P2P");

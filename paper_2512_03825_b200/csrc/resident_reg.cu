@@ -1,0 +1,249 @@
+// resident_reg.cu -- the resident run (sweeps + exchange rounds in one
+// cooperative launch, as resident.cu) for 64^2 ferro lattices held in
+// REGISTERS: one warp owns one lattice for the whole launch (C5: 4096 lattices
+// of 64^2, a round every sweep).
+//
+// A 64^2 lattice is 64 rows x 2 colours x one 32-site word (L % 64 == 0, WR =
+// 1).  Lane l keeps rows 2l and 2l+1 of both colours in four registers.  A
+// half-sweep of colour c needs the other colour's rows 2l-1 .. 2l+2: two of
+// them are the lane's own, the other two come from lanes l-1 and l+1 by one
+// shuffle each; the horizontal neighbour is the same row's word rotated by one
+// site (a row is one word, periodic).  So a sweep touches no memory at all:
+// the strip code of resident.cu (cb_resident_p2p_kernel, 2-row strips read
+// from L1/L2) spent ~40 % of its instructions on the loads, stores, address
+// arithmetic and the tie bookkeeping in shared memory.  The update itself --
+// bit-sliced classes, two Philox4x32-10 blocks per word, the byte compare
+// against the threshold planes, one tie walk per lane and half-sweep -- is
+// strip.cuh's, with the same counters: bit-exact with oracle/ptmh_oracle.c.
+// Exchange rounds are resident.cu's point-to-point rounds (rounds.cuh).
+#include <cooperative_groups.h>
+#include <cstdlib>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "launchers.cuh"
+#include "philox.cuh"
+#include "rounds.cuh"
+
+namespace ptmh {
+
+namespace {
+constexpr unsigned kAll = 0xffffffffu;
+}
+
+// the threshold-plane select coefficients of thresholds t3, t4 (strip.cuh:
+// Tm = K4 * TM + TC)
+__device__ __forceinline__ void reg64_planes(uint32_t t3, uint32_t t4, uint32_t (&TM)[8], uint32_t (&TC)[8]) {
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+        const uint32_t ta = (t3 >> (31 - p)) & 1u, tb = (t4 >> (31 - p)) & 1u;
+        TM[p] = tb - ta;
+        TC[p] = 0u - ta;
+    }
+}
+
+// One half-sweep of colour kColor of the warp's lattice.  C[c][rr]: colour c,
+// row 2*lane + rr.  kStats: the colour-1 pass also returns the lane's (S, Bond)
+// contributions of the new configuration (strip.cuh's formulas).
+template <int kColor, bool kStats>
+__device__ __forceinline__ void reg64_pass(uint32_t (&C)[2][2], const uint32_t (&TM)[8], const uint32_t (&TC)[8],
+                                           uint32_t t3, uint32_t t4, uint32_t slot, const RoundKeys32& rk,
+                                           uint32_t ctr1, int lane, int& sumS, int& sumB) {
+    const uint32_t o0 = C[1 - kColor][0], o1 = C[1 - kColor][1];
+    const uint32_t above = __shfl_sync(kAll, o1, (lane + 31) & 31);  // other colour, row 2l - 1
+    const uint32_t below = __shfl_sync(kAll, o0, (lane + 1) & 31);   // other colour, row 2l + 2
+    uint32_t eqm[2], k4m[2];
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+        const uint32_t w32 = (uint32_t)(2 * lane + rr);  // the row = the word's index in its colour plane
+        const bool even = ((rr + kColor) & 1) == 0;      // (row + colour) even: site m sees m - 1
+        const uint32_t S = C[kColor][rr];
+        const uint32_t mid = rr == 0 ? o0 : o1;
+        const uint32_t up = rr == 0 ? above : o0;
+        const uint32_t dn = rr == 0 ? o1 : below;
+        const uint32_t hz = even ? __funnelshift_l(mid, mid, 1) : __funnelshift_r(mid, mid, 1);
+        const uint32_t a = ~(S ^ up), b = ~(S ^ dn), c = ~(S ^ mid), d = ~(S ^ hz);
+        const uint32_t s1 = a ^ b, c1 = a & b, s2 = c ^ d, c2 = c & d;
+        const uint32_t k0 = s1 ^ s2, c3 = s1 & s2;
+        const uint32_t k1 = c1 ^ c2 ^ c3, K4 = c1 & c2;
+        const uint32_t upm = (k1 & k0) | K4;  // k = 3, 4
+        const uint32_t K2 = k1 & ~k0;         // k = 2: dE = 0
+        uint32_t acc = ~(k1 | K4);            // k = 0, 1: dE < 0
+        const uint4 r0 = philox4x32_10(make_uint4(2u * w32, ctr1, slot, 0u), rk);
+        const uint4 r1 = philox4x32_10(make_uint4(2u * w32 + 1u, ctr1, slot, 0u), rk);
+        const uint32_t U[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+        acc |= K2 & ~U[0];
+        uint32_t bor = 0, eq = upm;
+#pragma unroll
+        for (int p = 7; p >= 0; --p) {
+            const uint32_t Tm = K4 * TM[p] + TC[p];
+            bor = (~U[p] & Tm) | (~U[p] & bor) | (Tm & bor);
+            eq &= ~(U[p] ^ Tm);
+        }
+        acc |= bor & upm;
+        const uint32_t Sn = S ^ acc;
+        C[kColor][rr] = Sn;
+        eqm[rr] = eq;
+        k4m[rr] = K4;
+        if (kStats) {
+            const int kk = __popc(a ^ acc) + __popc(b ^ acc) + __popc(c ^ acc) + __popc(d ^ acc);
+            sumB += 2 * kk - 128;
+            sumS += 2 * (__popc(Sn) + __popc(mid)) - 64;
+        }
+    }
+    // ties (top byte equal): each lane walks its own; the warp iterates
+    // max-ties-per-lane times
+    while (__any_sync(kAll, (eqm[0] | eqm[1]) != 0)) {
+        const int rr = eqm[0] ? 0 : 1;
+        const uint32_t m = rr ? eqm[1] : eqm[0];
+        if (m != 0) {
+            const int bit = __ffs(m) - 1;
+            if (rr) eqm[1] &= eqm[1] - 1; else eqm[0] &= eqm[0] - 1;
+            const uint32_t k4 = ((rr ? k4m[1] : k4m[0]) >> bit) & 1u;
+            const uint32_t t24 = (k4 ? t4 : t3) & 0x00ffffffu;
+            const uint32_t w32 = (uint32_t)(2 * lane + rr);
+            const uint4 r2 = philox4x32_10(make_uint4(w32 * 32u + (uint32_t)bit, ctr1, slot, 1u), rk);
+            if ((r2.x >> 8) < t24) {
+                const uint32_t Sw = rr ? C[kColor][1] : C[kColor][0];
+                if (kStats) {
+                    sumS += ((Sw >> bit) & 1u) ? -2 : 2;
+                    sumB += k4 ? -8 : -4;
+                }
+                if (rr) C[kColor][1] = Sw ^ (1u << bit); else C[kColor][0] = Sw ^ (1u << bit);
+            }
+        }
+    }
+}
+
+template <int kThreads>
+__global__ void __launch_bounds__(kThreads) cb_resident_reg64_kernel(ResidentArgs A) {
+    const int lane = threadIdx.x & 31, wq = (int)threadIdx.x >> 5;
+    const bool multi = A.world > 1;
+    const int R = multi ? A.R_total : A.R;  // slots (pairs, swap streams, ring entries)
+    const int lo = (int)((int64_t)A.R * blockIdx.x / gridDim.x);
+    const int hi = (int)((int64_t)A.R * (blockIdx.x + 1) / gridDim.x);
+    if (wq >= hi - lo) return;  // no block-wide barrier below: spare warps leave
+    const int row = lo + wq;
+    uint32_t* const gl = A.packed + (int64_t)row * 2 * 64;
+    uint32_t C[2][2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+        const uint2 v = *reinterpret_cast<const uint2*>(gl + c * 64 + 2 * lane);
+        C[c][0] = v.x;
+        C[c][1] = v.y;
+    }
+    uint64_t* const ring = reinterpret_cast<uint64_t*>(A.slot_stats);  // kRing x R words
+    int k = A.r2s[A.buf][row];
+    uint32_t t3 = __ldg(A.thresh + k * 10 + 8), t4 = __ldg(A.thresh + k * 10 + 9);
+    uint32_t TM[8], TC[8];
+    reg64_planes(t3, t4, TM, TC);
+    int rounds = 0;
+    for (int64_t t = A.first_sweep; t < A.first_sweep + A.n_sweeps; ++t) {
+        const int64_t done = t + 1;
+        const bool rec = A.record_every > 0 && done % A.record_every == 0;
+        const bool exch = A.swap_every > 0 && done % A.swap_every == 0 && done < A.total_sweeps;
+        const bool last = t + 1 == A.first_sweep + A.n_sweeps;
+        const bool need_stats = rec || exch || last;
+        int sS = 0, sB = 0;
+        reg64_pass<0, false>(C, TM, TC, t3, t4, (uint32_t)k, A.rk, (uint32_t)(2 * t), lane, sS, sB);
+        if (need_stats)
+            reg64_pass<1, true>(C, TM, TC, t3, t4, (uint32_t)k, A.rk, (uint32_t)(2 * t + 1), lane, sS, sB);
+        else
+            reg64_pass<1, false>(C, TM, TC, t3, t4, (uint32_t)k, A.rk, (uint32_t)(2 * t + 1), lane, sS, sB);
+        if (!need_stats) continue;
+        sS = __reduce_add_sync(kAll, sS);
+        sB = __reduce_add_sync(kAll, sB);
+        int nk = k;
+        uint32_t n3 = t3, n4 = t4;
+        if (lane == 0) {
+            const int64_t S = sS, Bd = sB;
+            const int64_t round = exch ? done / A.swap_every - 1 : 0;
+            uint64_t* const slot_word = ring + (round % kRing) * (int64_t)R;
+            if (exch) {  // first: the partner is waiting for it
+                const uint64_t mine = p2p_pack(S, Bd, round);
+                if (multi) {
+                    for (int g = 0; g < A.world; ++g)
+                        st_relaxed_sys_u64(reinterpret_cast<uint64_t*>(A.pub_peer[g]) + (slot_word - ring) + k,
+                                           mine);
+                } else {
+                    st_relaxed_u64(slot_word + k, mine);
+                }
+            }
+            if (last) {
+                A.stats[2 * row] = S;
+                A.stats[2 * row + 1] = Bd;
+            }
+            if (rec) {  // by slot, before the round (executor.py order)
+                const int64_t col = done / A.record_every - 1;
+                A.obs_e[(int64_t)k * A.ncols + col] = __dsub_rn(__dmul_rn(A.B, (double)S), __dmul_rn(A.J, (double)Bd));
+                A.obs_m[(int64_t)k * A.ncols + col] = __ddiv_rn((double)S, (double)A.L * A.L);
+            }
+            const int first = (int)(round % 2), n_pairs = (R - first) / 2;
+            if (exch && k >= first && (k - first) / 2 < n_pairs) {
+                // everything that does not need the partner's energy, while its word travels
+                const int p = (k - first) / 2, i = first + 2 * p, other = k == i ? i + 1 : i;
+                const double u = A.u_table[(round - A.u_round0) * A.u_stride + p];
+                const double bi = A.betas[i], bj = A.betas[i + 1];
+                const uint32_t ot3 = __ldg(A.thresh + other * 10 + 8), ot4 = __ldg(A.thresh + other * 10 + 9);
+                const uint64_t want = (uint64_t)((round & 0x7fff) | 0x8000);
+                uint64_t v = multi ? ld_relaxed_sys_u64(slot_word + other) : ld_relaxed_u64(slot_word + other);
+                while ((v & 0xffffull) != want) {
+                    __nanosleep(64);
+                    v = multi ? ld_relaxed_sys_u64(slot_word + other) : ld_relaxed_u64(slot_word + other);
+                }
+                const int64_t So = p2p_field(v, 16), Bo = p2p_field(v, 40);
+                const int64_t Si = k == i ? S : So, Bi = k == i ? Bd : Bo;
+                const int64_t Sj = k == i ? So : S, Bj = k == i ? Bo : Bd;
+                const double Ei = __dsub_rn(__dmul_rn(A.B, (double)Si), __dmul_rn(A.J, (double)Bi));
+                const double Ej = __dsub_rn(__dmul_rn(A.B, (double)Sj), __dmul_rn(A.J, (double)Bj));
+                bool near = false;
+                const bool acc = swap_decide(__dsub_rn(bi, bj), Ei, Ej, u, near);
+                if (k == i) {
+                    if (acc) atomicAdd((unsigned long long*)&A.counters[0], 1ull);
+                    if (near) atomicAdd((unsigned long long*)&A.counters[1], 1ull);
+                }
+                if (acc) {
+                    nk = other;
+                    n3 = ot3;
+                    n4 = ot4;
+                }
+            }
+        }
+        if (exch) ++rounds;
+        const int k_new = __shfl_sync(kAll, nk, 0);
+        if (k_new != k) {  // (warp-uniform) the new slot's thresholds
+            k = k_new;
+            t3 = __shfl_sync(kAll, n3, 0);
+            t4 = __shfl_sync(kAll, n4, 0);
+            reg64_planes(t3, t4, TM, TC);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+        *reinterpret_cast<uint2*>(gl + c * 64 + 2 * lane) = make_uint2(C[c][0], C[c][1]);
+    // the permutation is an output only: the final mapping, in the buffer the
+    // grid-barrier kernel would leave it in (buf flips once per round)
+    if (lane == 0) {
+        const int fb = A.buf ^ (rounds & 1);
+        A.r2s[fb][row] = k;
+        A.s2r[fb][k] = A.row_lo + row;
+    }
+}
+
+// 64^2 ferro lattices (W = 64 words per colour, one per row), one warp each,
+// every lattice's warp resident at once.  Returns 1 when it does not apply.
+int launch_cb_resident_reg64(const ResidentArgs& a, int grid, int threads, cudaStream_t s) {
+    const char* e = getenv("PTMH_RESIDENT_REG");  // "0": resident.cu's strip kernel (A/B)
+    if (e && e[0] == '0') return 1;
+    if (!a.ferro || a.L != 64 || a.WR != 1 || a.W != 64 || (a.swap_every > 0 && !a.u_table)) return 1;
+    const char* ep = getenv("PTMH_RESIDENT_P2P");  // "0": grid-barrier rounds (resident.cu)
+    if (ep && ep[0] == '0' && a.swap_every > 0) return 1;
+    if (threads > 1024 || (int64_t)(a.R + grid - 1) / grid > threads / 32) return 1;
+    if (a.swap_every > 0 && a.world == 1) PTMH_CUDA(cudaMemsetAsync(a.slot_stats, 0, (size_t)kRing * a.R * 8, s));
+    void* kargs[] = {const_cast<ResidentArgs*>(&a)};
+    PTMH_CUDA(cudaLaunchCooperativeKernel((const void*)cb_resident_reg64_kernel<1024>, grid, threads, kargs, 0, s));
+    cb_set_last_launch(CbLaunchInfo{9, 2, threads, 1, 0, grid});
+    return PTMH_OK;
+}
+
+}  // namespace ptmh

@@ -314,6 +314,36 @@ def test_cluster_smem_kernel_matches_oracle(mods, monkeypatch, L, R, sweeps, eve
         (ref.swap_rounds, ref.swaps_attempted, ref.swaps_accepted)
 
 
+@pytest.mark.parametrize("R,sweeps,every,rec_every,J", [
+    (4096, 6, 1, 2, 1.0),   # C5's shape
+    (333, 9, 1, 3, 1.0),    # ragged lattices per CTA
+    (200, 7, 3, 7, 1.0),
+    (97, 11, 0, 11, 1.0),   # no exchanges
+    (130, 5, 1, 5, 0.5),    # another coupling (thresholds from J)
+])
+def test_reg64_kernel_matches_oracle(mods, R, sweeps, every, rec_every, J):
+    """cb_resident_reg64_kernel (64^2 ferro lattices held in registers, a warp
+    each: neighbour rows by shuffles, no memory traffic during the sweeps)
+    against the oracle; the launch is asserted.  (Up to 64 lattices of 64^2
+    the launcher puts every lattice in ONE CTA instead.)"""
+    p = mods[0]
+    from paper_2512_03825_b200 import _lib
+    L, seed = 64, 600 + R
+    cfg = p.SimulationConfig(side=L, replicas=R, iterations=sweeps * L * L, swap_interval=every * L * L,
+                             seed=seed, params=p.IsingParams(J=J, B=0.0), sweep_mode="checkerboard",
+                             record_every=rec_every, return_final_state=True, kernel="resident")
+    rec = p.run(cfg)
+    assert rec.valid, rec.error
+    assert _lib.cb_last_launch()["kind"] == 9
+    ref = oracle.run_checkerboard(L, R, sweeps, every, seed, J=J, record_every=rec_every)
+    assert np.array_equal(rec.final_spins, ref.final_spins)
+    assert np.array_equal(rec.slot_to_row, ref.slot_to_row)
+    assert np.array_equal(rec.energies, ref.energies)
+    assert np.array_equal(rec.magnetizations, ref.magnetizations)
+    assert (rec.swap_rounds, rec.swaps_attempted, rec.swaps_accepted) == \
+        (ref.swap_rounds, ref.swaps_attempted, ref.swaps_accepted)
+
+
 def test_resident_segments_compose(mods):
     """Two resident segments == one resident run == the sweep-kernel path."""
     p, engine, _, _ = mods
