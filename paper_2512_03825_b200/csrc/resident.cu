@@ -794,9 +794,15 @@ static int launch_resident_t(const ResidentArgs& a, int sms, cudaStream_t s) {
     }
     // enough blocks to fill the GPU, few enough that no block owns more
     // lattices than its shared-memory tables hold
-    // Tiny runs (C1: 8 lattices of 16 words per colour) go to ONE CTA: its
-    // exchange rounds then need a CTA barrier instead of a grid barrier.
-    const bool one_cta = cs == 1 && (int64_t)a.R * a.W <= 4 * kThreads && a.R <= kMaxLatPerBlock;
+    // ONE CTA for every lattice of a tiny run (its rounds then need a CTA
+    // barrier instead of a grid barrier) only on request: with the
+    // point-to-point rounds, spreading the lattices over the SMs measured
+    // faster for every small shape (us per sweep + round, one CTA -> spread:
+    // 32^2 x 8 (C1) 2.63 -> 2.40, 64^2 x 16 4.46 -> 2.94, 64^2 x 64 21.0 ->
+    // 3.0, 128^2 x 16 21.0 -> 5.1).  PTMH_RESIDENT_ONECTA=1 forces it (A/B).
+    const char* eo = getenv("PTMH_RESIDENT_ONECTA");
+    const bool one_cta = cs == 1 && (int64_t)a.R * a.W <= 4 * kThreads && a.R <= kMaxLatPerBlock &&
+                         eo && eo[0] == '1';
     const int grid = cs > 1 ? a.R * cs : (one_cta ? 1 : std::min(a.R, slots));
     if (cs == 1 && (a.R + grid - 1) / grid > kMaxLatPerBlock) {
         set_error("resident kernel: too many lattices per block for this grid");

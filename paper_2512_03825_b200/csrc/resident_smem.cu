@@ -412,9 +412,14 @@ int launch_cb_cluster_smem(const ResidentArgs& a, cudaStream_t s) {
     if (e && e[0] != '\0') {
         if (sscanf(e, "%d,%d,%d", &cs, &rows, &threads) != 3) return kNotApplicable;
     } else {
-        // clusters of cs CTAs: as many CTAs as SMs, at most 8 per cluster
+        // clusters of cs CTAs: up to as many CTAs as SMs, at most 8 per
+        // cluster, while the band still splits into whole warps of 2-row strips
+        auto whole_warps = [&](int c) {
+            const int band = a.L / c;
+            return a.L % c == 0 && band % 2 == 0 && (band / 2 * a.WR) % 32 == 0;
+        };
         cs = 1;
-        while (cs < 8 && (int64_t)a.R * cs * 2 <= sms && a.L / (cs * 2) >= 16) cs *= 2;
+        while (cs < 8 && (int64_t)a.R * cs * 2 <= sms && whole_warps(cs * 2)) cs *= 2;
     }
     if (cs < 1 || cs > 16 || a.L % cs != 0) return kNotApplicable;
     if (rows == 1 && threads == 256) return launch_smem_t<1, 256>(a, cs, s);
