@@ -19,7 +19,7 @@ tail -n 1 gpurun_out/bench_*.log
 # the resident kernels, 20 sweeps with a round every sweep: C5 (warp-owned lattices) and C2
 # (lattices in cluster shared memory; ncu replays the cooperative cluster launch only without the
 # cooperative attribute, PTMH_SMEM_NOCOOP=1 -- every cluster is resident on an idle GPU either way)
-ncu --set full --clock-control none --import-source on -k regex:cb_resident -c 1 -o gpurun_out/res_c5 -f \
+ncu --set full --clock-control none --import-source on -k regex:cb_resident_reg64 -c 1 -o gpurun_out/res_c5 -f \
     python tools/prof_resident.py c5 1 > /dev/null 2>&1
 PTMH_SMEM_NOCOOP=1 ncu --set full --clock-control none --import-source on -k regex:cb_cluster_smem -c 1 \
     -o gpurun_out/res_c2 -f python tools/prof_resident.py c2 1 > /dev/null 2>&1
