@@ -24,6 +24,7 @@ void set_error(const std::string& msg);
     do {                                                                       \
         cudaError_t e_ = (call);                                               \
         if (e_ != cudaSuccess) {                                               \
+            cudaGetLastError(); /* a non-sticky error must not fail the next call */ \
             ::ptmh::set_error(std::string(#call) + ": " + cudaGetErrorString(e_)); \
             return PTMH_ERR_CUDA;                                              \
         }                                                                      \

@@ -800,82 +800,92 @@ static int launch_resident_t(const ResidentArgs& a, int sms, cudaStream_t s) {
     // faster for every small shape (us per sweep + round, one CTA -> spread:
     // 32^2 x 8 (C1) 2.63 -> 2.40, 64^2 x 16 4.46 -> 2.94, 64^2 x 64 21.0 ->
     // 3.0, 128^2 x 16 21.0 -> 5.1).  PTMH_RESIDENT_ONECTA=1 forces it (A/B).
-    const char* eo = getenv("PTMH_RESIDENT_ONECTA");
-    const bool one_cta = cs == 1 && (int64_t)a.R * a.W <= 4 * kThreads && a.R <= kMaxLatPerBlock &&
-                         eo && eo[0] == '1';
-    const int grid = cs > 1 ? a.R * cs : (one_cta ? 1 : std::min(a.R, slots));
-    if (cs == 1 && (a.R + grid - 1) / grid > kMaxLatPerBlock) {
-        set_error("resident kernel: too many lattices per block for this grid");
-        return PTMH_ERR_ARG;
-    }
-    // as few threads as keep the item loop's trip count: every thread then
-    // does the same number of words per colour (no tail warps at the barrier)
-    const int64_t items = (int64_t)((a.R * cs + grid - 1) / grid) * a.W / cs;
-    const int64_t trips = (items + kThreads - 1) / kThreads;
-    int threads = (int)std::min<int64_t>(kThreads, (((items + trips - 1) / trips) + 31) & ~31);
-    ResidentArgs args = a;
-    // warp-owned lattices when a lattice is at most 2 words per lane per
-    // colour and the CTA's lattices fit its warps (C5: 28 lattices of 64
-    // words per CTA); PTMH_RESIDENT_WARPLAT=0 turns it off (A/B)
-    const char* ew = getenv("PTMH_RESIDENT_WARPLAT");
-    const int nl_max = (a.R + grid - 1) / grid;
-    args.warp_lat = cs == 1 && !(ew && ew[0] == '0') && a.W <= 64 && nl_max <= kThreads / 32;
-    if (args.warp_lat) threads = 32 * nl_max;
-    // L = 64 (one word per colour row): the lane-per-2-row-strip code of the
-    // sweep kernels; PTMH_RESIDENT_STRIP=0 keeps the per-word code (A/B)
-    const char* es = getenv("PTMH_RESIDENT_STRIP");
-    args.strip = args.warp_lat && a.ferro && a.W == 64 && a.WR == 1 && !(es && es[0] == '0');
-    void* kargs[] = {&args};
-    if (args.strip) {  // 64^2 ferro lattices: held in registers (resident_reg.cu)
-        const int rc = launch_cb_resident_reg64(args, grid, threads, s);
-        if (rc != 1) return rc;
-    }
-    // point-to-point rounds (cb_resident_p2p_kernel): warp-owned lattices, one
-    // per warp, one GPU, a swap-draw table; PTMH_RESIDENT_P2P=0 turns it off
-    const char* ep = getenv("PTMH_RESIDENT_P2P");
-    if (cs == 1 && args.warp_lat && a.u_table && nl_max <= threads / 32 && a.L <= 1024 &&
-        !(ep && ep[0] == '0')) {
-        // one GPU: zero the ring (entries of an earlier launch could carry a
-        // matching stamp).  Across GPUs other ranks may already be storing
-        // into it: a run's ring starts zeroed (ptmh_peer_alloc) and its round
-        // indices only grow, so an older entry never matches
-        if (a.swap_every > 0 && a.world == 1)
-            PTMH_CUDA(cudaMemsetAsync(a.slot_stats, 0, (size_t)kRing * a.R * 8, s));
-        PTMH_CUDA(cudaLaunchCooperativeKernel((const void*)cb_resident_p2p_kernel<kMode, kFerro, kThreads>, grid,
-                                              threads, kargs, 0, s));
-        cb_set_last_launch(CbLaunchInfo{6, 1, threads, 1, 0, grid});
+    for (;; cs = std::max(1, cs / 2)) {
+        const char* eo = getenv("PTMH_RESIDENT_ONECTA");
+        const bool one_cta = cs == 1 && (int64_t)a.R * a.W <= 4 * kThreads && a.R <= kMaxLatPerBlock &&
+                             eo && eo[0] == '1';
+        const int grid = cs > 1 ? a.R * cs : (one_cta ? 1 : std::min(a.R, slots));
+        if (cs == 1 && (a.R + grid - 1) / grid > kMaxLatPerBlock) {
+            set_error("resident kernel: too many lattices per block for this grid");
+            return PTMH_ERR_ARG;
+        }
+        // as few threads as keep the item loop's trip count: every thread then
+        // does the same number of words per colour (no tail warps at the barrier)
+        const int64_t items = (int64_t)((a.R * cs + grid - 1) / grid) * a.W / cs;
+        const int64_t trips = (items + kThreads - 1) / kThreads;
+        int threads = (int)std::min<int64_t>(kThreads, (((items + trips - 1) / trips) + 31) & ~31);
+        ResidentArgs args = a;
+        // warp-owned lattices when a lattice is at most 2 words per lane per
+        // colour and the CTA's lattices fit its warps (C5: 28 lattices of 64
+        // words per CTA); PTMH_RESIDENT_WARPLAT=0 turns it off (A/B)
+        const char* ew = getenv("PTMH_RESIDENT_WARPLAT");
+        const int nl_max = (a.R + grid - 1) / grid;
+        args.warp_lat = cs == 1 && !(ew && ew[0] == '0') && a.W <= 64 && nl_max <= kThreads / 32;
+        if (args.warp_lat) threads = 32 * nl_max;
+        // L = 64 (one word per colour row): the lane-per-2-row-strip code of the
+        // sweep kernels; PTMH_RESIDENT_STRIP=0 keeps the per-word code (A/B)
+        const char* es = getenv("PTMH_RESIDENT_STRIP");
+        args.strip = args.warp_lat && a.ferro && a.W == 64 && a.WR == 1 && !(es && es[0] == '0');
+        void* kargs[] = {&args};
+        if (args.strip) {  // 64^2 ferro lattices: held in registers (resident_reg.cu)
+            const int rc = launch_cb_resident_reg64(args, grid, threads, s);
+            if (rc != 1) return rc;
+        }
+        // point-to-point rounds (cb_resident_p2p_kernel): warp-owned lattices, one
+        // per warp, one GPU, a swap-draw table; PTMH_RESIDENT_P2P=0 turns it off
+        const char* ep = getenv("PTMH_RESIDENT_P2P");
+        if (cs == 1 && args.warp_lat && a.u_table && nl_max <= threads / 32 && a.L <= 1024 &&
+            !(ep && ep[0] == '0')) {
+            // one GPU: zero the ring (entries of an earlier launch could carry a
+            // matching stamp).  Across GPUs other ranks may already be storing
+            // into it: a run's ring starts zeroed (ptmh_peer_alloc) and its round
+            // indices only grow, so an older entry never matches
+            if (a.swap_every > 0 && a.world == 1)
+                PTMH_CUDA(cudaMemsetAsync(a.slot_stats, 0, (size_t)kRing * a.R * 8, s));
+            PTMH_CUDA(cudaLaunchCooperativeKernel((const void*)cb_resident_p2p_kernel<kMode, kFerro, kThreads>, grid,
+                                                  threads, kargs, 0, s));
+            cb_set_last_launch(CbLaunchInfo{6, 1, threads, 1, 0, grid});
+            return PTMH_OK;
+        }
+        if (cs == 1) {
+            PTMH_CUDA(cudaLaunchCooperativeKernel((const void*)cb_resident_kernel<kMode, kFerro, kThreads, false>, grid,
+                                                  threads, kargs, 0, s));
+            cb_set_last_launch(CbLaunchInfo{5, 1, threads, 1, 0, grid});
+            return PTMH_OK;
+        }
+        if (a.u_table && a.world == 1 && a.L <= 1024 && !(ep && ep[0] == '0')) {
+            args.p2p = 1;  // cluster-owned lattices: point-to-point rounds
+            if (a.swap_every > 0) PTMH_CUDA(cudaMemsetAsync(a.slot_stats, 0, (size_t)kRing * a.R * 8, s));
+        }
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)grid);
+        cfg.blockDim = dim3((unsigned)threads);
+        cfg.stream = s;
+        cudaLaunchAttribute attr[2];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)cs;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        attr[1].id = cudaLaunchAttributeCooperative;
+        attr[1].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 2;
+        // cluster CTAs of <= 256 threads (C2): the 256-thread build (<= 128
+        // registers, two CTAs per SM) instead of the 64-register 1024-thread one
+        const void* fn = threads <= 256 ? (const void*)cb_resident_kernel<kMode, kFerro, 256, true>
+                                        : (const void*)cb_resident_kernel<kMode, kFerro, kThreads, true>;
+        const cudaError_t le = cudaLaunchKernelExC(&cfg, fn, kargs);
+        if (le == cudaErrorCooperativeLaunchTooLarge) {
+            // every cluster must be resident at once; cluster placement can
+            // refuse a grid the SM count admits (1024^2 x 32 on 4-CTA clusters
+            // of 1024 threads): retry on smaller clusters, finally on CTAs
+            cudaGetLastError();
+            continue;
+        }
+        PTMH_CUDA(le);
+        cb_set_last_launch(CbLaunchInfo{args.p2p ? 7 : 5, cs, threads, 1, 0, grid});
         return PTMH_OK;
     }
-    if (cs == 1) {
-        PTMH_CUDA(cudaLaunchCooperativeKernel((const void*)cb_resident_kernel<kMode, kFerro, kThreads, false>, grid,
-                                              threads, kargs, 0, s));
-        cb_set_last_launch(CbLaunchInfo{5, 1, threads, 1, 0, grid});
-        return PTMH_OK;
-    }
-    if (a.u_table && a.world == 1 && a.L <= 1024 && !(ep && ep[0] == '0')) {
-        args.p2p = 1;  // cluster-owned lattices: point-to-point rounds
-        if (a.swap_every > 0) PTMH_CUDA(cudaMemsetAsync(a.slot_stats, 0, (size_t)kRing * a.R * 8, s));
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3((unsigned)threads);
-    cfg.stream = s;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = (unsigned)cs;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    attr[1].id = cudaLaunchAttributeCooperative;
-    attr[1].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 2;
-    // cluster CTAs of <= 256 threads (C2): the 256-thread build (<= 128
-    // registers, two CTAs per SM) instead of the 64-register 1024-thread one
-    const void* fn = threads <= 256 ? (const void*)cb_resident_kernel<kMode, kFerro, 256, true>
-                                    : (const void*)cb_resident_kernel<kMode, kFerro, kThreads, true>;
-    PTMH_CUDA(cudaLaunchKernelExC(&cfg, fn, kargs));
-    cb_set_last_launch(CbLaunchInfo{args.p2p ? 7 : 5, cs, threads, 1, 0, grid});
-    return PTMH_OK;
 }
 
 template <int kMode, bool kFerro>

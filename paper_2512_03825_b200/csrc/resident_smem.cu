@@ -389,7 +389,14 @@ static int launch_smem_t(const ResidentArgs& a, int cs, cudaStream_t s) {
     if (a.swap_every > 0 && a.world == 1)
         PTMH_CUDA(cudaMemsetAsync(a.slot_stats, 0, (size_t)kRing * a.R * 8, s));
     void* kargs[] = {const_cast<ResidentArgs*>(&a)};
-    PTMH_CUDA(cudaLaunchKernelExC(&cfg, fn, kargs));
+    const cudaError_t le = cudaLaunchKernelExC(&cfg, fn, kargs);
+    if (le == cudaErrorCooperativeLaunchTooLarge) {
+        // the occupancy query can admit a grid that the cooperative launch
+        // then refuses (cluster placement): resident.cu's kernel instead
+        cudaGetLastError();
+        return kNotApplicable;
+    }
+    PTMH_CUDA(le);
     cb_set_last_launch(CbLaunchInfo{8, kRows, threads, cs, 0, a.R * cs});
     return PTMH_OK;
 }

@@ -344,6 +344,27 @@ def test_reg64_kernel_matches_oracle(mods, R, sweeps, every, rec_every, J):
         (ref.swap_rounds, ref.swaps_attempted, ref.swaps_accepted)
 
 
+@pytest.mark.parametrize("J,B", [(1.0, 0.1), (-1.0, 0.0)])
+def test_resident_large_lattices_non_ferro(mods, J, B):
+    """The L2-resident kernel at 1024^2 x 32 with a round every sweep (a field
+    or an antiferromagnet: no shared-memory kernel): its 4-CTA clusters of
+    1024 threads cannot all be resident at once, so the launcher retries on
+    smaller clusters (cudaErrorCooperativeLaunchTooLarge) -- and the next run
+    on the same process is unaffected by that refused launch."""
+    p = mods[0]
+    L, R, sweeps = 1024, 32, 2
+    for seed in (3, 4):
+        cfg = p.SimulationConfig(side=L, replicas=R, iterations=sweeps * L * L, swap_interval=L * L, seed=seed,
+                                 params=p.IsingParams(J=J, B=B), sweep_mode="checkerboard",
+                                 return_final_state=True)
+        rec = p.run(cfg)
+        assert rec.valid, rec.error
+        ref = oracle.run_checkerboard(L, R, sweeps, 1, seed, J=J, B=B)
+        assert np.array_equal(rec.final_spins, ref.final_spins)
+        assert np.array_equal(rec.energies, ref.energies)
+        assert np.array_equal(rec.slot_to_row, ref.slot_to_row)
+
+
 def test_resident_segments_compose(mods):
     """Two resident segments == one resident run == the sweep-kernel path."""
     p, engine, _, _ = mods
