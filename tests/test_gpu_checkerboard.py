@@ -582,3 +582,32 @@ def test_resident_sharded_virtual_ranks(mods, monkeypatch, L, R, G, total, every
     assert np.array_equal(stats, ref.local_stats.cpu().numpy())
     assert sum(e.swap_counts()[0] for e in engs) == ref.swap_counts()[0]
     assert torch.equal(sum(oes), roe) and torch.equal(sum(oms), rom)
+
+
+@pytest.mark.parametrize("L,R,sweeps,every,J,B", [
+    (96, 130, 3, 1, 1.0, 0.0), (192, 40, 3, 2, 1.0, 0.0), (320, 17, 2, 1, 1.0, 0.0),
+    (512, 40, 3, 1, 1.0, 0.0), (512, 9, 4, 2, 0.5, 0.1), (640, 12, 2, 1, 1.0, 0.0),
+    (1024, 20, 2, 1, 1.0, 0.0), (1024, 7, 2, 1, -1.0, 0.0), (1536, 5, 2, 1, 1.0, 0.0),
+    (2048, 6, 2, 1, 1.0, 0.0), (2048, 3, 2, 1, 1.0, -0.2),
+])
+def test_resident_and_sweep_paths_agree(mods, L, R, sweeps, every, J, B):
+    """Larger shapes than the oracle tests reach: the resident run (whichever
+    kernel the launcher picks: shared-memory clusters, L2 clusters, CTA- or
+    warp-owned lattices, with the cooperative-launch fallbacks) and the sweep
+    path (persistent or per-launch kernels + exchange kernel) are the same
+    chain, so their records must be identical."""
+    p = mods[0]
+    recs = []
+    for kernel in ("resident", "sweep"):
+        cfg = p.SimulationConfig(side=L, replicas=R, iterations=sweeps * L * L, swap_interval=every * L * L,
+                                 seed=L + R, params=p.IsingParams(J=J, B=B), sweep_mode="checkerboard",
+                                 return_final_state=True, kernel=kernel)
+        rec = p.run(cfg)
+        assert rec.valid, (kernel, rec.error)
+        recs.append(rec)
+    a, b = recs
+    assert np.array_equal(a.final_spins, b.final_spins)
+    assert np.array_equal(a.energies, b.energies)
+    assert np.array_equal(a.magnetizations, b.magnetizations)
+    assert np.array_equal(a.slot_to_row, b.slot_to_row)
+    assert (a.swaps_attempted, a.swaps_accepted) == (b.swaps_attempted, b.swaps_accepted)
