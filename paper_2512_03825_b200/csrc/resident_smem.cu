@@ -152,7 +152,7 @@ __device__ __forceinline__ void smem_strip(uint32_t* __restrict__ own, const uin
 }
 
 // the threshold-plane select coefficients of slot k (strip.cuh: Tm = K4 * TM + TC)
-__device__ __forceinline__ void smem_set_slot(const ResidentArgs& A, int k, uint32_t t3, uint32_t t4,
+__device__ __forceinline__ void smem_set_slot(int k, uint32_t t3, uint32_t t4,
                                               uint32_t* s_mask) {
 #pragma unroll
     for (int p = 0; p < 8; ++p) {
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(kThreads) cb_cluster_smem_kernel(ResidentArgs 
         }
     if (threadIdx.x == 0) {
         const int k = A.r2s[A.buf][row];
-        smem_set_slot(A, k, __ldg(A.thresh + k * 10 + 8), __ldg(A.thresh + k * 10 + 9), s_mask);
+        smem_set_slot(k, __ldg(A.thresh + k * 10 + 8), __ldg(A.thresh + k * 10 + 9), s_mask);
     }
     const uint32_t* up_pl = cluster.map_shared_rank(s_lat, (q + cs - 1) % cs);
     const uint32_t* dn_pl = cluster.map_shared_rank(s_lat, (q + 1) % cs);
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(kThreads) cb_cluster_smem_kernel(ResidentArgs 
                     if (acc) atomicAdd((unsigned long long*)&A.counters[0], 1ull);
                     if (near) atomicAdd((unsigned long long*)&A.counters[1], 1ull);
                 }
-                if (acc) smem_set_slot(A, other, ot3, ot4, s_mask);
+                if (acc) smem_set_slot(other, ot3, ot4, s_mask);
             }
         }
         if (exch) ++rounds;
