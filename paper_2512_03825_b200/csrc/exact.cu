@@ -653,8 +653,15 @@ __global__ void __launch_bounds__(256, PTMH_DRAW_MINB) draw_w_kernel(DrawArgs D)
 // partial sum is exact, so the window's energies in attempt order are a
 // CTA-wide prefix sum of the accepted increments (the -0.0 identity and the
 // "no accepted attempt yet" rule keep the reference's signed zeros).
-template <bool kRec>
+//
+// kSmem: the slot's bit lattice is copied into shared memory for the call
+// (dynamic, nwords words; L <= 1024 at 128 KB) and back at the end, so the
+// spin gathers and flips of every window hit shared memory instead of L2:
+// the window commit is a chain of dependent loads and atomics (free pass,
+// then the dependent attempts level by level).
+template <bool kRec, bool kSmem>
 __global__ void __launch_bounds__(256) commit_w_kernel(CommitArgs C) {
+    extern __shared__ uint32_t s_latw[];
     __shared__ uint32_t dep_bits[kWin / 32];
     __shared__ double s_d[kRec ? kWin : 1];
     __shared__ int s_ds[kRec ? kWin : 1];
@@ -671,7 +678,12 @@ __global__ void __launch_bounds__(256) commit_w_kernel(CommitArgs C) {
     const int Li = (int)A.L;
     const float invL = 1.0f / (float)Li;
     const int64_t nwords = ((int64_t)Li * Li + 31) >> 5;
-    uint32_t* latw = A.bits + A.slot_to_row[slot] * nwords;
+    uint32_t* const latw_g = A.bits + A.slot_to_row[slot] * nwords;
+    if (kSmem) {
+        for (int64_t k = threadIdx.x; k < nwords; k += blockDim.x) s_latw[k] = latw_g[k];
+        // (ordered before the first gather by the window loop's first barrier)
+    }
+    uint32_t* latw = kSmem ? s_latw : latw_g;
     auto spin = [&](int x) -> int { return 2 * (int)((latw[x >> 5] >> (x & 31)) & 1u) - 1; };
     auto nbrs = [&](int x, int& up, int& dn, int& rt, int& lf) {
         const int r = site_row(x, Li, invL), c = x - r * Li;
@@ -887,6 +899,8 @@ __global__ void __launch_bounds__(256) commit_w_kernel(CommitArgs C) {
         red_s[warp] = acc_ds;
     }
     __syncthreads();
+    if (kSmem)  // the window loop's last barrier ordered every flip before this
+        for (int64_t k = threadIdx.x; k < nwords; k += blockDim.x) latw_g[k] = s_latw[k];
     if (threadIdx.x == 0) {
         double td = -0.0;
         long long ts = 0;
@@ -1223,6 +1237,17 @@ int launch_advance_2phase(const AdvanceArgs& a, void* ws, int64_t ws_bytes, cuda
     const char* ew = getenv("PTMH_EXACT_WINDOWS");
     const bool windows = !rounds && a.bits && a.int_energy && a.record <= 1 && a.L <= 4096 &&
                          (ew && ew[0] == '2' ? a.L >= 3 : a.L >= 16) && !(ew && ew[0] == '0');
+    // the window commit with the slot's bit lattice in shared memory where it
+    // fits (L <= 1024: 128 KB; PTMH_EXACT_LAT_SMEM=0 keeps it in L2, A/B)
+    const char* els = getenv("PTMH_EXACT_LAT_SMEM");
+    const size_t lat_bytes = (size_t)((a.L * a.L + 31) / 32) * 4;
+    const bool lat_smem = windows && lat_bytes <= 160 * 1024 && !(els && els[0] == '0');
+    if (lat_smem && lat_bytes > 48 * 1024) {
+        PTMH_CUDA(cudaFuncSetAttribute((const void*)commit_w_kernel<true, true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lat_bytes));
+        PTMH_CUDA(cudaFuncSetAttribute((const void*)commit_w_kernel<false, true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lat_bytes));
+    }
     size_t res_smem = 0;
     if (rounds) {  // exact_resident_kernel: one CTA, a warp per slot, every lattice in shared memory
         res_smem = (size_t)nslots * (size_t)((a.L * a.L + 31) / 32) * 4;
@@ -1277,10 +1302,14 @@ int launch_advance_2phase(const AdvanceArgs& a, void* ws, int64_t ws_bytes, cuda
             exact_resident_kernel<512><<<1, (unsigned)(32 * nslots), res_smem, sc>>>(C, *rounds);
         else if (rounds)
             exact_resident_kernel<1024><<<1, (unsigned)(32 * nslots), res_smem, sc>>>(C, *rounds);
+        else if (windows && lat_smem && a.record == 1)
+            commit_w_kernel<true, true><<<(unsigned)nslots, 256, lat_bytes, sc>>>(C);
+        else if (windows && lat_smem)
+            commit_w_kernel<false, true><<<(unsigned)nslots, 256, lat_bytes, sc>>>(C);
         else if (windows && a.record == 1)
-            commit_w_kernel<true><<<(unsigned)nslots, 256, 0, sc>>>(C);
+            commit_w_kernel<true, false><<<(unsigned)nslots, 256, 0, sc>>>(C);
         else if (windows)
-            commit_w_kernel<false><<<(unsigned)nslots, 256, 0, sc>>>(C);
+            commit_w_kernel<false, false><<<(unsigned)nslots, 256, 0, sc>>>(C);
         else if (a.bits)
             commit_kernel<true><<<ceil_div(nslots, 4), 128, 0, sc>>>(C);
         else
