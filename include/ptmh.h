@@ -155,7 +155,8 @@ int ptmh_fill_lattices_parallel(int8_t *spins, int64_t rows, int64_t L,
  * point-to-point rounds; info[1] = cluster size there; 8
  * cb_cluster_smem_kernel, lattices in the shared memory of clusters of
  * info[3] CTAs, info[1] = strip rows; 9 cb_resident_reg64_kernel, 64^2
- * lattices held in registers, a warp each),
+ * lattices held in registers, a warp each; 10 cb_resident_reg32_kernel,
+ * the same for 32^2),
  * info[1] = rows per thread, [2] = threads per item / CTA, [3] = blocks per
  * item (group), [4] = band dependencies, [5] = grid (persistent only). */
 int ptmh_cb_last_launch(int32_t *info);

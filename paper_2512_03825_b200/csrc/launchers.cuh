@@ -81,7 +81,8 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
 // 6 cb_resident_p2p_kernel (warp-owned lattices), 7 cb_resident_kernel on
 // clusters with point-to-point rounds, 8 cb_cluster_smem_kernel (rows = strip
 // rows, group = cluster size; resident_smem.cu), 9 cb_resident_reg64_kernel
-// (64^2 lattices in registers; resident_reg.cu)
+// (64^2 lattices in registers; resident_reg.cu), 10 cb_resident_reg32_kernel
+// (32^2 lattices in registers)
 struct CbLaunchInfo {
     int kind, rows, threads, group, bands, grid;
 };
@@ -125,6 +126,7 @@ struct ResidentArgs {
     int warp_lat;               // launcher-set: each warp owns whole lattices (no CTA barrier per colour)
     int strip;                  // launcher-set: warp-owned 64^2 ferro lattices use the strip code
     int p2p;                    // launcher-set: cluster-owned lattices decide rounds pairwise (u_table)
+    int local_ring;             // launcher-set: one CTA holds every lattice, round words in shared memory
     // Sharded across GPUs (world > 1): R above counts this rank's lattices
     // (global rows row_lo ..), slots and pairs range over R_total.  Each
     // round's (S, Bond) by slot goes to every rank's pub buffer (peer memory
@@ -148,6 +150,7 @@ int launch_cb_cluster_smem(const ResidentArgs& a, cudaStream_t s);
 // resident_reg.cu: 64^2 ferro lattices held in registers, one warp each
 // (grid CTAs of `threads`); returns 1 when it does not apply
 int launch_cb_resident_reg64(const ResidentArgs& a, int grid, int threads, cudaStream_t s);
+int launch_cb_resident_reg32(const ResidentArgs& a, int grid, int threads, cudaStream_t s);
 // workspace of the point-to-point rounds: the swap draws of n_rounds rounds
 int64_t resident_ws_bytes(int64_t R, int64_t n_rounds);
 void fill_class_plan(uint32_t always_mask, int* n_up, int* k, int* sf, int* cls, int* ferro);

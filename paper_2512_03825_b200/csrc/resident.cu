@@ -831,6 +831,10 @@ static int launch_resident_t(const ResidentArgs& a, int sms, cudaStream_t s) {
             const int rc = launch_cb_resident_reg64(args, grid, threads, s);
             if (rc != 1) return rc;
         }
+        if (args.warp_lat && a.ferro && a.L == 32) {  // 32^2 ferro lattices (C1): the same
+            const int rc = launch_cb_resident_reg32(args, grid, threads, s);
+            if (rc != 1) return rc;
+        }
         // point-to-point rounds (cb_resident_p2p_kernel): warp-owned lattices, one
         // per warp, one GPU, a swap-draw table; PTMH_RESIDENT_P2P=0 turns it off
         const char* ep = getenv("PTMH_RESIDENT_P2P");

@@ -365,6 +365,35 @@ def test_resident_large_lattices_non_ferro(mods, J, B):
         assert np.array_equal(rec.slot_to_row, ref.slot_to_row)
 
 
+@pytest.mark.parametrize("R,sweeps,every,rec_every,J", [
+    (8, 40, 1, 2, 1.0),     # C1's shape
+    (3, 25, 1, 5, 1.0),
+    (77, 9, 2, 3, 1.0),     # several lattices per CTA, ragged
+    (5, 11, 0, 11, 1.0),    # no exchanges
+    (6, 15, 1, 5, 0.5),
+])
+def test_reg32_kernel_matches_oracle(mods, R, sweeps, every, rec_every, J):
+    """cb_resident_reg32_kernel (32^2 ferro lattices held in registers, a warp
+    each: 16 lanes own a word of both colours, neighbour rows by shuffles and
+    segment shifts) against the oracle; the launch is asserted."""
+    p = mods[0]
+    from paper_2512_03825_b200 import _lib
+    L, seed = 32, 900 + R
+    cfg = p.SimulationConfig(side=L, replicas=R, iterations=sweeps * L * L, swap_interval=every * L * L,
+                             seed=seed, params=p.IsingParams(J=J, B=0.0), sweep_mode="checkerboard",
+                             record_every=rec_every, return_final_state=True, kernel="resident")
+    rec = p.run(cfg)
+    assert rec.valid, rec.error
+    assert _lib.cb_last_launch()["kind"] == 10
+    ref = oracle.run_checkerboard(L, R, sweeps, every, seed, J=J, record_every=rec_every)
+    assert np.array_equal(rec.final_spins, ref.final_spins)
+    assert np.array_equal(rec.slot_to_row, ref.slot_to_row)
+    assert np.array_equal(rec.energies, ref.energies)
+    assert np.array_equal(rec.magnetizations, ref.magnetizations)
+    assert (rec.swap_rounds, rec.swaps_attempted, rec.swaps_accepted) == \
+        (ref.swap_rounds, ref.swaps_attempted, ref.swaps_accepted)
+
+
 def test_resident_segments_compose(mods):
     """Two resident segments == one resident run == the sweep-kernel path."""
     p, engine, _, _ = mods
