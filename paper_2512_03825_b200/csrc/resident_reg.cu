@@ -115,25 +115,6 @@ __device__ __forceinline__ void reg64_pass(uint32_t (&C)[2][2], const uint32_t (
     }
 }
 
-// The rounds and observations of a run segment without a 64-bit division per
-// sweep: (done / every, done % every) are kept incrementally (done = t + 1).
-struct RegSchedule {
-    int64_t every, q, r;  // every > 0: done = q * every + r
-    __device__ void init(int64_t ev, int64_t done0) {
-        every = ev;
-        q = ev > 0 ? done0 / ev : 0;
-        r = ev > 0 ? done0 - q * ev : 1;
-    }
-    __device__ bool hit() const { return every > 0 && r == 0; }  // done % every == 0
-    __device__ int64_t index() const { return q - 1; }           // done / every - 1 at a hit
-    __device__ void step() {
-        if (every > 0 && ++r == every) {
-            r = 0;
-            ++q;
-        }
-    }
-};
-
 // Lane 0 of a warp that owns a lattice, after a sweep whose (S, Bond) it
 // holds: the final stats, the observables by slot and the point-to-point
 // round (resident.cu, rounds.cuh); nk / n3 / n4 receive the lattice's slot
@@ -231,7 +212,7 @@ __global__ void __launch_bounds__(kThreads) cb_resident_reg64_kernel(ResidentArg
     uint32_t TM[8], TC[8];
     reg64_planes(t3, t4, TM, TC);
     int rounds = 0;
-    RegSchedule sx, sr;
+    RunSchedule sx, sr;
     sx.init(A.swap_every, A.first_sweep + 1);
     sr.init(A.record_every, A.first_sweep + 1);
     for (int64_t t = A.first_sweep; t < A.first_sweep + A.n_sweeps; ++t, sx.step(), sr.step()) {
@@ -388,7 +369,7 @@ __global__ void __launch_bounds__(kThreads) cb_resident_reg32_kernel(ResidentArg
     uint32_t TM[8], TC[8];
     reg64_planes(t3, t4, TM, TC);
     int rounds = 0;
-    RegSchedule sx, sr;
+    RunSchedule sx, sr;
     sx.init(A.swap_every, A.first_sweep + 1);
     sr.init(A.record_every, A.first_sweep + 1);
     for (int64_t t = A.first_sweep; t < A.first_sweep + A.n_sweeps; ++t, sx.step(), sr.step()) {

@@ -220,10 +220,13 @@ __global__ void __launch_bounds__(kThreads) cb_cluster_smem_kernel(ResidentArgs 
     // release/acquire phase flags pushed into the neighbours' shared memory
     // cost ~2x more per phase.)
     int rounds = 0;
-    for (int64_t t = A.first_sweep; t < A.first_sweep + A.n_sweeps; ++t) {
+    RunSchedule sx, sr;
+    sx.init(A.swap_every, A.first_sweep + 1);
+    sr.init(A.record_every, A.first_sweep + 1);
+    for (int64_t t = A.first_sweep; t < A.first_sweep + A.n_sweeps; ++t, sx.step(), sr.step()) {
         const int64_t done = t + 1;
-        const bool rec = A.record_every > 0 && done % A.record_every == 0;
-        const bool exch = A.swap_every > 0 && done % A.swap_every == 0 && done < A.total_sweeps;
+        const bool rec = sr.hit();
+        const bool exch = sx.hit() && done < A.total_sweeps;
         const bool last = t + 1 == A.first_sweep + A.n_sweeps;
         const bool need_stats = rec || exch || last;
         const int par = (int)(t & 1);
@@ -237,8 +240,8 @@ __global__ void __launch_bounds__(kThreads) cb_cluster_smem_kernel(ResidentArgs 
         if (threadIdx.x == 0) {
             k = (int)s_mask[18];
             if (exch) {
-                round = done / A.swap_every - 1;
-                const int first = (int)(round % 2), n_pairs = (R - first) / 2;
+                round = sx.index();
+                const int first = (int)(round & 1), n_pairs = (R - first) / 2;
                 if (k >= first && (k - first) / 2 < n_pairs) {
                     const int p = (k - first) / 2;
                     si = first + 2 * p;
@@ -282,7 +285,7 @@ __global__ void __launch_bounds__(kThreads) cb_cluster_smem_kernel(ResidentArgs 
             const int64_t S = part0[0], Bd = part0[1];
             if (q == 0) {
                 if (exch) {  // first: the partner is waiting for it
-                    const int64_t ro = (round % kRing) * (int64_t)R;
+                    const int64_t ro = (round & (kRing - 1)) * (int64_t)R;
                     const uint64_t mine = p2p_pack(S, Bd, round);
                     if (multi) {
                         for (int g = 0; g < A.world; ++g)
@@ -296,7 +299,7 @@ __global__ void __launch_bounds__(kThreads) cb_cluster_smem_kernel(ResidentArgs 
                     A.stats[2 * row + 1] = Bd;
                 }
                 if (rec) {  // by slot, before the round (executor.py order)
-                    const int64_t col = done / A.record_every - 1;
+                    const int64_t col = sr.index();
                     A.obs_e[(int64_t)k * A.ncols + col] =
                         __dsub_rn(__dmul_rn(A.B, (double)S), __dmul_rn(A.J, (double)Bd));
                     A.obs_m[(int64_t)k * A.ncols + col] = __ddiv_rn((double)S, (double)A.L * A.L);
@@ -304,7 +307,7 @@ __global__ void __launch_bounds__(kThreads) cb_cluster_smem_kernel(ResidentArgs 
             }
             if (other >= 0) {
                 const uint64_t want = (uint64_t)((round & 0x7fff) | 0x8000);
-                const uint64_t* src = ring + (round % kRing) * (int64_t)R + other;
+                const uint64_t* src = ring + (round & (kRing - 1)) * (int64_t)R + other;
                 uint64_t v = multi ? ld_relaxed_sys_u64(src) : ld_relaxed_u64(src);
                 while ((v & 0xffffull) != want) {
                     __nanosleep(32);

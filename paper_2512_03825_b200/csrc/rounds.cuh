@@ -66,4 +66,23 @@ __device__ __forceinline__ bool swap_decide(double bd, double Ei, double Ej, dou
     return u < prob;
 }
 
+// The rounds and observations of a run segment without a 64-bit division per
+// sweep: (done / every, done % every) are kept incrementally (done = t + 1).
+struct RunSchedule {
+    int64_t every, q, r;  // every > 0: done = q * every + r
+    __device__ void init(int64_t ev, int64_t done0) {
+        every = ev;
+        q = ev > 0 ? done0 / ev : 0;
+        r = ev > 0 ? done0 - q * ev : 1;
+    }
+    __device__ bool hit() const { return every > 0 && r == 0; }  // done % every == 0
+    __device__ int64_t index() const { return q - 1; }           // done / every - 1 at a hit
+    __device__ void step() {
+        if (every > 0 && ++r == every) {
+            r = 0;
+            ++q;
+        }
+    }
+};
+
 }  // namespace ptmh
