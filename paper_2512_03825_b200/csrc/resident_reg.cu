@@ -121,9 +121,28 @@ __device__ __forceinline__ void reg64_pass(uint32_t (&C)[2][2], const uint32_t (
 // and thresholds for the next sweep.
 // local: the ring is in the CTA's shared memory (every lattice of the run in
 // one CTA), so the round word is a volatile shared store / poll.
+// pre: the round's partner-independent inputs if loaded already (RoundIn::
+// load), or null to load them here (loading them before the sweep, held in
+// registers across it, measured slower at C5: 6.55 -> 6.80 us).
+struct RoundIn {
+    double u, bi, bj;
+    uint32_t ot3, ot4;
+    __device__ void load(const ResidentArgs& A, int R, int64_t round, int k) {
+        const int first = (int)(round & 1), n_pairs = (R - first) / 2;
+        if (k < first || (k - first) / 2 >= n_pairs) return;
+        const int p = (k - first) / 2, i = first + 2 * p, other = k == i ? i + 1 : i;
+        u = A.u_table[(round - A.u_round0) * A.u_stride + p];
+        bi = A.betas[i];
+        bj = A.betas[i + 1];
+        ot3 = __ldg(A.thresh + other * 10 + 8);
+        ot4 = __ldg(A.thresh + other * 10 + 9);
+    }
+};
+
 __device__ __forceinline__ void reg_round(const ResidentArgs& A, uint64_t* ring, int R, bool multi, bool local,
                                           int row, int64_t round, int64_t col, bool rec, bool exch, bool last, int k,
-                                          int64_t S, int64_t Bd, int& nk, uint32_t& n3, uint32_t& n4) {
+                                          int64_t S, int64_t Bd, int& nk, uint32_t& n3, uint32_t& n4,
+                                          const RoundIn* pre = nullptr) {
     static_assert((kRing & (kRing - 1)) == 0, "ring depth: a power of two");
     uint64_t* const slot_word = ring + (round & (kRing - 1)) * (int64_t)R;
     if (exch) {  // first: the partner is waiting for it
@@ -150,9 +169,10 @@ __device__ __forceinline__ void reg_round(const ResidentArgs& A, uint64_t* ring,
     if (exch && k >= first && (k - first) / 2 < n_pairs) {
         // everything that does not need the partner's energy, while its word travels
         const int p = (k - first) / 2, i = first + 2 * p, other = k == i ? i + 1 : i;
-        const double u = A.u_table[(round - A.u_round0) * A.u_stride + p];
-        const double bi = A.betas[i], bj = A.betas[i + 1];
-        const uint32_t ot3 = __ldg(A.thresh + other * 10 + 8), ot4 = __ldg(A.thresh + other * 10 + 9);
+        RoundIn in;
+        if (pre) in = *pre; else in.load(A, R, round, k);
+        const double u = in.u, bi = in.bi, bj = in.bj;
+        const uint32_t ot3 = in.ot3, ot4 = in.ot4;
         const uint64_t want = (uint64_t)((round & 0x7fff) | 0x8000);
         auto poll = [&]() -> uint64_t {
             if (local) return *reinterpret_cast<volatile const uint64_t*>(slot_word + other);
@@ -267,7 +287,12 @@ int launch_cb_resident_reg64(const ResidentArgs& a, int grid, int threads, cudaS
     if (threads > 1024 || (int64_t)(a.R + grid - 1) / grid > threads / 32) return 1;
     if (a.swap_every > 0 && a.world == 1) PTMH_CUDA(cudaMemsetAsync(a.slot_stats, 0, (size_t)kRing * a.R * 8, s));
     void* kargs[] = {const_cast<ResidentArgs*>(&a)};
-    PTMH_CUDA(cudaLaunchCooperativeKernel((const void*)cb_resident_reg64_kernel<1024>, grid, threads, kargs, 0, s));
+    // C5's CTAs hold 28 lattices (896 threads): the 896-thread build may use
+    // 72 registers instead of 64 (PTMH_RESIDENT_REG896=0: the 1024 build, A/B)
+    const char* e9 = getenv("PTMH_RESIDENT_REG896");
+    const void* fn = threads <= 896 && !(e9 && e9[0] == '0') ? (const void*)cb_resident_reg64_kernel<896>
+                                                              : (const void*)cb_resident_reg64_kernel<1024>;
+    PTMH_CUDA(cudaLaunchCooperativeKernel(fn, grid, threads, kargs, 0, s));
     cb_set_last_launch(CbLaunchInfo{9, 2, threads, 1, 0, grid});
     return PTMH_OK;
 }
