@@ -1,6 +1,7 @@
 """Randomised A/B of the persistent sweep kernel against the per-launch
 kernels (bit-exact lattices and stats), over shapes, row permutations, sweep
-ranges and the PTMH_PERSIST_* knobs: `python tools/fuzz_persistent.py [n] [seed]`."""
+ranges and the PTMH_PERSIST_* knobs (temporally blocked items included):
+`python tools/fuzz_persistent.py [n] [seed]`."""
 import os
 import sys
 
@@ -14,7 +15,8 @@ from paper_2512_03825_b200.engine import CheckerboardEngine  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 30
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
-knobs = ("PTMH_PERSIST_ROWS", "PTMH_PERSIST_THREADS", "PTMH_PERSIST_BANDS", "PTMH_PERSIST_ITEMS_PER_SLOT")
+knobs = ("PTMH_PERSIST_ROWS", "PTMH_PERSIST_THREADS", "PTMH_PERSIST_BANDS", "PTMH_PERSIST_ITEMS_PER_SLOT",
+         "PTMH_PERSIST_TB")
 bad = 0
 for case in range(n):
     L = int(rng.choice([1024, 1536, 2048]))
@@ -23,7 +25,8 @@ for case in range(n):
     env = {"PTMH_PERSIST_ROWS": str(rng.choice(["", "2", "4", "8", "16", "32"])),
            "PTMH_PERSIST_THREADS": str(rng.choice(["", "128", "256"])),
            "PTMH_PERSIST_BANDS": str(rng.choice(["", "0", "1"])),
-           "PTMH_PERSIST_ITEMS_PER_SLOT": str(rng.choice(["", "0", "1"]))}
+           "PTMH_PERSIST_ITEMS_PER_SLOT": str(rng.choice(["", "0", "1"])),
+           "PTMH_PERSIST_TB": str(rng.choice(["", "0", "1"]))}
     for k in knobs:
         if env[k]:
             os.environ[k] = env[k]
