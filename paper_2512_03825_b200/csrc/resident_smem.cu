@@ -56,69 +56,41 @@ __device__ __forceinline__ int band_word(int rl, int k, int WR, int NS) {
 // word column k.  own / oth: this CTA's planes; up_row / dn_row: the other
 // colour's row above / below the band (a neighbour CTA's shared memory, or
 // this CTA's own when the cluster is one CTA), as word-column arrays.
-template <int kRows, int kColor, bool kStats>
-__device__ __forceinline__ void smem_strip(uint32_t* __restrict__ own, const uint32_t* __restrict__ oth,
-                                           const uint32_t* up_row, const uint32_t* dn_row, int s, int WR,
-                                           int wr_shift, int NS, int band_lo, const uint32_t (&TM)[8],
-                                           const uint32_t (&TC)[8], uint32_t t3, uint32_t t4, uint32_t slot,
-                                           const RoundKeys32& rk, uint32_t ctr1, uint32_t (&tie_m)[kRows][32],
-                                           uint32_t (&tie_k4)[kRows][32], uint32_t (&tie_sn)[kRows][32],
-                                           int& sumS, int& sumB) {
-    const int lane = threadIdx.x & 31;
+// The strip's random planes (two Philox4x32-10 blocks per row word).  They
+// do not depend on the spins, so the kernel draws them ahead of the pass
+// where a thread owns one strip (smem_draws below): between the arrive and
+// the wait of the cluster barrier before the pass, and during the round for
+// the next sweep's colour 0.
+template <int kRows>
+__device__ __forceinline__ void smem_draws(int s, int WR, int wr_shift, int band_lo, uint32_t slot,
+                                           const RoundKeys32& rk, uint32_t ctr1, uint32_t (&U)[kRows][8]) {
     const int sr = wr_shift >= 0 ? s >> wr_shift : s / WR;
     const int k = s - sr * WR;
-    const bool top = sr == 0, bottom = s >= NS - WR;
-    const int kl = (k == 0) ? WR - 1 : k - 1;
-    const int kr = (k == WR - 1) ? 0 : k + 1;
-    const int i0 = band_lo + sr * kRows;
-    uint32_t up = top ? up_row[k] : oth[(kRows - 1) * NS + s - WR];
-    uint32_t mid = oth[s];
-    uint32_t tie_rows = 0;
 #pragma unroll
     for (int rr = 0; rr < kRows; ++rr) {
-        const int i = i0 + rr;
-        const bool even = ((i + kColor) & 1) == 0;
-        const uint32_t dn = rr + 1 < kRows ? oth[(rr + 1) * NS + s] : (bottom ? dn_row[k] : oth[s + WR]);
-        const uint32_t adj = oth[rr * NS + s - k + (even ? kl : kr)];
-        const uint32_t S = own[rr * NS + s];
-        const uint32_t hz = even ? __funnelshift_l(adj, mid, 1)   // m sees m-1
-                                 : __funnelshift_r(mid, adj, 1);  // m sees m+1
-        const uint32_t a = ~(S ^ up), b = ~(S ^ dn), c = ~(S ^ mid), d = ~(S ^ hz);
-        const uint32_t s1 = a ^ b, c1 = a & b, s2 = c ^ d, c2 = c & d;
-        const uint32_t k0 = s1 ^ s2, c3 = s1 & s2;
-        const uint32_t k1 = c1 ^ c2 ^ c3, K4 = c1 & c2;
-        const uint32_t upm = (k1 & k0) | K4;  // k = 3, 4
-        const uint32_t K2 = k1 & ~k0;         // k = 2: dE = 0
-        uint32_t acc = ~(k1 | K4);            // k = 0, 1: dE < 0
-        const uint32_t w32 = (uint32_t)(i * WR + k);
+        const uint32_t w32 = (uint32_t)((band_lo + sr * kRows + rr) * WR + k);
         const uint4 r0 = philox4x32_10(make_uint4(2u * w32, ctr1, slot, 0u), rk);
         const uint4 r1 = philox4x32_10(make_uint4(2u * w32 + 1u, ctr1, slot, 0u), rk);
-        const uint32_t U[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
-        acc |= K2 & ~U[0];
-        uint32_t bor = 0, eq = upm;
-#pragma unroll
-        for (int p = 7; p >= 0; --p) {
-            const uint32_t Tm = K4 * TM[p] + TC[p];
-            bor = (~U[p] & Tm) | (~U[p] & bor) | (Tm & bor);
-            eq &= ~(U[p] ^ Tm);
-        }
-        acc |= bor & upm;
-        const uint32_t Sn = S ^ acc;
-        tie_m[rr][lane] = eq;
-        tie_k4[rr][lane] = K4;
-        tie_sn[rr][lane] = Sn;
-        if (eq) tie_rows |= 1u << rr;
-        if (acc) own[rr * NS + s] = Sn;
-        if (kStats) {
-            const int kk = __popc(a ^ acc) + __popc(b ^ acc) + __popc(c ^ acc) + __popc(d ^ acc);
-            sumB += 2 * kk - 128;
-            sumS += 2 * (__popc(Sn) + __popc(mid)) - 64;
-        }
-        up = mid;
-        mid = dn;
+        U[rr][0] = r0.x;
+        U[rr][1] = r0.y;
+        U[rr][2] = r0.z;
+        U[rr][3] = r0.w;
+        U[rr][4] = r1.x;
+        U[rr][5] = r1.y;
+        U[rr][6] = r1.z;
+        U[rr][7] = r1.w;
     }
-    // ties (top byte equal): the lane walks its own, the warp iterates
-    // max-ties-per-lane times (strip.cuh)
+}
+
+// ties (top byte equal): the lane walks its own, the warp iterates
+// max-ties-per-lane times (strip.cuh)
+template <int kRows, bool kStats>
+__device__ __forceinline__ void smem_ties(uint32_t* __restrict__ own, int s, int WR, int NS, int i0, int k,
+                                          uint32_t tie_rows, uint32_t t3, uint32_t t4, uint32_t slot,
+                                          const RoundKeys32& rk, uint32_t ctr1, uint32_t (&tie_m)[kRows][32],
+                                          uint32_t (&tie_k4)[kRows][32], uint32_t (&tie_sn)[kRows][32],
+                                          int& sumS, int& sumB) {
+    const int lane = threadIdx.x & 31;
     int rr = -1;
     uint32_t m = 0, mk4 = 0, Sw = 0, w32 = 0;
     bool dirty = false;
@@ -151,6 +123,78 @@ __device__ __forceinline__ void smem_strip(uint32_t* __restrict__ own, const uin
     }
 }
 
+template <int kRows, int kColor, bool kStats, bool kPre = false>
+__device__ __forceinline__ void smem_strip(uint32_t* __restrict__ own, const uint32_t* __restrict__ oth,
+                                           const uint32_t* up_row, const uint32_t* dn_row, int s, int WR,
+                                           int wr_shift, int NS, int band_lo, const uint32_t (&TM)[8],
+                                           const uint32_t (&TC)[8], uint32_t t3, uint32_t t4, uint32_t slot,
+                                           const RoundKeys32& rk, uint32_t ctr1, uint32_t (&tie_m)[kRows][32],
+                                           uint32_t (&tie_k4)[kRows][32], uint32_t (&tie_sn)[kRows][32],
+                                           int& sumS, int& sumB, const uint32_t (*Upre)[8] = nullptr) {
+    const int lane = threadIdx.x & 31;
+    const int sr = wr_shift >= 0 ? s >> wr_shift : s / WR;
+    const int k = s - sr * WR;
+    const bool top = sr == 0, bottom = s >= NS - WR;
+    const int kl = (k == 0) ? WR - 1 : k - 1;
+    const int kr = (k == WR - 1) ? 0 : k + 1;
+    const int i0 = band_lo + sr * kRows;
+    uint32_t up = top ? up_row[k] : oth[(kRows - 1) * NS + s - WR];
+    uint32_t mid = oth[s];
+    uint32_t tie_rows = 0;
+#pragma unroll
+    for (int rr = 0; rr < kRows; ++rr) {
+        const int i = i0 + rr;
+        const bool even = ((i + kColor) & 1) == 0;
+        const uint32_t dn = rr + 1 < kRows ? oth[(rr + 1) * NS + s] : (bottom ? dn_row[k] : oth[s + WR]);
+        const uint32_t adj = oth[rr * NS + s - k + (even ? kl : kr)];
+        const uint32_t S = own[rr * NS + s];
+        const uint32_t hz = even ? __funnelshift_l(adj, mid, 1)   // m sees m-1
+                                 : __funnelshift_r(mid, adj, 1);  // m sees m+1
+        const uint32_t a = ~(S ^ up), b = ~(S ^ dn), c = ~(S ^ mid), d = ~(S ^ hz);
+        const uint32_t s1 = a ^ b, c1 = a & b, s2 = c ^ d, c2 = c & d;
+        const uint32_t k0 = s1 ^ s2, c3 = s1 & s2;
+        const uint32_t k1 = c1 ^ c2 ^ c3, K4 = c1 & c2;
+        const uint32_t upm = (k1 & k0) | K4;  // k = 3, 4
+        const uint32_t K2 = k1 & ~k0;         // k = 2: dE = 0
+        uint32_t acc = ~(k1 | K4);            // k = 0, 1: dE < 0
+        uint32_t U[8];
+        if constexpr (kPre) {
+#pragma unroll
+            for (int p = 0; p < 8; ++p) U[p] = Upre[rr][p];
+        } else {
+            const uint32_t w32 = (uint32_t)(i * WR + k);
+            const uint4 r0 = philox4x32_10(make_uint4(2u * w32, ctr1, slot, 0u), rk);
+            const uint4 r1 = philox4x32_10(make_uint4(2u * w32 + 1u, ctr1, slot, 0u), rk);
+            U[0] = r0.x; U[1] = r0.y; U[2] = r0.z; U[3] = r0.w;
+            U[4] = r1.x; U[5] = r1.y; U[6] = r1.z; U[7] = r1.w;
+        }
+        acc |= K2 & ~U[0];
+        uint32_t bor = 0, eq = upm;
+#pragma unroll
+        for (int p = 7; p >= 0; --p) {
+            const uint32_t Tm = K4 * TM[p] + TC[p];
+            bor = (~U[p] & Tm) | (~U[p] & bor) | (Tm & bor);
+            eq &= ~(U[p] ^ Tm);
+        }
+        acc |= bor & upm;
+        const uint32_t Sn = S ^ acc;
+        tie_m[rr][lane] = eq;
+        tie_k4[rr][lane] = K4;
+        tie_sn[rr][lane] = Sn;
+        if (eq) tie_rows |= 1u << rr;
+        if (acc) own[rr * NS + s] = Sn;
+        if (kStats) {
+            const int kk = __popc(a ^ acc) + __popc(b ^ acc) + __popc(c ^ acc) + __popc(d ^ acc);
+            sumB += 2 * kk - 128;
+            sumS += 2 * (__popc(Sn) + __popc(mid)) - 64;
+        }
+        up = mid;
+        mid = dn;
+    }
+    smem_ties<kRows, kStats>(own, s, WR, NS, i0, k, tie_rows, t3, t4, slot, rk, ctr1, tie_m, tie_k4, tie_sn, sumS,
+                             sumB);
+}
+
 // the threshold-plane select coefficients of slot k (strip.cuh: Tm = K4 * TM + TC)
 __device__ __forceinline__ void smem_set_slot(int k, uint32_t t3, uint32_t t4,
                                               uint32_t* s_mask) {
@@ -165,11 +209,12 @@ __device__ __forceinline__ void smem_set_slot(int k, uint32_t t3, uint32_t t4,
     s_mask[18] = (uint32_t)k;
 }
 
-template <int kRows, int kThreads, int kColor, bool kStats>
+template <int kRows, int kThreads, int kColor, bool kStats, bool kPre = false>
 __device__ __forceinline__ void smem_pass(const ResidentArgs& A, uint32_t* s_lat, const uint32_t* up_pl,
                                           const uint32_t* dn_pl, int BW, int NS, int band_lo, int wr_shift,
                                           const uint32_t* s_mask, uint32_t ctr1,
-                                          uint32_t (&s_tie)[kThreads / 32][3][kRows][32], int& sS, int& sB) {
+                                          uint32_t (&s_tie)[kThreads / 32][3][kRows][32], int& sS, int& sB,
+                                          const uint32_t (*Upre)[8] = nullptr) {
     uint32_t TM[8], TC[8];
 #pragma unroll
     for (int p = 0; p < 8; ++p) {
@@ -183,12 +228,24 @@ __device__ __forceinline__ void smem_pass(const ResidentArgs& A, uint32_t* s_lat
     // the neighbours' other-colour rows: band-1 of the CTA above, 0 of the one below
     const uint32_t* up_row = up_pl + (1 - kColor) * BW + (kRows - 1) * NS + NS - WR;
     const uint32_t* dn_row = dn_pl + (1 - kColor) * BW;
-    for (int s = (int)threadIdx.x; s < NS; s += (int)blockDim.x)
-        smem_strip<kRows, kColor, kStats>(own, oth, up_row, dn_row, s, WR, wr_shift, NS, band_lo, TM, TC, t3, t4,
-                                          slot, A.rk, ctr1, s_tie[wq][0], s_tie[wq][1], s_tie[wq][2], sS, sB);
+    if constexpr (kPre) {  // one strip per thread (NS == blockDim.x), planes drawn ahead
+        smem_strip<kRows, kColor, kStats, true>(own, oth, up_row, dn_row, (int)threadIdx.x, WR, wr_shift, NS,
+                                                band_lo, TM, TC, t3, t4, slot, A.rk, ctr1, s_tie[wq][0],
+                                                s_tie[wq][1], s_tie[wq][2], sS, sB, Upre);
+    } else {
+        for (int s = (int)threadIdx.x; s < NS; s += (int)blockDim.x)
+            smem_strip<kRows, kColor, kStats>(own, oth, up_row, dn_row, s, WR, wr_shift, NS, band_lo, TM, TC, t3,
+                                              t4, slot, A.rk, ctr1, s_tie[wq][0], s_tie[wq][1], s_tie[wq][2], sS,
+                                              sB);
+    }
 }
 
-template <int kRows, int kThreads>
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+
+// kPre: one strip per thread (NS == blockDim.x); the random planes of each
+// pass are drawn ahead, off the critical path (smem_draws)
+template <int kRows, int kThreads, bool kPre = false>
 __global__ void __launch_bounds__(kThreads) cb_cluster_smem_kernel(ResidentArgs A) {
     extern __shared__ uint32_t s_lat[];  // [2][band * WR], band_word layout
     __shared__ uint32_t s_mask[19];      // TM[8], TC[8], t3, t4, slot
@@ -220,6 +277,12 @@ __global__ void __launch_bounds__(kThreads) cb_cluster_smem_kernel(ResidentArgs 
     // release/acquire phase flags pushed into the neighbours' shared memory
     // cost ~2x more per phase.)
     int rounds = 0;
+    // kPre: the next colour-0 pass's planes, for the lattice's slot (U0) and,
+    // across a round, for the partner's slot too (U0x, taken if the swap is
+    // accepted); the colour-1 pass's (U1)
+    uint32_t U0[kRows][8], U0x[kRows][8], U1[kRows][8];
+    if constexpr (kPre)
+        smem_draws<kRows>((int)threadIdx.x, WR, wr_shift, band_lo, s_mask[18], A.rk, (uint32_t)(2 * A.first_sweep), U0);
     RunSchedule sx, sr;
     sx.init(A.swap_every, A.first_sweep + 1);
     sr.init(A.record_every, A.first_sweep + 1);
@@ -263,12 +326,19 @@ __global__ void __launch_bounds__(kThreads) cb_cluster_smem_kernel(ResidentArgs 
         }
         int* const part0 = cluster.map_shared_rank(&s_part[par][0], 0);
         int sS = 0, sB = 0;
-        smem_pass<kRows, kThreads, 0, false>(A, s_lat, up_pl, dn_pl, BW, NS, band_lo, wr_shift, s_mask,
-                                             (uint32_t)(2 * t), s_tie, sS, sB);
-        cluster.sync();
+        smem_pass<kRows, kThreads, 0, false, kPre>(A, s_lat, up_pl, dn_pl, BW, NS, band_lo, wr_shift, s_mask,
+                                                   (uint32_t)(2 * t), s_tie, sS, sB, U0);
+        if constexpr (kPre) {  // colour 1's planes while the cluster catches up
+            const uint32_t slot = s_mask[18];
+            cluster_arrive();
+            smem_draws<kRows>((int)threadIdx.x, WR, wr_shift, band_lo, slot, A.rk, (uint32_t)(2 * t + 1), U1);
+            cluster_wait();
+        } else {
+            cluster.sync();
+        }
         if (need_stats) {
-            smem_pass<kRows, kThreads, 1, true>(A, s_lat, up_pl, dn_pl, BW, NS, band_lo, wr_shift, s_mask,
-                                                (uint32_t)(2 * t + 1), s_tie, sS, sB);
+            smem_pass<kRows, kThreads, 1, true, kPre>(A, s_lat, up_pl, dn_pl, BW, NS, band_lo, wr_shift, s_mask,
+                                                      (uint32_t)(2 * t + 1), s_tie, sS, sB, U1);
             sS = __reduce_add_sync(kFullMask, sS);
             sB = __reduce_add_sync(kFullMask, sB);
             if ((threadIdx.x & 31) == 0) {  // DSMEM atomics into rank 0's sums
@@ -276,10 +346,34 @@ __global__ void __launch_bounds__(kThreads) cb_cluster_smem_kernel(ResidentArgs 
                 atomicAdd(part0 + 1, sB);
             }
         } else {
-            smem_pass<kRows, kThreads, 1, false>(A, s_lat, up_pl, dn_pl, BW, NS, band_lo, wr_shift, s_mask,
-                                                 (uint32_t)(2 * t + 1), s_tie, sS, sB);
+            smem_pass<kRows, kThreads, 1, false, kPre>(A, s_lat, up_pl, dn_pl, BW, NS, band_lo, wr_shift, s_mask,
+                                                       (uint32_t)(2 * t + 1), s_tie, sS, sB, U1);
         }
-        cluster.sync();  // colour 1 done everywhere, rank 0's sums complete
+        // colour 1 done everywhere, rank 0's sums complete
+        uint32_t cur = 0, alt = 0;
+        if constexpr (kPre) {
+            // the next colour 0's planes while the cluster catches up: for the
+            // lattice's slot and, if it is paired in this sweep's round, for
+            // the partner's (the round may hand the lattice that slot)
+            cur = s_mask[18];  // (read before arriving: thread 0 may update it once the cluster has arrived)
+            cluster_arrive();
+            alt = cur;
+            if (exch) {
+                const int64_t rd = sx.index();
+                const int first = (int)(rd & 1), n_pairs = (R - first) / 2;
+                const int kc = (int)cur;
+                if (kc >= first && (kc - first) / 2 < n_pairs) {
+                    const int si0 = first + 2 * ((kc - first) / 2);
+                    alt = (uint32_t)(kc == si0 ? si0 + 1 : si0);
+                }
+            }
+            const uint32_t c0n = (uint32_t)(2 * t + 2);
+            smem_draws<kRows>((int)threadIdx.x, WR, wr_shift, band_lo, cur, A.rk, c0n, U0);
+            if (alt != cur) smem_draws<kRows>((int)threadIdx.x, WR, wr_shift, band_lo, alt, A.rk, c0n, U0x);
+            cluster_wait();
+        } else {
+            cluster.sync();
+        }
         if (!need_stats) continue;
         if (threadIdx.x == 0) {
             const int64_t S = part0[0], Bd = part0[1];
@@ -330,6 +424,14 @@ __global__ void __launch_bounds__(kThreads) cb_cluster_smem_kernel(ResidentArgs 
         }
         if (exch) ++rounds;
         __syncthreads();  // the next sweep reads s_mask
+        if constexpr (kPre) {
+            if (s_mask[18] != cur) {  // the swap was accepted: the partner slot's planes
+#pragma unroll
+                for (int rr = 0; rr < kRows; ++rr)
+#pragma unroll
+                    for (int p = 0; p < 8; ++p) U0[rr][p] = U0x[rr][p];
+            }
+        }
     }
     // the band back to global memory; the permutation where the grid-barrier
     // kernel would leave it (its buffer flips once per round)
@@ -347,6 +449,7 @@ __global__ void __launch_bounds__(kThreads) cb_cluster_smem_kernel(ResidentArgs 
     cluster.sync();  // no CTA leaves while a neighbour may still read its shared memory
 }
 
+
 template <int kRows, int kThreads>
 static int launch_smem_t(const ResidentArgs& a, int cs, cudaStream_t s) {
     const int band = a.L / cs;
@@ -354,7 +457,11 @@ static int launch_smem_t(const ResidentArgs& a, int cs, cudaStream_t s) {
     const int NS = band / kRows * a.WR;
     if (NS % 32 != 0) return kNotApplicable;  // whole warps walk their ties together
     const size_t smem = 2 * (size_t)band * a.WR * sizeof(uint32_t);
-    const void* fn = (const void*)cb_cluster_smem_kernel<kRows, kThreads>;
+    // one strip per thread: the planes drawn ahead (kPre); PTMH_SMEM_PRE=0 turns it off
+    const char* ep = getenv("PTMH_SMEM_PRE");
+    const bool pre = NS <= kThreads && !(ep && ep[0] == '0');
+    const void* fn = pre ? (const void*)cb_cluster_smem_kernel<kRows, kThreads, true>
+                         : (const void*)cb_cluster_smem_kernel<kRows, kThreads, false>;
     if (cs > 8) PTMH_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     if (smem > 48 * 1024)
         PTMH_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
