@@ -149,7 +149,8 @@ int ptmh_fill_lattices_parallel(int8_t *spins, int64_t rows, int64_t L,
 /* The sweep kernel the calling thread's last ptmh_cb_sweeps / _sync call
  * launched: info[0] = kind (0 none, 1 cb_sweeps_persistent<rows, threads>,
  * 2 cb_half_sweep_ferro<rows>, 3 cb_half_sweep_fast, 4 cb_half_sweep_generic;
- * info[4] = 2: temporally blocked items (ptmh_cb_sweeps_ws);
+ * info[4] = 2: temporally blocked items (ptmh_cb_sweeps_ws), 3: the same
+ * streamed through each band (states of more than 2^25 sites);
  * after a resident run: 5 cb_resident_kernel with grid-barrier rounds, 6
  * cb_resident_p2p_kernel, 7 cb_resident_kernel on clusters with
  * point-to-point rounds; info[1] = cluster size there; 8

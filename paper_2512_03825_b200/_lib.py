@@ -128,6 +128,6 @@ def cb_last_launch() -> dict:
              9: "cb_resident_reg64_kernel (64^2 lattices in registers, a warp each, point-to-point rounds)",
              10: "cb_resident_reg32_kernel (32^2 lattices in registers, a warp each, point-to-point rounds)"}
     k = kinds.get(v[0])
-    return {"kind": v[0], "rows": v[1], "threads": v[2], "group": v[3], "bands": bool(v[4]), "tb": v[4] == 2,
-            "grid": v[5], "name": k.format(r=v[1], t=v[2], g=v[3], tb=" (temporally blocked)" if v[4] == 2 else "")
+    return {"kind": v[0], "rows": v[1], "threads": v[2], "group": v[3], "bands": bool(v[4]), "tb": v[4] >= 2, "streamed": v[4] == 3,
+            "grid": v[5], "name": k.format(r=v[1], t=v[2], g=v[3], tb=" (temporally blocked)" if v[4] == 2 else " (temporally blocked, streamed)" if v[4] == 3 else "")
             if k else None}

@@ -317,7 +317,7 @@ __device__ __forceinline__ uint32_t ferro_word0(const uint32_t* __restrict__ in,
 // (band dependencies, below) or the shard is big, else 256 (the launcher).
 // tb: temporally blocked items (a separate instantiation: carrying both
 // item kinds in one kernel doubled its code and cost the per-colour path 2 %)
-template <int kRows, int kPT, bool tb = false>
+template <int kRows, int kPT, int tb = 0>
 __global__ void __launch_bounds__(kPT, PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_persistent(
     uint32_t* __restrict__ packed, int64_t rows, int L, int WR, int64_t W,
     const int32_t* __restrict__ row_to_slot, const uint32_t* __restrict__ thresh, const RoundKeys32 rk,
@@ -423,31 +423,55 @@ __global__ void __launch_bounds__(kPT, PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_pe
             const int band_rows = (int)(group * (kPT / WR) * kRows);
             const int band_lo = (int)sub * band_rows, band_hi = band_lo + band_rows;
             const uint32_t* pl = s_planes[it & 1];
-            for (uint32_t g = 0; g < group; ++g)
-                ferro_strip<kRows, 0, false, true, 1>(src, L, WR, W, row_to_slot, thresh, rk, c0, stats, esz, true,
-                                                      lat, (int)((sub * group + g) * kPT + threadIdx.x),
-                                                      tie_m[warp], tie_k4[warp], tie_sn[warp], sumS, sumB,
-                                                      wr_shift, pl, dstb);
-            for (int x = (int)threadIdx.x; x < 2 * WR; x += kPT) {
-                const int side = x >= WR, k = x - side * WR;
-                const int r = side ? (band_hi == L ? 0 : band_hi) : (band_lo == 0 ? L - 1 : band_lo - 1);
-                s_halo[side][k] = ferro_word0(src, L, WR, W, lat, r, k, pl, rk, c0);
-            }
-            __syncthreads();  // the band's colour-0 words (stored at L2) and the halo rows
             const bool last_sweep = phase + 1 == n_steps;
-#define PTMH_TB1(ST)                                                                                           \
-    for (uint32_t g = 0; g < group; ++g)                                                                       \
-        ferro_strip<kRows, 1, ST, false, 2>(src, L, WR, W, row_to_slot, thresh, rk, c0 + 1, stats, esz, true, \
-                                            lat, (int)((sub * group + g) * kPT + threadIdx.x), tie_m[warp],   \
-                                            tie_k4[warp], tie_sn[warp], sumS, sumB, wr_shift, pl, dstb,        \
-                                            s_halo[0], s_halo[1], band_lo, band_hi)
-            if (last_sweep) {
-                PTMH_TB1(true);
-                flush_stats(stats, lat, true, sumS, sumB);  // stats zeroed by the launcher
+#define PTMH_TB0(G)                                                                                            \
+    ferro_strip<kRows, 0, false, true, 1>(src, L, WR, W, row_to_slot, thresh, rk, c0, stats, esz, true, lat,  \
+                                          (int)((sub * group + (G)) * kPT + threadIdx.x), tie_m[warp],        \
+                                          tie_k4[warp], tie_sn[warp], sumS, sumB, wr_shift, pl, dstb)
+#define PTMH_TB1(G, ST)                                                                                        \
+    ferro_strip<kRows, 1, ST, false, 2>(src, L, WR, W, row_to_slot, thresh, rk, c0 + 1, stats, esz, true, lat, \
+                                        (int)((sub * group + (G)) * kPT + threadIdx.x), tie_m[warp],          \
+                                        tie_k4[warp], tie_sn[warp], sumS, sumB, wr_shift, pl, dstb, s_halo[0], \
+                                        s_halo[1], band_lo, band_hi)
+#define PTMH_TB_HALO()                                                                                         \
+    for (int x = (int)threadIdx.x; x < 2 * WR; x += kPT) {                                                     \
+        const int side = x >= WR, k = x - side * WR;                                                           \
+        const int r = side ? (band_hi == L ? 0 : band_hi) : (band_lo == 0 ? L - 1 : band_lo - 1);              \
+        s_halo[side][k] = ferro_word0(src, L, WR, W, lat, r, k, pl, rk, c0);                                   \
+    }
+            if constexpr (tb == 2) {
+                // large states: streamed through the band.  Step g updates
+                // colour 0 of block g and, after a barrier, colour 1 of block
+                // g - 1, whose rows below are then final: a CTA keeps about two
+                // blocks live in L2 (band at once, C4's 444 bands x 256 KB in
+                // flight outgrew L2)
+                for (uint32_t g = 0; g <= group; ++g) {
+                    if (g < group) PTMH_TB0(g);
+                    if (g == 0) PTMH_TB_HALO();
+                    // block g's colour-0 words (stored at L2) and the halo rows (the
+                    // last step's colour 1 reads nothing newer than step group - 1's)
+                    if (g < group) __syncthreads();
+                    if (g > 0) {
+                        if (last_sweep)
+                            PTMH_TB1(g - 1, true);
+                        else
+                            PTMH_TB1(g - 1, false);
+                    }
+                }
             } else {
-                PTMH_TB1(false);
+                for (uint32_t g = 0; g < group; ++g) PTMH_TB0(g);
+                PTMH_TB_HALO();
+                __syncthreads();  // the band's colour-0 words (stored at L2) and the halo rows
+                if (last_sweep) {
+                    for (uint32_t g = 0; g < group; ++g) PTMH_TB1(g, true);
+                } else {
+                    for (uint32_t g = 0; g < group; ++g) PTMH_TB1(g, false);
+                }
             }
+            if (last_sweep) flush_stats(stats, lat, true, sumS, sumB);  // stats zeroed by the launcher
+#undef PTMH_TB0
 #undef PTMH_TB1
+#undef PTMH_TB_HALO
             __syncthreads();  // every store of this item is issued before the release
             if (threadIdx.x == 0) red_release_gpu_add(band + (size_t)lat * subs + sub, 1u);
             continue;
@@ -862,11 +886,13 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
                 {(const void*)cb_sweeps_persistent<32, 128>, (const void*)cb_sweeps_persistent<16, 128>,
                  (const void*)cb_sweeps_persistent<8, 128>, (const void*)cb_sweeps_persistent<4, 128>,
                  (const void*)cb_sweeps_persistent<2, 128>}};
-            const void* fns_tb[5] = {(const void*)cb_sweeps_persistent<32, 128, true>,
-                                     (const void*)cb_sweeps_persistent<16, 128, true>,
-                                     (const void*)cb_sweeps_persistent<8, 128, true>,
-                                     (const void*)cb_sweeps_persistent<4, 128, true>,
-                                     (const void*)cb_sweeps_persistent<2, 128, true>};
+            const void* fns_tb[7] = {(const void*)cb_sweeps_persistent<32, 128, 1>,
+                                     (const void*)cb_sweeps_persistent<16, 128, 1>,
+                                     (const void*)cb_sweeps_persistent<8, 128, 1>,
+                                     (const void*)cb_sweeps_persistent<4, 128, 1>,
+                                     (const void*)cb_sweeps_persistent<2, 128, 1>,
+                                     (const void*)cb_sweeps_persistent<32, 128, 2>,
+                                     (const void*)cb_sweeps_persistent<16, 128, 2>};
             for (const void* fn : fns_tb)
                 if (t128)
                     PTMH_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -950,22 +976,30 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
         const bool tb = scratch != nullptr && kpt == 128 && kpt % WR == 0 &&
                         (etb ? etb[0] == '1' : rows * L * L <= (1LL << 25));
         const bool bands = tb || (kpt % WR == 0 && (eb ? eb[0] == '1' : rows * L * L < (1LL << 28)));
-        g_last_launch = CbLaunchInfo{1, krows, kpt, (int)group, tb ? 2 : (bands ? 1 : 0), (int)grid};
+        const bool stream = tb && rows * L * L > (1LL << 25) && (krows == 32 || krows == 16);
+        g_last_launch = CbLaunchInfo{1, krows, kpt, (int)group, tb ? (stream ? 3 : 2) : (bands ? 1 : 0), (int)grid};
         if (tb) PTMH_CUDA(cudaMemsetAsync(stats, 0, (size_t)rows * 2 * sizeof(int64_t), s));
 #define PTMH_PERSIST(K, T)                                                                                    \
     cb_sweeps_persistent<K, T><<<grid, T, persistent_smem(K, T), s>>>(packed, rows, (int)L, WR, W, row_to_slot, \
                                                                       thresh, rk, c0, np, stats, 4u, sync,    \
                                                                       (uint32_t)group, bands, scratch)
-#define PTMH_PERSIST_TB(K)                                                                                       \
-    cb_sweeps_persistent<K, 128, true><<<grid, 128, persistent_smem(K, 128), s>>>(                               \
+#define PTMH_PERSIST_TB(K, M)                                                                                    \
+    cb_sweeps_persistent<K, 128, M><<<grid, 128, persistent_smem(K, 128), s>>>(                                  \
         packed, rows, (int)L, WR, W, row_to_slot, thresh, rk, c0, np, stats, 4u, sync, (uint32_t)group, bands, \
         scratch)
-        if (tb) {
-            if (krows == 32) PTMH_PERSIST_TB(32);
-            else if (krows == 16) PTMH_PERSIST_TB(16);
-            else if (krows == 8) PTMH_PERSIST_TB(8);
-            else if (krows == 4) PTMH_PERSIST_TB(4);
-            else PTMH_PERSIST_TB(2);
+        // Beyond the blocked default's range (forced, e.g. C4) a blocked item
+        // streams through its band (colour 0 of block g, then colour 1 of
+        // block g - 1), so its working set stays small: C4's DRAM bytes per
+        // launch 1.45 -> 1.17x the algorithmic ones (ncu); within the range
+        // the band-at-once items measure 1.5 % faster (1024^2 x 16).
+        if (stream && krows == 32) PTMH_PERSIST_TB(32, 2);
+        else if (stream) PTMH_PERSIST_TB(16, 2);
+        else if (tb) {
+            if (krows == 32) PTMH_PERSIST_TB(32, 1);
+            else if (krows == 16) PTMH_PERSIST_TB(16, 1);
+            else if (krows == 8) PTMH_PERSIST_TB(8, 1);
+            else if (krows == 4) PTMH_PERSIST_TB(4, 1);
+            else PTMH_PERSIST_TB(2, 1);
         } else if (t128) {
             if (krows == 32) PTMH_PERSIST(32, 128);
             else if (krows == 16) PTMH_PERSIST(16, 128);

@@ -34,9 +34,7 @@ __device__ __forceinline__ uint32_t ld_other(const uint32_t* p) {
 // while the item runs, and the item's acquire invalidated L1 after their
 // last readers elsewhere
 __device__ __forceinline__ uint32_t ld_cta(const uint32_t* p) {
-    uint32_t v;  // (explicit: a const __restrict__ pointer would be turned into the .nc path)
-    asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
+    return __ldca(p);  // (explicit: a const __restrict__ pointer would be turned into the .nc path)
 }
 template <bool kNC, int kTB>
 __device__ __forceinline__ uint32_t ld_oth(const uint32_t* p) {

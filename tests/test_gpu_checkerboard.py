@@ -515,6 +515,9 @@ def test_persistent_sweeps_equal_per_launch_path(mods, monkeypatch, L, R, first,
             # temporally blocked items: 128-thread items that span whole rows (L <= 8192)
             spans = launch["threads"] == 128 and 128 % (L // 64) == 0
             assert launch["tb"] == (spans and (tb == "1" or (tb is None and R * L * L <= 1 << 25)))
+            # beyond 2^25 sites (16- / 32-row items) the blocked items stream through their band
+            streamed = launch["tb"] and R * L * L > 1 << 25 and launch["rows"] in (16, 32)
+            assert launch["streamed"] == streamed
         eng.sweeps(first + nsweeps, 1)  # a second call reuses the (re-zeroed) sync block
         torch.cuda.synchronize()
         if persistent:

@@ -12,6 +12,9 @@ ncu --set full --clock-control none --import-source on -k regex:cb_sweeps_persis
     -o gpurun_out/persist_c3 -f python tools/prof_sweep.py c3 10 > gpurun_out/ncu_full.log 2>&1
 ncu --set full --clock-control none -k regex:cb_sweeps_persistent -c 1 \
     -o gpurun_out/persist_c4 -f python tools/prof_sweep.py c4 2 > /dev/null 2>&1
+# C4 with temporally blocked items forced on (streamed through each band): DRAM bytes vs the default
+PTMH_PERSIST_TB=1 ncu --set full --clock-control none -k regex:cb_sweeps_persistent -c 1 \
+    -o gpurun_out/persist_c4_tbs -f python tools/prof_sweep.py c4 2 > /dev/null 2>&1
 # a rank's C3 shard at 8 GPUs: the temporally blocked persistent launch
 ncu --set full --clock-control none --import-source on -k regex:cb_sweeps_persistent -c 1 \
     -o gpurun_out/persist_shard32 -f python tools/prof_sweep.py 1024,32 10 > /dev/null 2>&1

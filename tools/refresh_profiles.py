@@ -97,6 +97,21 @@ for c, rep, L, R, kern in (("c5", "res_c5", 64, 4096, "cb_resident_reg64_kernel<
             "issue": dict(issue(k, R * L * L * 20 / 32),
                           note="latency-bound: few words per thread per colour phase, cluster / round waits")}
 summ("persist_shard32", "ncu_full_persistent_shard32_tb")
+# C4 with the temporally blocked items forced on (PTMH_PERSIST_TB=1: streamed through each band)
+if os.path.exists(os.path.join(G, "persist_c4_tbs.ncu-rep")):
+    kt = summ("persist_c4_tbs", "ncu_full_persistent_c4_tb_streamed")
+    alg = 2 * 512 * 4096 * 4096 * 0.25
+    d["c4_tb_streamed"] = {
+        "source": f"profiles/{RND}_ncu_full_persistent_c4_tb_streamed.json (PTMH_PERSIST_TB=1: "
+                  "cb_sweeps_persistent<32,128,2>, one launch of 2 sweeps of 512 x 4096^2)",
+        "dram_bytes_per_launch_2_sweeps": kt["dram_read"] + kt["dram_write"],
+        "algorithmic_bytes_2_sweeps": alg,
+        "ratio": round((kt["dram_read"] + kt["dram_write"]) / alg, 3),
+        "ratio_default_path": round((k4["dram_read"] + k4["dram_write"]) / alg, 3),
+        "issue": issue(kt, 512 * 4096 * 4096 * 2 / 32),
+        "note": "a sweep of a band per item, streamed (colour 0 of block g, then colour 1 of block g-1): "
+                "DRAM near the algorithmic bytes, but ~9 % more instructions per word (out-of-place stores, "
+                "halo rows) than the per-colour default, which stays faster at C4"}
 json.dump(d, open(os.path.join(P, "ncu_sweep_summary.json"), "w"), indent=1)
 with open(os.path.join(P, f"{RND}_sanitizer.txt"), "w") as f:
     f.write("# compute-sanitizer over tools/sanitize_paths.py (round 2, final build, one B200)\n")
