@@ -317,8 +317,13 @@ __device__ __forceinline__ uint32_t ferro_word0(const uint32_t* __restrict__ in,
 // (band dependencies, below) or the shard is big, else 256 (the launcher).
 // tb: temporally blocked items (a separate instantiation: carrying both
 // item kinds in one kernel doubled its code and cost the per-colour path 2 %)
+// streamed blocked items (tb == 2): 4 CTAs per SM at up to 128 registers
+// (C4, blocked items forced: 6 / 5 / 4 / 3 CTAs 3.52 / 3.60 / 3.64 / 3.26e12)
+#ifndef PTMH_TB2_MINB
+#define PTMH_TB2_MINB 4
+#endif
 template <int kRows, int kPT, int tb = 0>
-__global__ void __launch_bounds__(kPT, PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_persistent(
+__global__ void __launch_bounds__(kPT, tb == 2 ? PTMH_TB2_MINB : PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_persistent(
     uint32_t* __restrict__ packed, int64_t rows, int L, int WR, int64_t W,
     const int32_t* __restrict__ row_to_slot, const uint32_t* __restrict__ thresh, const RoundKeys32 rk,
     uint32_t ctr_base, uint32_t n_phases, int64_t* __restrict__ stats, uint32_t esz,
@@ -866,6 +871,7 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
     if (sync && ferro && cb_sweeps_persistent_applies(L, always_mask, n_sweeps) &&
         2 * n_sweeps * rows * (L * L / 16384) < (1LL << 31)) {  // item count at 2 rows, 128 threads
         static int cached_slots[256][2] = {};  // resident CTAs per device, [0]: 256-, [1]: 128-thread CTAs
+        static int cached_stream_slots[256] = {};  // ... of the streamed blocked kernel (tb == 2)
         int dev = 0;
         PTMH_CUDA(cudaGetDevice(&dev));
         if (dev >= 256) dev = 255;
@@ -907,6 +913,12 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
                 PTMH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cb_sweeps_persistent<16, 256>, 256,
                                                                         persistent_smem(16, 256)));
             cached_slots[dev][t128] = sms * std::max(occ, 1);
+            if (t128) {
+                int occ2 = 0;
+                PTMH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, cb_sweeps_persistent<32, 128, 2>, 128,
+                                                                        persistent_smem(32, 128)));
+                cached_stream_slots[dev] = sms * std::max(occ2, 1);
+            }
         }
         const int64_t slots = cached_slots[dev][t128];
         const int WR = (int)(L / 64);
@@ -954,7 +966,7 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
                rows * blocks / (group * 2) >= per_slot * slots)
             group *= 2;
         const int64_t items = 2 * n_sweeps * rows * (blocks / group);  // (tb: half as many, twice as long)
-        const unsigned grid = (unsigned)std::min<int64_t>(items, slots);
+        unsigned grid = (unsigned)std::min<int64_t>(items, slots);
         const uint32_t c0 = (uint32_t)(2 * first_sweep), np = (uint32_t)(2 * n_sweeps);
         // band dependencies pay where a phase has few items per CTA slot
         // (1024^2 x 128: 3.21 -> 3.25e12); at C3 size and above lattice-wide
@@ -977,6 +989,7 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
                         (etb ? etb[0] == '1' : rows * L * L <= (1LL << 25));
         const bool bands = tb || (kpt % WR == 0 && (eb ? eb[0] == '1' : rows * L * L < (1LL << 28)));
         const bool stream = tb && rows * L * L > (1LL << 25) && (krows == 32 || krows == 16);
+        if (stream) grid = (unsigned)std::min<int64_t>(items, cached_stream_slots[dev]);  // (fewer CTAs per SM)
         g_last_launch = CbLaunchInfo{1, krows, kpt, (int)group, tb ? (stream ? 3 : 2) : (bands ? 1 : 0), (int)grid};
         if (tb) PTMH_CUDA(cudaMemsetAsync(stats, 0, (size_t)rows * 2 * sizeof(int64_t), s));
 #define PTMH_PERSIST(K, T)                                                                                    \
@@ -990,8 +1003,9 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
         // Beyond the blocked default's range (forced, e.g. C4) a blocked item
         // streams through its band (colour 0 of block g, then colour 1 of
         // block g - 1), so its working set stays small: C4's DRAM bytes per
-        // launch 1.45 -> 1.17x the algorithmic ones (ncu); within the range
-        // the band-at-once items measure 1.5 % faster (1024^2 x 16).
+        // launch 1.45 -> 1.05x the algorithmic ones (ncu, 4 CTAs per SM);
+        // within the range the band-at-once items measure 1.5 % faster
+        // (1024^2 x 16).
         if (stream && krows == 32) PTMH_PERSIST_TB(32, 2);
         else if (stream) PTMH_PERSIST_TB(16, 2);
         else if (tb) {
