@@ -322,8 +322,17 @@ __device__ __forceinline__ uint32_t ferro_word0(const uint32_t* __restrict__ in,
 #ifndef PTMH_TB2_MINB
 #define PTMH_TB2_MINB 4
 #endif
+// band-at-once blocked items (tb == 1, small shards): 5 CTAs per SM at up to
+// 96 registers (6 CTAs at 80 rematerialised the base addresses in the row
+// loops): 1024^2 x 32 (a rank's C3 shard at 8 GPUs) 2.43 -> 2.49e12, 2048^2 x
+// 8 2.34 -> 2.41e12, 1024^2 x 16 1.95 -> 1.91e12 (4 CTAs: 2.38 / 2.30 / 1.72)
+#ifndef PTMH_TB1_MINB
+#define PTMH_TB1_MINB 5
+#endif
 template <int kRows, int kPT, int tb = 0>
-__global__ void __launch_bounds__(kPT, tb == 2 ? PTMH_TB2_MINB : PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_persistent(
+__global__ void __launch_bounds__(kPT, tb == 2   ? PTMH_TB2_MINB
+                                      : tb == 1 ? PTMH_TB1_MINB
+                                                : PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_persistent(
     uint32_t* __restrict__ packed, int64_t rows, int L, int WR, int64_t W,
     const int32_t* __restrict__ row_to_slot, const uint32_t* __restrict__ thresh, const RoundKeys32 rk,
     uint32_t ctr_base, uint32_t n_phases, int64_t* __restrict__ stats, uint32_t esz,
@@ -871,7 +880,7 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
     if (sync && ferro && cb_sweeps_persistent_applies(L, always_mask, n_sweeps) &&
         2 * n_sweeps * rows * (L * L / 16384) < (1LL << 31)) {  // item count at 2 rows, 128 threads
         static int cached_slots[256][2] = {};  // resident CTAs per device, [0]: 256-, [1]: 128-thread CTAs
-        static int cached_stream_slots[256] = {};  // ... of the streamed blocked kernel (tb == 2)
+        static int cached_tb_slots[256][2] = {};  // ... of the blocked kernels (tb == 1, 2)
         int dev = 0;
         PTMH_CUDA(cudaGetDevice(&dev));
         if (dev >= 256) dev = 255;
@@ -914,10 +923,13 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
                                                                         persistent_smem(16, 256)));
             cached_slots[dev][t128] = sms * std::max(occ, 1);
             if (t128) {
-                int occ2 = 0;
-                PTMH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, cb_sweeps_persistent<32, 128, 2>, 128,
+                int o1 = 0, o2 = 0;
+                PTMH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, cb_sweeps_persistent<16, 128, 1>, 128,
+                                                                        persistent_smem(16, 128)));
+                PTMH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, cb_sweeps_persistent<32, 128, 2>, 128,
                                                                         persistent_smem(32, 128)));
-                cached_stream_slots[dev] = sms * std::max(occ2, 1);
+                cached_tb_slots[dev][0] = sms * std::max(o1, 1);
+                cached_tb_slots[dev][1] = sms * std::max(o2, 1);
             }
         }
         const int64_t slots = cached_slots[dev][t128];
@@ -989,7 +1001,7 @@ int launch_cb_sweeps(uint32_t* packed, int64_t rows, int64_t L, const int32_t* r
                         (etb ? etb[0] == '1' : rows * L * L <= (1LL << 25));
         const bool bands = tb || (kpt % WR == 0 && (eb ? eb[0] == '1' : rows * L * L < (1LL << 28)));
         const bool stream = tb && rows * L * L > (1LL << 25) && (krows == 32 || krows == 16);
-        if (stream) grid = (unsigned)std::min<int64_t>(items, cached_stream_slots[dev]);  // (fewer CTAs per SM)
+        if (tb) grid = (unsigned)std::min<int64_t>(items, cached_tb_slots[dev][stream]);  // (their occupancy)
         g_last_launch = CbLaunchInfo{1, krows, kpt, (int)group, tb ? (stream ? 3 : 2) : (bands ? 1 : 0), (int)grid};
         if (tb) PTMH_CUDA(cudaMemsetAsync(stats, 0, (size_t)rows * 2 * sizeof(int64_t), s));
 #define PTMH_PERSIST(K, T)                                                                                    \
