@@ -317,6 +317,34 @@ __device__ __forceinline__ uint32_t ferro_word0(const uint32_t* __restrict__ in,
 // (band dependencies, below) or the shard is big, else 256 (the launcher).
 // tb: temporally blocked items (a separate instantiation: carrying both
 // item kinds in one kernel doubled its code and cost the per-colour path 2 %)
+// n / d for the blocked kernels' item decode (n < 2^31): a shift where d is a
+// power of two, else a multiply by m = ceil(2^32 / d), whose estimate is q or
+// q + 1 (n*m / 2^32 - n/d < n / 2^32 < 1/2), and one correction -- instead of
+// the ~20-instruction integer division every thread ran per item (a rank's
+// C3 shard 2.50 -> 2.53e12, 1024^2 x 24 1.93 -> 1.99e12; in the per-colour
+// kernels it measured 0.5-1 % slower: C3 / C4 keep the divisions)
+struct UDiv {
+    uint32_t d, m;
+    int sh;  // >= 0: d = 2^sh
+};
+__device__ __forceinline__ UDiv udiv_make(uint32_t d) {
+    UDiv u;
+    u.d = d;
+    u.sh = (d & (d - 1)) == 0 ? __ffs(d) - 1 : -1;
+    u.m = u.sh >= 0 ? 0u : (uint32_t)((0x100000000ull + d - 1) / d);
+    return u;
+}
+__device__ __forceinline__ uint32_t udiv(uint32_t n, const UDiv& u) {
+    if (u.sh >= 0) return n >> u.sh;
+    const uint32_t q = __umulhi(n, u.m);
+    return (int32_t)(n - q * u.d) < 0 ? q - 1 : q;
+}
+template <int tb>
+__device__ __forceinline__ uint32_t item_div(uint32_t n, uint32_t d, const UDiv& u) {
+    if constexpr (tb != 0) return udiv(n, u);
+    return n / d;
+}
+
 // streamed blocked items (tb == 2): 4 CTAs per SM at up to 128 registers
 // (C4, blocked items forced: 6 / 5 / 4 / 3 CTAs 3.52 / 3.60 / 3.64 / 3.26e12)
 #ifndef PTMH_TB2_MINB
@@ -354,6 +382,7 @@ __global__ void __launch_bounds__(kPT, tb == 2   ? PTMH_TB2_MINB
     // has >= 8 items per resident CTA)
     const uint32_t subs = (uint32_t)((L / kRows) * WR / kPT) / group;
     const uint32_t per_phase = (uint32_t)rows * subs;
+    const UDiv div_phase = udiv_make(per_phase), div_subs = udiv_make(subs);  // (blocked kernels)
     // tb: an item is a whole sweep of its band (both colours), so a "phase"
     // below counts sweeps and the dependency counters count sweeps done
     const uint32_t n_steps = tb ? n_phases / 2 : n_phases;
@@ -385,8 +414,8 @@ __global__ void __launch_bounds__(kPT, tb == 2   ? PTMH_TB2_MINB
     for (int it = 0;; ++it) {
         if (threadIdx.x == 0) {
             if (next < n_items) {
-                const uint32_t phase = next / per_phase;
-                const uint32_t lat = (next - phase * per_phase) / subs;
+                const uint32_t phase = item_div<tb>(next, per_phase, div_phase);
+                const uint32_t lat = item_div<tb>(next - phase * per_phase, subs, div_subs);
                 // the lattice's threshold planes, once per item instead of per
                 // thread (the loads overlap the dependency poll)
                 const int slot = row_to_slot[lat];
@@ -421,9 +450,9 @@ __global__ void __launch_bounds__(kPT, tb == 2   ? PTMH_TB2_MINB
         __syncthreads();
         const uint32_t item = s_item[it & 1];
         if (item >= n_items) break;
-        const uint32_t phase = item / per_phase;
+        const uint32_t phase = item_div<tb>(item, per_phase, div_phase);
         const uint32_t r = item - phase * per_phase;
-        const uint32_t lat = r / subs, sub = r - lat * subs;
+        const uint32_t lat = item_div<tb>(r, subs, div_subs), sub = r - lat * subs;
         int sumS = 0, sumB = 0;
         if constexpr (tb) {
             // ---- temporally blocked item: sweep `phase` of band `sub`, out of
