@@ -121,9 +121,10 @@ __device__ __forceinline__ void reg64_pass(uint32_t (&C)[2][2], const uint32_t (
 // and thresholds for the next sweep.
 // local: the ring is in the CTA's shared memory (every lattice of the run in
 // one CTA), so the round word is a volatile shared store / poll.
-// pre: the round's partner-independent inputs if loaded already (RoundIn::
-// load), or null to load them here (loading them before the sweep, held in
-// registers across it, measured slower at C5: 6.55 -> 6.80 us).
+// The round's partner-independent inputs, loaded after the publish so that
+// their latency overlaps the partner's word in flight (loading them before
+// the sweep, held in registers across it, measured slower at C5: 6.55 ->
+// 6.80 us).
 struct RoundIn {
     double u, bi, bj;
     uint32_t ot3, ot4;
@@ -141,8 +142,7 @@ struct RoundIn {
 
 __device__ __forceinline__ void reg_round(const ResidentArgs& A, uint64_t* ring, int R, bool multi, bool local,
                                           int row, int64_t round, int64_t col, bool rec, bool exch, bool last, int k,
-                                          int64_t S, int64_t Bd, int& nk, uint32_t& n3, uint32_t& n4,
-                                          const RoundIn* pre = nullptr) {
+                                          int64_t S, int64_t Bd, int& nk, uint32_t& n3, uint32_t& n4) {
     static_assert((kRing & (kRing - 1)) == 0, "ring depth: a power of two");
     uint64_t* const slot_word = ring + (round & (kRing - 1)) * (int64_t)R;
     if (exch) {  // first: the partner is waiting for it
@@ -170,7 +170,7 @@ __device__ __forceinline__ void reg_round(const ResidentArgs& A, uint64_t* ring,
         // everything that does not need the partner's energy, while its word travels
         const int p = (k - first) / 2, i = first + 2 * p, other = k == i ? i + 1 : i;
         RoundIn in;
-        if (pre) in = *pre; else in.load(A, R, round, k);
+        in.load(A, R, round, k);
         const double u = in.u, bi = in.bi, bj = in.bj;
         const uint32_t ot3 = in.ot3, ot4 = in.ot4;
         const uint64_t want = (uint64_t)((round & 0x7fff) | 0x8000);
