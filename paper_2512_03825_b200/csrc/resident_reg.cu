@@ -115,12 +115,6 @@ __device__ __forceinline__ void reg64_pass(uint32_t (&C)[2][2], const uint32_t (
     }
 }
 
-// Lane 0 of a warp that owns a lattice, after a sweep whose (S, Bond) it
-// holds: the final stats, the observables by slot and the point-to-point
-// round (resident.cu, rounds.cuh); nk / n3 / n4 receive the lattice's slot
-// and thresholds for the next sweep.
-// local: the ring is in the CTA's shared memory (every lattice of the run in
-// one CTA), so the round word is a volatile shared store / poll.
 // The round's partner-independent inputs, loaded after the publish so that
 // their latency overlaps the partner's word in flight (loading them before
 // the sweep, held in registers across it, measured slower at C5: 6.55 ->
@@ -140,6 +134,12 @@ struct RoundIn {
     }
 };
 
+// Lane 0 of a warp that owns a lattice, after a sweep whose (S, Bond) it
+// holds: the final stats, the observables by slot and the point-to-point
+// round (resident.cu, rounds.cuh); nk / n3 / n4 receive the lattice's slot
+// and thresholds for the next sweep.
+// local: the ring is in the CTA's shared memory (every lattice of the run in
+// one CTA), so the round word is a volatile shared store / poll.
 __device__ __forceinline__ void reg_round(const ResidentArgs& A, uint64_t* ring, int R, bool multi, bool local,
                                           int row, int64_t round, int64_t col, bool rec, bool exch, bool last, int k,
                                           int64_t S, int64_t Bd, int& nk, uint32_t& n3, uint32_t& n4) {
