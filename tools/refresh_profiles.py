@@ -90,7 +90,7 @@ d["c4"].update({"dram_bytes_per_launch": 5 * (k4["dram_read"] + k4["dram_write"]
                               note="bound by ALU + FMA-heavy pipe issue, not HBM")})
 # the resident kernels: 20 sweeps with a round every sweep (issue figures only; the state is L2-resident)
 for c, rep, L, R, kern in (("c5", "res_c5", 64, 4096, "cb_resident_reg64_kernel<1024>"),
-                           ("c2", "res_c2", 256, 64, "cb_cluster_smem_kernel<2, 256>")):
+                           ("c2", "res_c2", 256, 64, "cb_cluster_smem_kernel<1, 512>")):
     k = summ(rep, f"ncu_full_res_{c}")
     d[c] = {"source": f"profiles/{RND}_ncu_full_res_{c}.json (ncu --set full, one resident launch of 20 sweeps "
                       "with a round every sweep)", "kernels": [kern],
