@@ -314,6 +314,30 @@ def test_cluster_smem_kernel_matches_oracle(mods, monkeypatch, L, R, sweeps, eve
         (ref.swap_rounds, ref.swaps_attempted, ref.swaps_accepted)
 
 
+@pytest.mark.parametrize("rows1,pre,expect", [("1", "1", (1, 512)), ("0", "1", (2, 256)), ("0", "0", (2, 256))])
+def test_c2_shape_kernel_variants_match_oracle(mods, monkeypatch, rows1, pre, expect):
+    """C2's shape (256^2 x 64, a round every sweep) on the launcher's choice
+    (1-row strips on 512 threads, random planes drawn ahead of each pass and,
+    across a round, for both slots the lattice may hold), on 2-row strips,
+    and with the planes drawn inside the passes: all equal to the oracle."""
+    monkeypatch.setenv("PTMH_SMEM_ROWS1", rows1)
+    monkeypatch.setenv("PTMH_SMEM_PRE", pre)
+    p = mods[0]
+    from paper_2512_03825_b200 import _lib
+    L, R, sweeps, seed = 256, 64, 5, 4242
+    rec = p.run(p.SimulationConfig(side=L, replicas=R, iterations=sweeps * L * L, swap_interval=L * L, seed=seed,
+                                   sweep_mode="checkerboard", record_every=1, return_final_state=True,
+                                   kernel="resident"))
+    assert rec.valid, rec.error
+    launch = _lib.cb_last_launch()
+    assert launch["kind"] == 8 and (launch["rows"], launch["threads"]) == expect and launch["group"] == 2
+    ref = oracle.run_checkerboard(L, R, sweeps, 1, seed, record_every=1)
+    assert np.array_equal(rec.final_spins, ref.final_spins)
+    assert np.array_equal(rec.slot_to_row, ref.slot_to_row)
+    assert np.array_equal(rec.energies, ref.energies)
+    assert rec.swaps_accepted == ref.swaps_accepted
+
+
 @pytest.mark.parametrize("R,sweeps,every,rec_every,J", [
     (4096, 6, 1, 2, 1.0),   # C5's shape
     (333, 9, 1, 3, 1.0),    # ragged lattices per CTA
