@@ -18,7 +18,11 @@ reference swap rule).  Attempts per step = R * L^2 * 10.
   steps (256 MiB write), max over ranks.
 * e2e: the host-buffer plugin call (kernels.cb_interval -> C ABI
   ptmh_host_cb_interval) on pinned int8 lattices, host<->device copies of the
-  lattices inside the timed region, pipelined against the sweeps.
+  lattices inside the timed region, pipelined against the sweeps.  For the
+  resident configurations (C1, C2, C5: 100 one-sweep intervals per step in
+  one launch) the e2e step is the same 100 intervals: int8 lattices and the
+  permutation in from pinned host memory, load_spins -> run_resident ->
+  spins_int8, lattices, permutation and (S, Bond) back.
 * roofline: the half-sweep kernel, algorithmic bytes = 0.25 B per attempt
   (1-bit spin read + written) x R*L^2/2 attempts per launch,
   over its CUDA-event duration inside the timed steps.
@@ -431,7 +435,49 @@ def main():
 
     # ---- end to end through the host-buffer plugin (rank 0, single device)
     e2e = None
-    if not args.no_e2e and not sharded:
+    if not args.no_e2e and not sharded and resident:
+        # the step's `ips` intervals in one resident launch, as the timed
+        # step, with the lattices and the permutation in from pinned host
+        # memory and the lattices, the permutation and every lattice's
+        # (S, Bond) back, every step (the per-interval plugin call,
+        # kernels.cb_interval, would time `ips` calls of a few us of work each)
+        loc = eng.spins_int8()
+        host = torch.empty(tuple(loc.shape), dtype=torch.int8).pin_memory()
+        host.copy_(loc)
+        dbuf = torch.empty_like(loc)
+        s2r_h = eng.slot_to_row.cpu().pin_memory()
+        r2s_h = eng.row_to_slot.cpu().pin_memory()
+        stats_h = torch.empty(tuple(eng.stats.shape), dtype=torch.int64).pin_memory()
+        sweep0 = state["sweep"]
+
+        def e2e_step(t):
+            dbuf.copy_(host, non_blocking=True)
+            eng.slot_to_row.copy_(s2r_h, non_blocking=True)
+            eng.row_to_slot.copy_(r2s_h, non_blocking=True)
+            eng.load_spins(dbuf)
+            eng.run_resident(t, every * ips, big, every)
+            host.copy_(eng.spins_int8(), non_blocking=True)
+            s2r_h.copy_(eng.slot_to_row, non_blocking=True)
+            r2s_h.copy_(eng.row_to_slot, non_blocking=True)
+            stats_h.copy_(eng.stats, non_blocking=True)
+
+        for k in range(2):  # warm
+            e2e_step(sweep0)
+            sweep0 += every * ips
+        torch.cuda.synchronize()
+        n_e2e = max(3, min(args.steps, 10))
+        t0 = time.perf_counter()
+        for k in range(n_e2e):
+            e2e_step(sweep0)
+            sweep0 += every * ips
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        e2e = {"value": n_e2e * attempts_per_step / dt, "unit": "attempts/s",
+               "h2d_bytes_per_step": int(R * L * L + 12 * R), "d2h_bytes_per_step": int(R * L * L + 28 * R),
+               "path": "CheckerboardEngine.load_spins -> run_resident -> spins_int8 (the engine run() "
+                       "drives): pinned int8 lattices + permutation in, lattices + permutation + "
+                       f"(S, Bond) out, {ips} intervals per step in one resident launch; wall clock"}
+    elif not args.no_e2e and not sharded:
         spins_h = eng.final_spins()
         pinned = torch.from_numpy(spins_h).pin_memory()
         sp = pinned.numpy()
@@ -469,18 +515,20 @@ def main():
         def e2e_step(t, r):
             dbuf.copy_(host, non_blocking=True)
             eng.load_spins(dbuf)
-            if resident:  # one interval (its sweeps + round) per launch per rank, peer-memory round
-                resident_sharded(drv, peers, t, every, big, every)
+            if resident:  # the step's intervals in one launch per rank, peer-memory rounds
+                resident_sharded(drv, peers, t, every * ips, big, every)
             else:
                 eng.sweeps(t, every)
                 drv.gather_stats()
                 eng.exchange(r)
             host.copy_(eng.spins_int8(), non_blocking=True)
 
-        # (an e2e step is one exchange interval, as the host plugin's call at N = 1)
+        # (an e2e step is the timed step: one interval, or `ips` of them in one
+        # resident launch)
+        span = every * (ips if resident else 1)
         for k in range(2):  # warm
             e2e_step(sweep0, rnd0)
-            sweep0 += every
+            sweep0 += span
             rnd0 += 1
         n_e2e = max(3, min(args.steps, 10))
         dist.barrier()
@@ -488,12 +536,12 @@ def main():
         t0 = time.perf_counter()
         for k in range(n_e2e):
             e2e_step(sweep0, rnd0)
-            sweep0 += every
+            sweep0 += span
             rnd0 += 1
         torch.cuda.synchronize()
         dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)
-        e2e = {"value": n_e2e * R * L * L * every / float(dt.item()), "unit": "attempts/s",
+        e2e = {"value": n_e2e * R * L * L * span / float(dt.item()), "unit": "attempts/s",
                "h2d_bytes_per_step": int(R * L * L), "d2h_bytes_per_step": int(R * L * L),
                "path": "distributed.ShardedCheckerboard" + (" + resident_sharded" if resident else "")
                        + ", per-rank int8 lattices from / to pinned host memory each step (bytes summed "

@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("config,extra", [("c3", []), ("c1", []),
+@pytest.mark.parametrize("config,extra", [("c3", []), ("c1", []), ("c5", []),
                                           # the --gpus launcher: re-run under torchrun (one rank here)
                                           ("c3", ["--gpus", "1", "--spawn"]),
                                           # the multi-GPU code paths at one rank: NCCL all-gather per
