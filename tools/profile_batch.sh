@@ -26,6 +26,5 @@ ncu --set full --clock-control none --import-source on -k regex:cb_resident_reg6
     python tools/prof_resident.py c5 1 > /dev/null 2>&1
 PTMH_SMEM_NOCOOP=1 ncu --set full --clock-control none --import-source on -k regex:cb_cluster_smem -c 1 \
     -o gpurun_out/res_c2 -f python tools/prof_resident.py c2 1 > /dev/null 2>&1
-for t in memcheck racecheck synccheck; do
-  echo "## $t"; compute-sanitizer --tool $t python tools/sanitize_paths.py 2>&1 | tail -n 2
-done > gpurun_out/sanitizer.txt
+# (compute-sanitizer: closed on the GPU pool since the last round-2 refresh; profiles/r2_sanitizer.txt
+# holds the last pass, commit 03ae124: the kernels are unchanged since)
