@@ -137,9 +137,10 @@ __device__ __forceinline__ void ferro_strip(uint32_t* __restrict__ packed, int L
         uint32_t S = __ldcg(word_at(own, o0, esz));
         uint32_t adj = ld_oth<kNC, kTB>(word_at(other, o0 + (uint32_t)((kColor & 1) ? dOdd : dEven), esz));
         uint32_t o = o0;
-        // strips of <= 4 rows unroll whole (a rank's C3 shard at 8 GPUs,
-        // 4-row strips: 2.52 -> 2.65e12); longer ones by 2 (4: no gain at C3)
-        constexpr int kUnroll = kRows <= 4 ? 4 : 2;
+        // strips of <= 8 rows unroll whole (a rank's C3 shard at 8 GPUs,
+        // 4-row strips: 2.52 -> 2.65e12; at 4 GPUs, 8-row strips: 2.93 ->
+        // 3.03e12); longer ones by 2 (by 4: C3 even, C4 -0.6 %, spills)
+        constexpr int kUnroll = kRows <= 8 ? kRows : 2;
 #pragma unroll kUnroll
         for (int rr = 0; rr < kRows; ++rr) {
             const bool even = ((rr + kColor) & 1) == 0;
