@@ -449,6 +449,42 @@ def test_resident_segments_compose(mods):
         assert np.array_equal(o[3], outs[0][3])
 
 
+@pytest.mark.parametrize("L,R,ladder", [(32, 8, "geometric"), (256, 64, "linear"), (64, 4096, "linear")])
+def test_bench_e2e_round_trip_is_the_same_run(mods, L, R, ladder):
+    """bench.py's e2e step for the resident configurations (C1, C2, C5):
+    lattices and permutation to pinned host memory and back between
+    resident segments (load_spins -> run_resident -> spins_int8) gives the
+    run that never leaves the device."""
+    p, engine, _, _ = mods
+    temps = p.geometric_ladder(R) if ladder == "geometric" else p.build_ladder(R)
+    big, every, seg, nseg = 1 << 30, 1, 20, 3
+    ref = engine.CheckerboardEngine(L, R, temps, 42, 1.0, 0.0, 0.5, 0)
+    ref.init_state()
+    ref.run_resident(0, seg * nseg, big, every)
+    eng = engine.CheckerboardEngine(L, R, temps, 42, 1.0, 0.0, 0.5, 0)
+    eng.init_state()
+    host = torch.empty((R, L, L), dtype=torch.int8).pin_memory()
+    host.copy_(eng.spins_int8())
+    s2r_h = eng.slot_to_row.cpu().pin_memory()
+    r2s_h = eng.row_to_slot.cpu().pin_memory()
+    dbuf = torch.empty((R, L, L), dtype=torch.int8, device="cuda")
+    for k in range(nseg):
+        dbuf.copy_(host, non_blocking=True)
+        eng.slot_to_row.copy_(s2r_h, non_blocking=True)
+        eng.row_to_slot.copy_(r2s_h, non_blocking=True)
+        eng.load_spins(dbuf)
+        eng.run_resident(k * seg, seg, big, every)
+        host.copy_(eng.spins_int8(), non_blocking=True)
+        s2r_h.copy_(eng.slot_to_row, non_blocking=True)
+        r2s_h.copy_(eng.row_to_slot, non_blocking=True)
+    torch.cuda.synchronize()
+    assert np.array_equal(host.numpy(), ref.final_spins())
+    assert np.array_equal(s2r_h.numpy(), ref.slot_to_row.cpu().numpy())
+    assert np.array_equal(r2s_h.numpy(), ref.row_to_slot.cpu().numpy())
+    assert np.array_equal(eng.stats.cpu().numpy(), ref.stats.cpu().numpy())
+    assert eng.swap_counts() == ref.swap_counts()
+
+
 def test_sweeps_match_oracle_at_2048(mods):
     """L >= 1024 takes the 16-rows-per-thread fast-path instantiation (also at 2048)."""
     p, engine, _, _ = mods
