@@ -357,9 +357,16 @@ __device__ __forceinline__ uint32_t item_div(uint32_t n, uint32_t d, const UDiv&
 #ifndef PTMH_TB1_MINB
 #define PTMH_TB1_MINB 5
 #endif
+// Per-colour items of 128 threads: 5 CTAs per SM (96 registers; 6 at 80:
+// C3 3.44 -> 3.49e12, 1024^2 x 128 3.24 -> 3.32e12, C4 +0.3 %, 1024^2 x 64
+// -0.4 %; 4 at 128: -11 %)
+#ifndef PTMH_PERSIST128_MINB
+#define PTMH_PERSIST128_MINB 5
+#endif
 template <int kRows, int kPT, int tb = 0>
 __global__ void __launch_bounds__(kPT, tb == 2   ? PTMH_TB2_MINB
                                       : tb == 1 ? PTMH_TB1_MINB
+                                      : kPT == 128 ? PTMH_PERSIST128_MINB
                                                 : PTMH_FERRO_MINB * 256 / kPT) cb_sweeps_persistent(
     uint32_t* __restrict__ packed, int64_t rows, int L, int WR, int64_t W,
     const int32_t* __restrict__ row_to_slot, const uint32_t* __restrict__ thresh, const RoundKeys32 rk,
