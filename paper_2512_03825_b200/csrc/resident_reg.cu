@@ -92,7 +92,8 @@ __device__ __forceinline__ void reg64_pass(uint32_t (&C)[2][2], const uint32_t (
         }
     }
     // ties (top byte equal): each lane walks its own; the warp iterates
-    // max-ties-per-lane times
+    // max-ties-per-lane times.  sec24 < t24 <=> word 0 < t24 << 8
+    const uint32_t T3s = t3 << 8, T4s = t4 << 8;
     while (__any_sync(kAll, (eqm[0] | eqm[1]) != 0)) {
         const int rr = eqm[0] ? 0 : 1;
         const uint32_t m = rr ? eqm[1] : eqm[0];
@@ -100,10 +101,9 @@ __device__ __forceinline__ void reg64_pass(uint32_t (&C)[2][2], const uint32_t (
             const int bit = __ffs(m) - 1;
             if (rr) eqm[1] &= eqm[1] - 1; else eqm[0] &= eqm[0] - 1;
             const uint32_t k4 = ((rr ? k4m[1] : k4m[0]) >> bit) & 1u;
-            const uint32_t t24 = (k4 ? t4 : t3) & 0x00ffffffu;
             const uint32_t w32 = (uint32_t)(2 * lane + rr);
             const uint4 r2 = philox4x32_10(make_uint4(w32 * 32u + (uint32_t)bit, ctr1, slot, 1u), rk);
-            if ((r2.x >> 8) < t24) {
+            if (r2.x < (k4 ? T4s : T3s)) {
                 const uint32_t Sw = rr ? C[kColor][1] : C[kColor][0];
                 if (kStats) {
                     sumS += ((Sw >> bit) & 1u) ? -2 : 2;
@@ -365,9 +365,8 @@ __device__ __forceinline__ void reg32_pass(uint32_t (&C)[2], const uint32_t (&TM
             const int bit = __ffs(eq) - 1;
             eq &= eq - 1;
             const uint32_t k4 = (K4 >> bit) & 1u;
-            const uint32_t t24 = (k4 ? t4 : t3) & 0x00ffffffu;
             const uint4 r2 = philox4x32_10(make_uint4(w32 * 32u + (uint32_t)bit, ctr1, slot, 1u), rk);
-            if ((r2.x >> 8) < t24) {
+            if (r2.x < ((k4 ? t4 : t3) << 8)) {  // sec24 < t24 <=> word 0 < t24 << 8
                 if (kStats) {
                     sumS += ((Sn >> bit) & 1u) ? -2 : 2;
                     sumB += k4 ? -8 : -4;

@@ -108,9 +108,8 @@ __device__ __forceinline__ void smem_ties(uint32_t* __restrict__ own, int s, int
             const int bit = __ffs(m) - 1;
             m &= m - 1;
             const uint32_t k4 = (mk4 >> bit) & 1u;
-            const uint32_t t24 = (k4 ? t4 : t3) & 0x00ffffffu;
             const uint4 r2 = philox4x32_10(make_uint4(w32 * 32u + (uint32_t)bit, ctr1, slot, 1u), rk);
-            if ((r2.x >> 8) < t24) {
+            if (r2.x < ((k4 ? t4 : t3) << 8)) {  // sec24 < t24 <=> word 0 < t24 << 8
                 if (kStats) {
                     sumS += ((Sw >> bit) & 1u) ? -2 : 2;
                     sumB += k4 ? -8 : -4;

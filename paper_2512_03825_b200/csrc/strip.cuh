@@ -204,6 +204,8 @@ __device__ __forceinline__ void ferro_strip(uint32_t* __restrict__ packed, int L
     {
         int rr = -1;
         uint32_t m = 0, mk4 = 0, Sw = 0, w32 = 0;
+        // sec24 < t24  <=>  word 0 < t24 << 8 (t << 8 drops the top byte)
+        const uint32_t T3s = t3 << 8, T4s = t4 << 8;
         bool dirty = false;
         while (__any_sync(strip::kFull, tie_rows != 0 || m != 0)) {
             if (m == 0 && tie_rows != 0) {
@@ -221,10 +223,9 @@ __device__ __forceinline__ void ferro_strip(uint32_t* __restrict__ packed, int L
                 const int bit = __ffs(m) - 1;
                 m &= m - 1;
                 const uint32_t k4 = (mk4 >> bit) & 1u;
-                const uint32_t t24 = (k4 ? t4 : t3) & 0x00ffffffu;
                 const uint4 r2 =
                     philox4x32_10(make_uint4(w32 * 32u + (uint32_t)bit, ctr1, (uint32_t)slot, 1u), rk);
-                if ((r2.x >> 8) < t24) {
+                if (r2.x < (k4 ? T4s : T3s)) {
                     if (kColor == 1 && kStats) {
                         sumS += ((Sw >> bit) & 1u) ? -2 : 2;
                         sumB += k4 ? -8 : -4;
